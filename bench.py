@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""BP3 benchmark: PA-diffusion + Jacobi-PCG throughput on B200.
+
+metric  "BP3 PA-diffusion CG GDOF/s (p=3) at 1/2/4/8 B200; HBM GB/s vs roofline"
+        (BASELINE.json).  GDOF/s = DOFs x CG iterations / time.
+workload (N=1) configs[1]: BP3, p = 3, ~10M DOFs on one B200.  2D (the
+        reference's dimension: make_cartesian(1054, 1054) -> 10,004,569 DOFs,
+        q = p+2 Gauss-Legendre, kappa = 1, Dirichlet on the whole boundary),
+        one step = one cg_solve of a fixed 200 iterations (
+        rel_tol = 0 so max_iters is reached), rhs seeded U(-1, 1).
+value   device-resident: b, diag, x in HBM when the timed region starts;
+        CUDA events on the library's stream, max over ranks.
+e2e     the same solve through the C ABI with HOST buffers
+        (tfem_cg_solve_host: b and diag copied in, x copied out every step).
+roofline  dominant kernel = the PA operator application (element kernel +
+        shared-DOF scatter, one tfem_operator_mult): algorithmic bytes
+        B_op = E (nc q^2 8 + D1^2 4) + 16 N / event-timed
+        launch duration, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the reference itself (oracle/_ref, all host threads) on a
+        bounded sample (a few CG iterations of the same problem).
+
+--impl reference: times the reference's own CPU cg_solve on the host cores
+(rank 0 only), same metric / config, a few iterations per step.
+N > 1 (torchrun): the mesh is partitioned by element rows across ranks
+(weak scaling: ~10M DOFs per rank); see paper_1911_09220_b200/dist.py.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "BP3 PA-diffusion CG GDOF/s (p=3) at 1/2/4/8 B200; HBM GB/s vs roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tfem", choices=["tfem", "reference"])
+    ap.add_argument("--dim", type=int, default=2)
+    ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--n", type=int, default=0, help="cells per axis (0: ~10M DOFs)")
+    ap.add_argument("--iters", type=int, default=200)
+    ap.add_argument("--numerics", default="reference", choices=["reference", "fma"])
+    ap.add_argument("--cpu-iters", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def default_n(dim, p):
+    # ~10M DOFs: (n p + 1)^dim
+    return {2: round((10.0e6 ** 0.5 - 1) / p), 3: round((10.0e6 ** (1 / 3) - 1) / p)}[dim]
+
+
+def workload(args):
+    n = args.n or default_n(args.dim, args.order)
+    p = args.order
+    ndofs = (n * p + 1) ** args.dim
+    ne = n ** args.dim
+    return n, p, ndofs, ne
+
+
+class Clocks:
+    """nvidia-smi sampling during a timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.file = None
+
+    def __enter__(self):
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.file, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        try:
+            for line in open(self.file.name):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 8:
+                    continue
+                try:
+                    sm.append(float(f[0]))
+                    mx.append(float(f[1]))
+                except ValueError:
+                    continue
+                for name, v in zip(names, f[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(name)
+        finally:
+            os.unlink(self.file.name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_from_profile(key):
+    f = ROOT / "profiles" / "traffic.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text()).get(key)
+        except Exception:
+            return None
+    return None
+
+
+# ------------------------------------------------------------ reference arm
+def reference_problem(n, p, threads):
+    from oracle.pyoracle import RefForm, RefSpace, RefSystem
+    rs = RefSpace.cartesian(n, n, p)
+    f = RefForm(rs, [("diffusion", "const", 1.0)], threads=threads)
+    sys_ = RefSystem(f, "front")
+    b = np.random.default_rng(2020).uniform(-1.0, 1.0, rs.n_dofs)
+    b[sys_.ess] = 0.0
+    return rs, f, sys_, b
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_reference(n, p, iters, steps=1, warmup=0):
+    """GDOF/s of the reference cg_solve (Jacobi) on this host; falls back to
+    the C restatement when oracle/_ref is absent."""
+    threads = host_threads()
+    from oracle.pyoracle import Ref
+    if Ref.available():
+        rs, f, sys_, b = reference_problem(n, p, threads)
+        kind = "reference"
+        run = lambda: sys_.cg(0.0, iters, True, rhs=b)[3]
+        ndofs = rs.n_dofs
+    else:
+        from oracle.pyoracle import OrcCartesian
+        oc = OrcCartesian(2, (n, n), p)
+        qd = oc.setup("diffusion")
+        ess = oc.boundary_dofs()
+        op = oc.operator(["diffusion"], [qd], ess)
+        d = oc.diagonal("diffusion", qd)
+        d[ess] = 1.0
+        b = np.random.default_rng(2020).uniform(-1.0, 1.0, oc.ndofs)
+        b[ess] = 0.0
+        kind, threads, ndofs = "port", 1, oc.ndofs
+
+        def run():
+            t0 = time.perf_counter()
+            oc.cg(op, b, 0.0, iters, d)
+            return time.perf_counter() - t0
+    for _ in range(warmup):
+        run()
+    secs = [run() for _ in range(steps)]
+    return ndofs, secs, threads, kind
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    if args.dim != 2:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "the reference supports 2D quadrilaterals only"}))
+        return
+    n, p, _, _ = workload(args)
+    ndofs, secs, threads, kind = cpu_reference(n, p, args.cpu_iters, args.steps, args.warmup)
+    t = sum(secs)
+    value = ndofs * args.cpu_iters * args.steps / t / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args, n, p, ndofs, per_step_iters=args.cpu_iters),
+        "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": threads, "kind": kind,
+                         "sample": f"{args.cpu_iters} Jacobi-CG iterations per step on the "
+                                   f"same {ndofs}-DOF problem"},
+        "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+
+
+def config_of(args, n, p, ndofs, per_step_iters=None, world=1):
+    it = per_step_iters if per_step_iters is not None else args.iters
+    dim = args.dim
+    return {
+        "workload": f"BP3 {dim}D p={p} n={n}^{dim} ({ndofs:,} DOFs/rank), PA diffusion "
+                    f"q=p+2 Gauss-Legendre, Jacobi-PCG {it} iterations per step",
+        "dim": dim, "order": p, "cells_per_axis": n, "dofs_per_rank": ndofs,
+        "dofs_total": ndofs * world, "iterations_per_step": it, "numerics": args.numerics,
+        "l2": "inputs larger than L2 (qdata alone > 126 MB); no flush needed",
+        "parallelism": f"element-partitioned x{world}" if world > 1 else "single GPU",
+    }
+
+
+# ---------------------------------------------------------------- our arm
+def run_tfem(args):
+    import torch
+    import paper_1911_09220_b200 as tf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        from paper_1911_09220_b200 import dist
+        return dist.bench_distributed(args, rank, world, local)
+
+    torch.cuda.set_device(local)
+    dev = tf.Device(local, numerics=args.numerics)
+    stream = torch.cuda.ExternalStream(dev.stream)
+    n, p, _, _ = workload(args)
+    cells = (n,) * args.dim
+
+    t0 = time.perf_counter()
+    sp = tf.FeSpace.cartesian(dev, cells, p)
+    a = tf.BilinearForm(sp)
+    a.add_diffusion(1.0)
+    a.assemble()
+    ess = sp.essential_true_dofs()
+    op = tf.ConstrainedOperator(a, ess)
+    diag = op.diagonal()
+    dev.sync()
+    setup_s = time.perf_counter() - t0
+    N = sp.n_dofs
+    E = sp.n_elements
+    b_host = np.random.default_rng(2020).uniform(-1.0, 1.0, N)
+    b_host[ess] = 0.0
+    b = tf.Vector.from_numpy(dev, b_host)
+    x = tf.Vector(dev, N)
+
+    def step():
+        return tf.cg_solve(op, b, 0.0, args.iters, diag, x=x)
+
+    for _ in range(args.warmup):
+        res = step()
+    assert res.iterations == args.iters
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = dev.launch_count()
+    dev.sync()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ev1.synchronize()
+    t_value = ev0.elapsed_time(ev1) / 1e3
+    launches = dev.launch_count() - launches0
+    clocks = clk.summary()
+    value = N * args.iters * args.steps / t_value / 1e9
+
+    # ---- roofline of the dominant kernel: the operator application
+    nc = 3 if args.dim == 2 else 6
+    nq = p + 2
+    b_op = E * (nc * nq ** args.dim * 8 + (p + 1) ** args.dim * 4) + 16 * N
+    xin = tf.Vector.from_numpy(dev, b_host)
+    yout = tf.Vector(dev, N)
+    lib = tf.lib()
+    for _ in range(3):
+        tf.abi.check(lib.tfem_operator_mult_async(dev.h, op.h, xin.h, yout.h))
+    M = 50
+    dev.sync()
+    ev0.record(stream)
+    for _ in range(M):
+        tf.abi.check(lib.tfem_operator_mult_async(dev.h, op.h, xin.h, yout.h))
+    ev1.record(stream)
+    ev1.synchronize()
+    t_op = ev0.elapsed_time(ev1) / 1e3 / M
+    peak, peak_kind = peaks()
+    achieved = b_op / t_op / 1e9
+    b_it = b_op + 96 * N
+    cg_achieved = b_it * args.iters * args.steps / t_value / 1e9
+
+    # ---- end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        bp = torch.from_numpy(b_host).pin_memory()
+        dp = torch.from_numpy(diag.numpy()).pin_memory()
+        xp = torch.empty(N, dtype=torch.float64).pin_memory()
+        bh, dh, xh = bp.numpy(), dp.numpy(), xp.numpy()
+        tf.cg_solve_host(op, bh, 0.0, args.iters, dh, out=xh)
+        dev.sync()
+        w0 = time.perf_counter()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            _, it, _ = tf.cg_solve_host(op, bh, 0.0, args.iters, dh, out=xh)
+        ev1.record(stream)
+        ev1.synchronize()
+        t_e2e = max(ev0.elapsed_time(ev1) / 1e3, 0.0)
+        t_wall = time.perf_counter() - w0
+        t_e = max(t_e2e, t_wall)
+        e2e = {"value": N * args.iters * args.steps / t_e / 1e9, "unit": "GDOF/s",
+               "h2d_bytes_per_step": 16 * N, "d2h_bytes_per_step": 8 * N,
+               "ms_per_step": 1e3 * t_e / args.steps,
+               "api": "tfem_cg_solve_host (pinned host b, diag -> x)"}
+
+    cpu = None
+    if not args.no_cpu_baseline and args.dim == 2:
+        try:
+            ndofs_c, secs, threads, kind = cpu_reference(n, p, args.cpu_iters)
+            cpu = {"value": ndofs_c * args.cpu_iters / secs[0] / 1e9, "unit": "GDOF/s",
+                   "cores": threads, "kind": kind,
+                   "sample": f"{args.cpu_iters} Jacobi-CG iterations of the same "
+                             f"{ndofs_c:,}-DOF problem ({secs[0]:.2f} s)"}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "GDOF/s", "cores": host_threads(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_value / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args, n, p, N),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic_from_profile("operator"),
+                     "kernel": "PA operator (element kernel + shared-DOF scatter)",
+                     "bytes_per_launch": b_op, "ms_per_launch": 1e3 * t_op,
+                     "peak_source": peak_kind},
+        "cg_roofline": {"achieved": cg_achieved, "frac": cg_achieved / peak, "unit": "GB/s",
+                        "bytes_per_dof_iteration": b_it / N},
+        "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
+        "setup_s": setup_s,
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_tfem(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,244 @@
+/*
+ * tfem_cuda.h -- C ABI of libtfem_cuda.so, the B200 (sm_100a) partial-
+ * assembly (PA) operator + Jacobi-CG path of tensorfem.
+ *
+ * This is the drop-in boundary of the reference's hot path
+ * (/root/reference/proj, "tensorfem").  Plain C types only:
+ * pointers, sizes, int status codes.  Every entry point names the reference
+ * interface it replaces (file:line relative to /root/reference/proj).  The
+ * reference-side binding (the lines a maintainer adds to forms.cpp /
+ * solvers.cpp) is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Status: TFEM_OK (0) or the reference's exception class:
+ *      TFEM_INVALID_ARGUMENT  <-> std::invalid_argument
+ *      TFEM_RUNTIME_ERROR     <-> std::runtime_error
+ *      TFEM_LOGIC_ERROR       <-> std::logic_error
+ *      TFEM_CUDA_ERROR        device / driver failure
+ *    with the message text (same prefix as the reference's exception) in the
+ *    calling thread's tfem_last_error().
+ *  - Synchronous: every call has completed on the device when it returns
+ *    (SPEC.md:517), unless its name ends in _async.
+ *  - Device data: vectors live in HBM (tfem_vec); host arrays are copied in
+ *    by the create/upload calls.  A context owns one CUDA stream.
+ *  - DOF orders follow the reference: element DOFs x fastest
+ *    (mesh.hpp:85-95); quadrature points x fastest; qdata host layout
+ *    [e][q][c] (forms.cpp:219-225).  Device layouts are internal.
+ *  - Numerics: the default TFEM_NUMERICS_REFERENCE evaluates the 2D operator
+ *    in the reference's exact operation order (no FMA), so 2D results are
+ *    bit-identical to the CPU reference; TFEM_NUMERICS_FMA fuses multiply-
+ *    adds (1e-15-level relative differences).  3D (no reference) always
+ *    uses the FMA path.
+ */
+#ifndef TFEM_CUDA_H
+#define TFEM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TFEM_OK 0
+#define TFEM_INVALID_ARGUMENT 1
+#define TFEM_RUNTIME_ERROR 2
+#define TFEM_LOGIC_ERROR 3
+#define TFEM_CUDA_ERROR 4
+
+/* IntegratorKind (forms.hpp:18) */
+#define TFEM_DIFFUSION 0
+#define TFEM_MASS 1
+
+/* Quadrature rule families (quadrature.hpp:22,26) */
+#define TFEM_GAUSS_LEGENDRE 0
+#define TFEM_GAUSS_LOBATTO 1
+
+/* Node families of Basis1D (basis.hpp:15) */
+#define TFEM_NODES_GAUSS_LOBATTO 0
+#define TFEM_NODES_GAUSS_LEGENDRE 1
+#define TFEM_NODES_UNIFORM 2
+
+#define TFEM_NUMERICS_REFERENCE 0
+#define TFEM_NUMERICS_FMA 1
+
+typedef struct tfem_ctx tfem_ctx;
+typedef struct tfem_vec tfem_vec;
+typedef struct tfem_restriction tfem_restriction;
+typedef struct tfem_geometry tfem_geometry;
+typedef struct tfem_pa tfem_pa;
+typedef struct tfem_operator tfem_operator;
+
+/* ------------------------------------------------------------- errors */
+const char *tfem_last_error(void);
+const char *tfem_version(void);
+
+/* ------------------------------------------------------------ context */
+/* One device + one stream.  `device` < 0 selects the current device. */
+int tfem_ctx_create(int device, tfem_ctx **out);
+int tfem_ctx_destroy(tfem_ctx *ctx);
+int tfem_ctx_sync(tfem_ctx *ctx);
+/* The context's cudaStream_t, for interop (e.g. torch.cuda.ExternalStream). */
+void *tfem_ctx_stream(tfem_ctx *ctx);
+int tfem_ctx_set_numerics(tfem_ctx *ctx, int mode);
+/* Kernel launches issued through this context since creation. */
+int64_t tfem_ctx_launch_count(const tfem_ctx *ctx);
+
+/* -------------------------------------------- 1D rules and basis tables */
+/* gauss_legendre / gauss_lobatto on [0,1] (quadrature.cpp:64-125). */
+int tfem_quadrature(int rule, int n, double *points, double *weights);
+/* eval_matrices(Basis1D(p, node_kind), rule(nq)) -> B1d, G1d, nq x (p+1)
+ * row-major (basis.cpp:95-109). */
+int tfem_eval_matrices(int p, int node_kind, int nq, int rule, double *B,
+                       double *G);
+
+/* ------------------------------------------------------------ vectors */
+/* Vector (vector.hpp:14-48) resident in HBM. */
+int tfem_vec_create(tfem_ctx *ctx, int64_t n, tfem_vec **out);
+/* Non-owning view of existing device memory (e.g. a torch tensor). */
+int tfem_vec_wrap(tfem_ctx *ctx, double *device_ptr, int64_t n, tfem_vec **out);
+int tfem_vec_destroy(tfem_vec *v);
+int64_t tfem_vec_size(const tfem_vec *v);
+double *tfem_vec_data(tfem_vec *v);
+int tfem_vec_upload(tfem_vec *v, const double *host, int64_t n);
+int tfem_vec_download(const tfem_vec *v, double *host, int64_t n);
+int tfem_vec_fill(tfem_vec *v, double value);
+/* Vector::dot / axpy / norm2 (vector.cpp:13-36).  Deterministic (fixed-shape
+ * tree reduction), not sequential: results differ from the CPU by round-off. */
+int tfem_vec_dot(tfem_ctx *ctx, const tfem_vec *a, const tfem_vec *b,
+                 double *out);
+int tfem_vec_axpy(tfem_ctx *ctx, double a, const tfem_vec *x, tfem_vec *y);
+
+/* ------------------------------------------- element restriction (G, G^T) */
+/* The element -> DOF map of FeSpace::element_dofs (fespace.hpp:64), host
+ * array [e][i] with D1^dim entries per element.  Builds the deterministic
+ * transpose (DOF -> element slots sorted by element) on the device. */
+int tfem_restriction_create(tfem_ctx *ctx, int dim, int p, int64_t n_elem,
+                            int64_t n_dofs, const int32_t *elem_dofs,
+                            tfem_restriction **out);
+/* The same map generated on the device for an n[0] x ... Cartesian mesh:
+ * 2D reproduces build_h1_layout on make_cartesian bit for bit
+ * (mesh.cpp:65-115, 283-321); 3D uses the canonical numbering of DESIGN.md. */
+int tfem_restriction_cartesian(tfem_ctx *ctx, int dim, const int *n, int p,
+                               tfem_restriction **out);
+int tfem_restriction_destroy(tfem_restriction *r);
+int64_t tfem_restriction_n_dofs(const tfem_restriction *r);
+int64_t tfem_restriction_n_elem(const tfem_restriction *r);
+/* Download the map in the reference layout [e][i]. */
+int tfem_restriction_elem_dofs(const tfem_restriction *r, int32_t *host);
+/* Sorted DOFs on the boundary of a Cartesian restriction; count only when
+ * host == NULL (FeSpace::essential_true_dofs, fespace.cpp:205-242). */
+int tfem_restriction_boundary_dofs(const tfem_restriction *r, int32_t *host,
+                                   int64_t *count);
+/* ElementRestriction::Mult (L -> E, e-vector [e][i]) and MultTranspose
+ * (E -> L, y += in element order) (forms.cpp:250-255, 289-295). */
+int tfem_restriction_mult(tfem_ctx *ctx, const tfem_restriction *r,
+                          const tfem_vec *l, tfem_vec *e);
+int tfem_restriction_mult_transpose(tfem_ctx *ctx, const tfem_restriction *r,
+                                    const tfem_vec *e, tfem_vec *l);
+
+/* ----------------------------------------------------------- geometry */
+/* Element maps of Mesh::transformation (mesh.cpp:131-179, 228-260): order-m
+ * Gauss-Lobatto nodal geometry; control points E x (m+1)^dim x dim in
+ * lattice order (x fastest).  Straight quads: m = 1, corners v0, v1, v3, v2
+ * (mesh.cpp:238-240). */
+int tfem_geometry_create(tfem_ctx *ctx, int dim, int order, int64_t n_elem,
+                         const double *ctrl, tfem_geometry **out);
+/* make_cartesian(n, ext) generated on the device (mesh.cpp:283-321). */
+int tfem_geometry_cartesian(tfem_ctx *ctx, int dim, const int *n,
+                            const double *ext, tfem_geometry **out);
+int tfem_geometry_destroy(tfem_geometry *g);
+/* Physical coordinates of the nq^dim points of `rule` in every element,
+ * E x nq^dim x dim, so the host can evaluate a Coefficient
+ * (ElementTransformation::point, mesh.cpp:142-157). */
+int tfem_geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq,
+                         int rule, double *host_xyz);
+
+/* ------------------------------------------------- partial assembly (D) */
+/* pa_setup (forms.cpp:201-229, point_factors :46-68): geometric factors
+ * times the coefficient at the nq^dim points of `rule` (reference: q = p+2
+ * Gauss-Legendre; BP5: q = p+1 Gauss-Lobatto).  coeff == NULL -> constant
+ * coeff_const, else per point E x nq^dim (reference point order).  Errors
+ * as the reference: inverted element (runtime_error), non-positive
+ * coefficient (invalid_argument); *bad_elem (nullable) gets the element. */
+int tfem_pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p,
+                  int nq, int rule, const double *coeff, double coeff_const,
+                  tfem_pa **out, int64_t *bad_elem);
+int tfem_pa_destroy(tfem_pa *pa);
+int tfem_pa_info(const tfem_pa *pa, int *kind, int *dim, int *p, int *nq,
+                 int64_t *n_elem);
+/* PaData::stored_reals (forms.hpp:43-46) = E * nq^dim * ncomp. */
+int64_t tfem_pa_stored_reals(const tfem_pa *pa);
+/* Multiplies the instrumented reference kernels would count for one
+ * application (tensor_kernels.hpp:20-26; test_forms.cpp:397-412). */
+uint64_t tfem_pa_multiply_count(const tfem_pa *pa);
+/* PaData::d in the reference layout [e][q][c] (forms.cpp:194-199). */
+int tfem_pa_qdata(const tfem_pa *pa, double *host);
+/* PaData::b1d / g1d (forms.hpp:36-37), nq x (p+1). */
+int tfem_pa_basis(const tfem_pa *pa, double *B, double *G);
+/* pa_apply_local: y += G^T B^T D B G x on L-vectors (forms.cpp:231-296). */
+int tfem_pa_apply_local(tfem_ctx *ctx, const tfem_pa *pa,
+                        const tfem_restriction *r, const tfem_vec *x,
+                        tfem_vec *y);
+/* pa_diagonal: diag += exact diagonal (forms.cpp:311-382). */
+int tfem_pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa,
+                     const tfem_restriction *r, tfem_vec *diag);
+
+/* ------------------------------------------------------------- operator */
+/* BilinearForm::mult_true (forms.cpp:527-543) over n_pa integrators applied
+ * in insertion order; with n_ess > 0 the ConstrainedOperator of
+ * form_linear_system (forms.cpp:164-190): y = A(x with x[ess] = 0),
+ * y[ess] = x[ess].  ess is sorted and unique. */
+int tfem_operator_create(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa,
+                         const tfem_restriction *r, int64_t n_ess,
+                         const int32_t *ess, tfem_operator **out);
+/* SparseOperator over a CSR matrix (solvers.hpp:26-35). */
+int tfem_operator_create_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr,
+                             const int32_t *cols, const double *vals,
+                             tfem_operator **out);
+int tfem_operator_destroy(tfem_operator *op);
+int64_t tfem_operator_size(const tfem_operator *op);
+int tfem_operator_mult(tfem_ctx *ctx, const tfem_operator *op,
+                       const tfem_vec *x, tfem_vec *y);
+/* Same, enqueued on the context stream without waiting (for timing loops). */
+int tfem_operator_mult_async(tfem_ctx *ctx, const tfem_operator *op,
+                             const tfem_vec *x, tfem_vec *y);
+/* BilinearForm::diagonal_true (forms.cpp:545-557); with essential DOFs the
+ * driver's diag[ess] = 1 (driver.cpp:151-159). */
+int tfem_operator_diagonal(tfem_ctx *ctx, const tfem_operator *op,
+                           tfem_vec *diag);
+
+/* ------------------------------------------------------------------- CG */
+typedef struct {
+   int iterations;      /* CgResult::iterations (solvers.hpp:37-41) */
+   int converged;       /* CgResult::converged */
+   double final_norm;   /* ||r|| of the recursive residual at exit */
+   double initial_norm; /* ||b|| */
+} tfem_cg_result;
+
+/* on_iterate(it, x_host, user) after every iteration (solvers.cpp:82);
+ * forces a per-iteration device->host copy of x. */
+typedef void (*tfem_cg_callback)(int it, const double *x, int64_t n,
+                                 void *user);
+
+/* cg_solve (solvers.cpp:11-97): Jacobi-PCG from x = 0; stop when
+ * ||r|| <= rel_tol ||b|| (checked at the top of each iteration); on
+ * exhaustion x is the best iterate and converged = 0; breakdown ->
+ * TFEM_RUNTIME_ERROR with the reference message.  The whole loop runs on the
+ * device; only a 4-byte status crosses per batch of iterations. */
+int tfem_cg_solve(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *b,
+                  double rel_tol, int max_iters, const tfem_vec *jacobi_diag,
+                  tfem_vec *x, tfem_cg_result *res, tfem_cg_callback cb,
+                  void *user);
+/* Same with host buffers (copies in b / diag, copies out x): the call a
+ * host-memory caller of cg_solve makes.  jacobi_diag may be NULL. */
+int tfem_cg_solve_host(tfem_ctx *ctx, const tfem_operator *op,
+                       const double *b, double rel_tol, int max_iters,
+                       const double *jacobi_diag, double *x,
+                       tfem_cg_result *res);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

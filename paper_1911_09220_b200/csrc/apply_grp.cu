@@ -1,0 +1,414 @@
+// K2, one element per thread group (NT = round32(q^2) threads), contractions
+// staged through shared memory.
+//
+// 2D (p >= 4, where the register-resident kernel would spill): every stage
+// assigns one output entry to one thread, which sums sequentially in the
+// reference's order -- T = G V / B V (contract x), d = T B^t / T G^t
+// (contract y), pointwise D, S = G^t W / B^t W (contract qx), r = S B + S G
+// (contract qy) (tensor_kernels.cpp:76-110).  EXACT keeps it bit-identical.
+//
+// 3D: threads own (qx, qy) z-columns; the y/z contractions of a column stay
+// in registers, x/y contractions go through shared memory.  Order: in x, y,
+// z; out z, y, x (fused multiply-adds; 3D has no reference to match bits).
+//
+// Both read qdata element-major [e][c][q] (one coalesced row per component)
+// and the element-major map [e][nd]; B1d/G1d are copied into shared memory
+// once per block because the table indices differ across lanes.
+#include "kernels.cuh"
+
+namespace tfem {
+
+namespace {
+
+template <int P, int Q>
+struct Smem2D {
+   static constexpr int D1 = P + 1;
+   double V[D1 * D1];         // V[a*D1 + b]
+   double T1[Q * D1], T2[Q * D1]; // [qx][b]
+   double W1[Q * Q], W2[Q * Q];   // [qx][qy]
+   double S1[D1 * Q], S2[D1 * Q]; // [a][qy]
+};
+
+template <int P, int Q, int KIND, bool EXACT>
+__global__ void apply2d_grp_kernel(const ApplyArgs a)
+{
+   constexpr int D1 = P + 1, ND = D1 * D1, NQD = Q * Q;
+   constexpr int NT = round32(Q * Q);
+   if (a.done && *a.done) return;
+   __shared__ double sB[Q][D1], sG[Q][D1];
+   extern __shared__ double smem_raw[];
+   for (int j = threadIdx.x; j < Q * D1; j += blockDim.x) {
+      sB[j / D1][j % D1] = a.t.B[j / D1][j % D1];
+      sG[j / D1][j % D1] = a.t.G[j / D1][j % D1];
+   }
+   const int g = threadIdx.x / NT, t = threadIdx.x % NT;
+   const int64_t e = blockIdx.x * (int64_t)(blockDim.x / NT) + g;
+   const bool live = e < a.ne;
+   auto &sm = reinterpret_cast<Smem2D<P, Q> *>(smem_raw)[g];
+   uint32_t dof = 0;
+   if (live && t < ND) {
+      dof = __ldg(a.gmap + e * ND + t);
+      const uint32_t d = dof & kDofMask;
+      double v = __ldg(a.x + d);
+      if (a.mask_in && bit_set(a.mask_in, d)) v = 0.0;
+      sm.V[(t % D1) * D1 + t / D1] = v; // V(a, b) = x[dofs[b*D1 + a]]
+   }
+   __syncthreads();
+   if (live && t < Q * D1) { // contract x: [qx][b]
+      const int qx = t / D1, b = t % D1;
+      double s1 = mul<EXACT>(sG[qx][0], sm.V[b]);
+      double s2 = mul<EXACT>(sB[qx][0], sm.V[b]);
+#pragma unroll
+      for (int k = 1; k < D1; k++) {
+         if (KIND == TFEM_DIFFUSION) s1 = mac<EXACT>(s1, sG[qx][k], sm.V[k * D1 + b]);
+         s2 = mac<EXACT>(s2, sB[qx][k], sm.V[k * D1 + b]);
+      }
+      sm.T1[t] = s1;
+      sm.T2[t] = s2;
+   }
+   __syncthreads();
+   if (live && t < NQD) { // contract y and the point factors: [qx][qy]
+      const int qx = t % Q, qy = t / Q;
+      const double *qd = a.qdata + e * (int64_t)(KIND == TFEM_MASS ? 1 : 3) * NQD;
+      if (KIND == TFEM_DIFFUSION) {
+         double dx = mul<EXACT>(sm.T1[qx * D1], sB[qy][0]);
+         double dy = mul<EXACT>(sm.T2[qx * D1], sG[qy][0]);
+#pragma unroll
+         for (int b = 1; b < D1; b++) {
+            dx = mac<EXACT>(dx, sm.T1[qx * D1 + b], sB[qy][b]);
+            dy = mac<EXACT>(dy, sm.T2[qx * D1 + b], sG[qy][b]);
+         }
+         const double d0 = __ldg(qd + t), d1 = __ldg(qd + NQD + t), d2 = __ldg(qd + 2 * NQD + t);
+         sm.W1[qx * Q + qy] = add<EXACT>(mul<EXACT>(d0, dx), mul<EXACT>(d1, dy));
+         sm.W2[qx * Q + qy] = add<EXACT>(mul<EXACT>(d1, dx), mul<EXACT>(d2, dy));
+      } else {
+         double u = mul<EXACT>(sm.T2[qx * D1], sB[qy][0]);
+#pragma unroll
+         for (int b = 1; b < D1; b++) u = mac<EXACT>(u, sm.T2[qx * D1 + b], sB[qy][b]);
+         sm.W2[qx * Q + qy] = mul<EXACT>(u, __ldg(qd + t));
+      }
+   }
+   __syncthreads();
+   if (live && t < D1 * Q) { // contract qx: [a][qy]
+      const int i = t / Q, qy = t % Q;
+      if (KIND == TFEM_DIFFUSION) {
+         double s1 = mul<EXACT>(sG[0][i], sm.W1[qy]);
+         double s2 = mul<EXACT>(sB[0][i], sm.W2[qy]);
+#pragma unroll
+         for (int qx = 1; qx < Q; qx++) {
+            s1 = mac<EXACT>(s1, sG[qx][i], sm.W1[qx * Q + qy]);
+            s2 = mac<EXACT>(s2, sB[qx][i], sm.W2[qx * Q + qy]);
+         }
+         sm.S1[t] = s1;
+         sm.S2[t] = s2;
+      } else {
+         double s = mul<EXACT>(sB[0][i], sm.W2[qy]);
+#pragma unroll
+         for (int qx = 1; qx < Q; qx++) s = mac<EXACT>(s, sB[qx][i], sm.W2[qx * Q + qy]);
+         sm.S2[t] = s;
+      }
+   }
+   __syncthreads();
+   double dot = 0.0;
+   if (live && t < ND) { // contract qy: r(a, b), out[b*D1 + a] = r(a, b)
+      const int ia = t % D1, b = t / D1;
+      double r;
+      if (KIND == TFEM_DIFFUSION) {
+         double vx = mul<EXACT>(sm.S1[ia * Q], sB[0][b]);
+         double vy = mul<EXACT>(sm.S2[ia * Q], sG[0][b]);
+#pragma unroll
+         for (int qy = 1; qy < Q; qy++) {
+            vx = mac<EXACT>(vx, sm.S1[ia * Q + qy], sB[qy][b]);
+            vy = mac<EXACT>(vy, sm.S2[ia * Q + qy], sG[qy][b]);
+         }
+         r = add<EXACT>(vx, vy);
+      } else {
+         r = mul<EXACT>(sm.S2[ia * Q], sB[0][b]);
+#pragma unroll
+         for (int qy = 1; qy < Q; qy++) r = mac<EXACT>(r, sm.S2[ia * Q + qy], sB[qy][b]);
+      }
+      if (dof & kExclusive) {
+         const uint32_t d = dof & kDofMask;
+         if (!a.overwrite) r = add<EXACT>(a.y[d], r);
+         if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
+         a.y[d] = r;
+         if (a.partials) dot = mul<EXACT>(__ldg(a.x + d), r);
+      } else {
+         a.evec[e * ND + t] = r;
+      }
+   }
+   if (a.partials) {
+      __shared__ double part[32];
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
+      if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = dot;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+         double s = 0.0;
+         for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += part[w];
+         a.partials[blockIdx.x] = s;
+      }
+   }
+}
+
+template <int P, int Q>
+struct Smem3D {
+   static constexpr int D1 = P + 1;
+   double V[D1 * D1 * D1];                    // [c][b][a]
+   double TB[D1 * D1 * Q], TG[D1 * D1 * Q];   // [c][b][qx]
+   double Px[D1 * Q * Q], Py[D1 * Q * Q], Pz[D1 * Q * Q]; // [c][qy][qx]
+};
+
+template <int P, int Q, int KIND>
+__global__ void apply3d_kernel(const ApplyArgs a)
+{
+   constexpr int D1 = P + 1, ND = D1 * D1 * D1, NQD = Q * Q * Q;
+   constexpr int NT = round32(Q * Q);
+   if (a.done && *a.done) return;
+   __shared__ double sB[Q][D1], sG[Q][D1];
+   extern __shared__ double smem_raw[];
+   for (int j = threadIdx.x; j < Q * D1; j += blockDim.x) {
+      sB[j / D1][j % D1] = a.t.B[j / D1][j % D1];
+      sG[j / D1][j % D1] = a.t.G[j / D1][j % D1];
+   }
+   const int g = threadIdx.x / NT, t = threadIdx.x % NT;
+   const int64_t e = blockIdx.x * (int64_t)(blockDim.x / NT) + g;
+   const bool live = e < a.ne;
+   auto &sm = reinterpret_cast<Smem3D<P, Q> *>(smem_raw)[g];
+   const uint32_t *gm = a.gmap + e * ND;
+   if (live) {
+      for (int i = t; i < ND; i += NT) {
+         const uint32_t d = __ldg(gm + i) & kDofMask;
+         double v = __ldg(a.x + d);
+         if (a.mask_in && bit_set(a.mask_in, d)) v = 0.0;
+         sm.V[i] = v;
+      }
+   }
+   __syncthreads();
+   if (live) { // contract a -> TB / TG [c][b][qx]
+      for (int j = t; j < D1 * D1 * Q; j += NT) {
+         const int qx = j % Q, cb = j / Q;
+         double sb = 0.0, sg = 0.0;
+#pragma unroll
+         for (int k = 0; k < D1; k++) {
+            const double v = sm.V[cb * D1 + k];
+            sb = fma(sB[qx][k], v, sb);
+            if (KIND == TFEM_DIFFUSION) sg = fma(sG[qx][k], v, sg);
+         }
+         sm.TB[j] = sb;
+         sm.TG[j] = sg;
+      }
+   }
+   __syncthreads();
+   const int qx = t % Q, qy = t / Q;
+   if (live && t < Q * Q) {
+      double UBB[D1], UBG[D1], UGB[D1];
+#pragma unroll
+      for (int c = 0; c < D1; c++) { // contract b
+         double bb = 0.0, bg = 0.0, gb = 0.0;
+#pragma unroll
+         for (int b = 0; b < D1; b++) {
+            const double tb = sm.TB[(c * D1 + b) * Q + qx];
+            bb = fma(sB[qy][b], tb, bb);
+            if (KIND == TFEM_DIFFUSION) {
+               const double tg = sm.TG[(c * D1 + b) * Q + qx];
+               bg = fma(sG[qy][b], tb, bg);
+               gb = fma(sB[qy][b], tg, gb);
+            }
+         }
+         UBB[c] = bb;
+         UBG[c] = bg;
+         UGB[c] = gb;
+      }
+      double Px[D1], Py[D1], Pz[D1];
+#pragma unroll
+      for (int c = 0; c < D1; c++) Px[c] = Py[c] = Pz[c] = 0.0;
+      const double *qd = a.qdata + e * (int64_t)(KIND == TFEM_MASS ? 1 : 6) * NQD;
+#pragma unroll
+      for (int qz = 0; qz < Q; qz++) { // contract c, point factors, back over qz
+         const int q = qx + Q * (qy + Q * qz);
+         if (KIND == TFEM_MASS) {
+            double u = 0.0;
+#pragma unroll
+            for (int c = 0; c < D1; c++) u = fma(sB[qz][c], UBB[c], u);
+            const double w = u * __ldg(qd + q);
+#pragma unroll
+            for (int c = 0; c < D1; c++) Px[c] = fma(sB[qz][c], w, Px[c]);
+         } else {
+            double ux = 0.0, uy = 0.0, uz = 0.0;
+#pragma unroll
+            for (int c = 0; c < D1; c++) {
+               ux = fma(sB[qz][c], UGB[c], ux);
+               uy = fma(sB[qz][c], UBG[c], uy);
+               uz = fma(sG[qz][c], UBB[c], uz);
+            }
+            const double D00 = __ldg(qd + q), D01 = __ldg(qd + NQD + q);
+            const double D02 = __ldg(qd + 2 * NQD + q), D11 = __ldg(qd + 3 * NQD + q);
+            const double D12 = __ldg(qd + 4 * NQD + q), D22 = __ldg(qd + 5 * NQD + q);
+            const double wx = fma(D02, uz, fma(D01, uy, D00 * ux));
+            const double wy = fma(D12, uz, fma(D11, uy, D01 * ux));
+            const double wz = fma(D22, uz, fma(D12, uy, D02 * ux));
+#pragma unroll
+            for (int c = 0; c < D1; c++) {
+               Px[c] = fma(sB[qz][c], wx, Px[c]);
+               Py[c] = fma(sB[qz][c], wy, Py[c]);
+               Pz[c] = fma(sG[qz][c], wz, Pz[c]);
+            }
+         }
+      }
+#pragma unroll
+      for (int c = 0; c < D1; c++) {
+         sm.Px[(c * Q + qy) * Q + qx] = Px[c];
+         if (KIND == TFEM_DIFFUSION) {
+            sm.Py[(c * Q + qy) * Q + qx] = Py[c];
+            sm.Pz[(c * Q + qy) * Q + qx] = Pz[c];
+         }
+      }
+   }
+   __syncthreads();
+   if (live) { // contract qy -> [c][b][qx] (x-gradient part in TB, rest in TG)
+      for (int j = t; j < D1 * D1 * Q; j += NT) {
+         const int jx = j % Q, cb = j / Q, b = cb % D1, c = cb / D1;
+         double sx = 0.0, syz = 0.0;
+#pragma unroll
+         for (int y = 0; y < Q; y++) {
+            const int o = (c * Q + y) * Q + jx;
+            sx = fma(sB[y][b], sm.Px[o], sx);
+            if (KIND == TFEM_DIFFUSION) {
+               syz = fma(sG[y][b], sm.Py[o], syz);
+               syz = fma(sB[y][b], sm.Pz[o], syz);
+            }
+         }
+         sm.TB[j] = sx;
+         sm.TG[j] = syz;
+      }
+   }
+   __syncthreads();
+   double dot = 0.0;
+   if (live) { // contract qx -> r(a, b, c)
+      for (int i = t; i < ND; i += NT) {
+         const int ia = i % D1, cb = i / D1;
+         double r = 0.0;
+#pragma unroll
+         for (int x = 0; x < Q; x++) {
+            if (KIND == TFEM_MASS) {
+               r = fma(sB[x][ia], sm.TB[cb * Q + x], r);
+            } else {
+               r = fma(sG[x][ia], sm.TB[cb * Q + x], r);
+               r = fma(sB[x][ia], sm.TG[cb * Q + x], r);
+            }
+         }
+         const uint32_t gg = __ldg(gm + i);
+         if (gg & kExclusive) {
+            const uint32_t d = gg & kDofMask;
+            if (!a.overwrite) r += a.y[d];
+            if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
+            a.y[d] = r;
+            if (a.partials) dot = fma(__ldg(a.x + d), r, dot);
+         } else {
+            a.evec[e * ND + i] = r;
+         }
+      }
+   }
+   if (a.partials) {
+      __shared__ double part[32];
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
+      if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = dot;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+         double s = 0.0;
+         for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += part[w];
+         a.partials[blockIdx.x] = s;
+      }
+   }
+}
+
+// Elements per block so a block has ~256 threads.
+constexpr int groups_for(int nt) { return nt >= 256 ? 1 : 256 / nt; }
+
+template <typename K>
+void set_smem(K kernel, size_t bytes)
+{
+   if (bytes > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int P, int Q, int KIND, bool EXACT>
+void launch2d(const ApplyArgs &a, cudaStream_t s, unsigned blocks)
+{
+   constexpr int NT = round32(Q * Q), GR = groups_for(NT);
+   const size_t smem = sizeof(Smem2D<P, Q>) * GR;
+   static bool once = (set_smem(apply2d_grp_kernel<P, Q, KIND, EXACT>, smem), true);
+   (void)once;
+   apply2d_grp_kernel<P, Q, KIND, EXACT><<<blocks, NT * GR, smem, s>>>(a);
+}
+
+template <int P, int Q, int KIND>
+void launch3d(const ApplyArgs &a, cudaStream_t s, unsigned blocks)
+{
+   constexpr int NT = round32(Q * Q), GR = groups_for(NT);
+   const size_t smem = sizeof(Smem3D<P, Q>) * GR;
+   static bool once = (set_smem(apply3d_kernel<P, Q, KIND>, smem), true);
+   (void)once;
+   apply3d_kernel<P, Q, KIND><<<blocks, NT * GR, smem, s>>>(a);
+}
+
+template <int P, int Q, int KIND>
+KernelPick make2d(bool exact)
+{
+   KernelPick k;
+   k.launch = exact ? launch2d<P, Q, KIND, true> : launch2d<P, Q, KIND, false>;
+   k.elems_per_block = groups_for(round32(Q * Q));
+   k.threads = round32(Q * Q) * k.elems_per_block;
+   return k;
+}
+
+template <int P, int Q, int KIND>
+KernelPick make3d()
+{
+   KernelPick k;
+   k.launch = launch3d<P, Q, KIND>;
+   k.elems_per_block = groups_for(round32(Q * Q));
+   k.threads = round32(Q * Q) * k.elems_per_block;
+   return k;
+}
+
+template <int P, int KIND>
+KernelPick pick_q(int dim, int nq, bool exact)
+{
+   if (dim == 2) {
+      if constexpr (P >= 4) { // lower orders use the register kernel
+         if (nq == P + 2) return make2d<P, P + 2, KIND>(exact);
+         if (nq == P + 1) return make2d<P, P + 1, KIND>(exact);
+      }
+   } else {
+      if (nq == P + 2) return make3d<P, P + 2, KIND>();
+      if (nq == P + 1) return make3d<P, P + 1, KIND>();
+   }
+   return {};
+}
+
+template <int KIND>
+KernelPick pick_p(int dim, int p, int nq, bool exact)
+{
+   switch (p) {
+   case 1: return pick_q<1, KIND>(dim, nq, exact);
+   case 2: return pick_q<2, KIND>(dim, nq, exact);
+   case 3: return pick_q<3, KIND>(dim, nq, exact);
+   case 4: return pick_q<4, KIND>(dim, nq, exact);
+   case 5: return pick_q<5, KIND>(dim, nq, exact);
+   case 6: return pick_q<6, KIND>(dim, nq, exact);
+   case 7: return pick_q<7, KIND>(dim, nq, exact);
+   case 8: return pick_q<8, KIND>(dim, nq, exact);
+   }
+   return {};
+}
+
+} // namespace
+
+KernelPick pick_apply_grp(int dim, int p, int nq, int kind, bool exact)
+{
+   return kind == TFEM_MASS ? pick_p<TFEM_MASS>(dim, p, nq, exact)
+                            : pick_p<TFEM_DIFFUSION>(dim, p, nq, exact);
+}
+
+} // namespace tfem

@@ -1,0 +1,646 @@
+// The C ABI of libtfem_cuda.so (include/tfem_cuda.h).  Every entry point runs
+// its body under guard(): library exceptions become the status code of the
+// reference's exception class with the message in tfem_last_error().
+#include "common.cuh"
+
+#include <cstring>
+#include <string>
+
+namespace tfem {
+tfem_restriction *restriction_cartesian(tfem_ctx *ctx, int dim, const int *n, int p);
+tfem_restriction *restriction_create(tfem_ctx *ctx, int dim, int p, int64_t ne, int64_t ndofs,
+                                     const int32_t *elem_dofs);
+void restriction_destroy(tfem_restriction *r);
+void restriction_elem_dofs(const tfem_restriction *r, int32_t *host);
+int64_t restriction_boundary_dofs(const tfem_restriction *r, int32_t *host);
+void restriction_mult(tfem_ctx *ctx, const tfem_restriction *r, const double *l, double *e);
+void vec_axpy(tfem_ctx *ctx, double a, const double *x, double *y, int64_t n);
+void operator_set_ess(tfem_ctx *ctx, tfem_operator *op, int64_t n_ess, const int32_t *ess);
+tfem_operator *operator_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, const int32_t *cols,
+                            const double *vals);
+void operator_release(tfem_operator *op);
+void operator_diagonal(tfem_ctx *ctx, const tfem_operator *op, double *diag);
+} // namespace tfem
+
+using namespace tfem;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guard(F &&f)
+{
+   try {
+      f();
+      return TFEM_OK;
+   } catch (const Error &e) {
+      g_last_error = e.what();
+      return e.code;
+   } catch (const std::bad_alloc &) {
+      g_last_error = "out of host memory";
+      return TFEM_RUNTIME_ERROR;
+   } catch (const std::exception &e) {
+      g_last_error = e.what();
+      return TFEM_RUNTIME_ERROR;
+   }
+}
+
+void need(const void *p, const char *what)
+{
+   if (!p) invalid(std::string(what) + ": null argument");
+}
+
+void check_vec(const tfem_vec *v, int64_t n, const char *what)
+{
+   need(v, what);
+   if (v->n != n) invalid(std::string(what) + ": size mismatch");
+}
+
+} // namespace
+
+void tfem_ctx::ensure_partials(int64_t n)
+{
+   if (n <= red.cap) return;
+   cudaFree(red.partials);
+   TFEM_CUDA(cudaMalloc(&red.partials, sizeof(double) * n));
+   red.cap = n;
+}
+
+extern "C" {
+
+const char *tfem_last_error(void) { return g_last_error.c_str(); }
+const char *tfem_version(void) { return "tfem_cuda 0.1 (sm_100a)"; }
+
+// ------------------------------------------------------------------ context
+int tfem_ctx_create(int device, tfem_ctx **out)
+{
+   return guard([&] {
+      need(out, "tfem_ctx_create");
+      int count = 0;
+      TFEM_CUDA(cudaGetDeviceCount(&count));
+      if (device >= count) invalid("tfem_ctx_create: no such device");
+      if (device >= 0) TFEM_CUDA(cudaSetDevice(device));
+      auto *c = new tfem_ctx;
+      TFEM_CUDA(cudaGetDevice(&c->device));
+      TFEM_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
+      TFEM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      TFEM_CUDA(cudaMalloc(&c->scalars, sizeof(double) * 16));
+      TFEM_CUDA(cudaMallocHost(&c->host_scalars, sizeof(double) * 16));
+      *out = c;
+   });
+}
+
+int tfem_ctx_destroy(tfem_ctx *ctx)
+{
+   return guard([&] {
+      if (!ctx) return;
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->red.partials);
+      cudaFree(ctx->scalars);
+      cudaFreeHost(ctx->host_scalars);
+      cudaStreamDestroy(ctx->stream);
+      delete ctx;
+   });
+}
+
+int tfem_ctx_sync(tfem_ctx *ctx)
+{
+   return guard([&] {
+      need(ctx, "tfem_ctx_sync");
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+void *tfem_ctx_stream(tfem_ctx *ctx) { return ctx ? static_cast<void *>(ctx->stream) : nullptr; }
+
+int tfem_ctx_set_numerics(tfem_ctx *ctx, int mode)
+{
+   return guard([&] {
+      need(ctx, "tfem_ctx_set_numerics");
+      if (mode != TFEM_NUMERICS_REFERENCE && mode != TFEM_NUMERICS_FMA)
+         invalid("tfem_ctx_set_numerics: unknown mode");
+      ctx->numerics = mode;
+   });
+}
+
+int64_t tfem_ctx_launch_count(const tfem_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+// ------------------------------------------------------------------ tables
+int tfem_quadrature(int rule, int n, double *points, double *weights)
+{
+   return guard([&] {
+      need(points, "tfem_quadrature");
+      std::vector<double> w;
+      const std::vector<double> x = gauss_points(rule, n, &w);
+      std::memcpy(points, x.data(), sizeof(double) * n);
+      if (weights) std::memcpy(weights, w.data(), sizeof(double) * n);
+   });
+}
+
+int tfem_eval_matrices(int p, int node_kind, int nq, int rule, double *B, double *G)
+{
+   return guard([&] {
+      need(B, "tfem_eval_matrices");
+      need(G, "tfem_eval_matrices");
+      if (nq < 1) invalid("tfem_eval_matrices: need nq >= 1");
+      eval_matrices(p, node_kind, nq, rule, B, G);
+   });
+}
+
+// ------------------------------------------------------------------ vectors
+int tfem_vec_create(tfem_ctx *ctx, int64_t n, tfem_vec **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_vec_create");
+      need(out, "tfem_vec_create");
+      if (n < 0) invalid("tfem_vec_create: negative size");
+      auto *v = new tfem_vec;
+      v->ctx = ctx;
+      v->n = n;
+      cudaError_t e = cudaMalloc(&v->d, sizeof(double) * static_cast<size_t>(n > 0 ? n : 1));
+      if (e != cudaSuccess) {
+         delete v;
+         cuda_check(e, "tfem_vec_create");
+      }
+      TFEM_CUDA(cudaMemsetAsync(v->d, 0, sizeof(double) * n, ctx->stream));
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+      *out = v;
+   });
+}
+
+int tfem_vec_wrap(tfem_ctx *ctx, double *device_ptr, int64_t n, tfem_vec **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_vec_wrap");
+      need(out, "tfem_vec_wrap");
+      auto *v = new tfem_vec;
+      v->ctx = ctx;
+      v->d = device_ptr;
+      v->n = n;
+      v->owns = false;
+      *out = v;
+   });
+}
+
+int tfem_vec_destroy(tfem_vec *v)
+{
+   return guard([&] {
+      if (!v) return;
+      if (v->owns) cudaFree(v->d);
+      delete v;
+   });
+}
+
+int64_t tfem_vec_size(const tfem_vec *v) { return v ? v->n : 0; }
+double *tfem_vec_data(tfem_vec *v) { return v ? v->d : nullptr; }
+
+int tfem_vec_upload(tfem_vec *v, const double *host, int64_t n)
+{
+   return guard([&] {
+      check_vec(v, n, "tfem_vec_upload");
+      TFEM_CUDA(cudaMemcpyAsync(v->d, host, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                v->ctx->stream));
+      TFEM_CUDA(cudaStreamSynchronize(v->ctx->stream));
+   });
+}
+
+int tfem_vec_download(const tfem_vec *v, double *host, int64_t n)
+{
+   return guard([&] {
+      check_vec(v, n, "tfem_vec_download");
+      TFEM_CUDA(cudaMemcpyAsync(host, v->d, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                v->ctx->stream));
+      TFEM_CUDA(cudaStreamSynchronize(v->ctx->stream));
+   });
+}
+
+int tfem_vec_fill(tfem_vec *v, double value)
+{
+   return guard([&] {
+      need(v, "tfem_vec_fill");
+      vec_fill(v->ctx, v->d, v->n, value);
+      TFEM_CUDA(cudaStreamSynchronize(v->ctx->stream));
+   });
+}
+
+int tfem_vec_dot(tfem_ctx *ctx, const tfem_vec *a, const tfem_vec *b, double *out)
+{
+   return guard([&] {
+      need(ctx, "Vector::dot");
+      need(a, "Vector::dot");
+      check_vec(b, a->n, "Vector::dot");
+      *out = vec_dot(ctx, a->d, b->d, a->n);
+   });
+}
+
+int tfem_vec_axpy(tfem_ctx *ctx, double a, const tfem_vec *x, tfem_vec *y)
+{
+   return guard([&] {
+      need(ctx, "Vector::axpy");
+      need(x, "Vector::axpy");
+      check_vec(y, x->n, "Vector::axpy");
+      vec_axpy(ctx, a, x->d, y->d, x->n);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+// ------------------------------------------------------------- restriction
+int tfem_restriction_create(tfem_ctx *ctx, int dim, int p, int64_t n_elem, int64_t n_dofs,
+                            const int32_t *elem_dofs, tfem_restriction **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_restriction_create");
+      need(elem_dofs, "tfem_restriction_create");
+      need(out, "tfem_restriction_create");
+      *out = restriction_create(ctx, dim, p, n_elem, n_dofs, elem_dofs);
+   });
+}
+
+int tfem_restriction_cartesian(tfem_ctx *ctx, int dim, const int *n, int p,
+                               tfem_restriction **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_restriction_cartesian");
+      need(n, "tfem_restriction_cartesian");
+      need(out, "tfem_restriction_cartesian");
+      *out = restriction_cartesian(ctx, dim, n, p);
+   });
+}
+
+int tfem_restriction_destroy(tfem_restriction *r)
+{
+   return guard([&] { restriction_destroy(r); });
+}
+
+int64_t tfem_restriction_n_dofs(const tfem_restriction *r) { return r ? r->ndofs : 0; }
+int64_t tfem_restriction_n_elem(const tfem_restriction *r) { return r ? r->ne : 0; }
+
+int tfem_restriction_elem_dofs(const tfem_restriction *r, int32_t *host)
+{
+   return guard([&] {
+      need(r, "tfem_restriction_elem_dofs");
+      need(host, "tfem_restriction_elem_dofs");
+      restriction_elem_dofs(r, host);
+   });
+}
+
+int tfem_restriction_boundary_dofs(const tfem_restriction *r, int32_t *host, int64_t *count)
+{
+   return guard([&] {
+      need(r, "tfem_restriction_boundary_dofs");
+      need(count, "tfem_restriction_boundary_dofs");
+      *count = restriction_boundary_dofs(r, host);
+   });
+}
+
+int tfem_restriction_mult(tfem_ctx *ctx, const tfem_restriction *r, const tfem_vec *l,
+                          tfem_vec *e)
+{
+   return guard([&] {
+      need(ctx, "ElementRestriction::Mult");
+      need(r, "ElementRestriction::Mult");
+      check_vec(l, r->ndofs, "ElementRestriction::Mult");
+      check_vec(e, r->ne * r->nd, "ElementRestriction::Mult");
+      restriction_mult(ctx, r, l->d, e->d);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+int tfem_restriction_mult_transpose(tfem_ctx *ctx, const tfem_restriction *r, const tfem_vec *e,
+                                    tfem_vec *l)
+{
+   return guard([&] {
+      need(ctx, "ElementRestriction::MultTranspose");
+      need(r, "ElementRestriction::MultTranspose");
+      check_vec(l, r->ndofs, "ElementRestriction::MultTranspose");
+      check_vec(e, r->ne * r->nd, "ElementRestriction::MultTranspose");
+      restriction_mult_transpose(ctx, r, e->d, l->d);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+// ---------------------------------------------------------------- geometry
+int tfem_geometry_create(tfem_ctx *ctx, int dim, int order, int64_t n_elem, const double *ctrl,
+                         tfem_geometry **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_geometry_create");
+      need(ctrl, "tfem_geometry_create");
+      need(out, "tfem_geometry_create");
+      if (dim != 2 && dim != 3) invalid("tfem_geometry_create: dim must be 2 or 3");
+      if (order < 1) invalid("curve_mesh: order must be >= 1");
+      if (n_elem < 1) invalid("tfem_geometry_create: empty mesh");
+      auto *g = new tfem_geometry;
+      g->ctx = ctx;
+      g->dim = dim;
+      g->order = order;
+      g->ne = n_elem;
+      int64_t nc = 1;
+      for (int d = 0; d < dim; d++) nc *= order + 1;
+      const size_t bytes = sizeof(double) * static_cast<size_t>(n_elem * nc * dim);
+      TFEM_CUDA(cudaMalloc(&g->ctrl, bytes));
+      TFEM_CUDA(cudaMemcpy(g->ctrl, ctrl, bytes, cudaMemcpyHostToDevice));
+      *out = g;
+   });
+}
+
+int tfem_geometry_cartesian(tfem_ctx *ctx, int dim, const int *n, const double *ext,
+                            tfem_geometry **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_geometry_cartesian");
+      need(n, "tfem_geometry_cartesian");
+      need(out, "tfem_geometry_cartesian");
+      if (dim != 2 && dim != 3) invalid("tfem_geometry_cartesian: dim must be 2 or 3");
+      auto *g = new tfem_geometry;
+      g->ctx = ctx;
+      g->dim = dim;
+      g->order = 1;
+      g->cartesian = true;
+      g->ne = 1;
+      for (int d = 0; d < dim; d++) {
+         if (n[d] < 1) {
+            delete g;
+            invalid("make_cartesian: need nx, ny >= 1");
+         }
+         const double e = ext ? ext[d] : 1.0;
+         if (!(e > 0.0)) {
+            delete g;
+            invalid("make_cartesian: need positive extents");
+         }
+         g->n[d] = n[d];
+         g->ext[d] = e;
+         g->ne *= n[d];
+      }
+      *out = g;
+   });
+}
+
+int tfem_geometry_destroy(tfem_geometry *g)
+{
+   return guard([&] {
+      if (!g) return;
+      cudaFree(g->ctrl);
+      delete g;
+   });
+}
+
+int tfem_geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq, int rule,
+                         double *host_xyz)
+{
+   return guard([&] {
+      need(ctx, "tfem_geometry_points");
+      need(g, "tfem_geometry_points");
+      need(host_xyz, "tfem_geometry_points");
+      geometry_points(ctx, g, nq, rule, host_xyz);
+   });
+}
+
+// ---------------------------------------------------------------------- PA
+int tfem_pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq, int rule,
+                  const double *coeff, double coeff_const, tfem_pa **out, int64_t *bad_elem)
+{
+   return guard([&] {
+      need(ctx, "pa_setup");
+      need(g, "pa_setup");
+      need(out, "pa_setup");
+      *out = pa_setup(ctx, kind, g, p, nq, rule, coeff, coeff_const, bad_elem);
+   });
+}
+
+int tfem_pa_destroy(tfem_pa *pa)
+{
+   return guard([&] {
+      if (!pa) return;
+      cudaFree(pa->qdata);
+      delete pa;
+   });
+}
+
+int tfem_pa_info(const tfem_pa *pa, int *kind, int *dim, int *p, int *nq, int64_t *n_elem)
+{
+   return guard([&] {
+      need(pa, "tfem_pa_info");
+      if (kind) *kind = pa->kind;
+      if (dim) *dim = pa->dim;
+      if (p) *p = pa->p;
+      if (nq) *nq = pa->nq;
+      if (n_elem) *n_elem = pa->ne;
+   });
+}
+
+int64_t tfem_pa_stored_reals(const tfem_pa *pa)
+{
+   return pa ? pa->ne * pa->nqd * pa->ncomp : 0;
+}
+
+uint64_t tfem_pa_multiply_count(const tfem_pa *pa)
+{
+   if (!pa) return 0;
+   const uint64_t a = pa->p + 1, q = pa->nq, e = pa->ne;
+   uint64_t per;
+   if (pa->dim == 2)
+      per = pa->kind == TFEM_MASS ? 2 * (q * a * a + q * q * a) + q * q
+                                  : 4 * (q * a * a + q * q * a) + 4 * q * q;
+   else
+      per = pa->kind == TFEM_MASS
+               ? 2 * (q * a * a * a + q * q * a * a + q * q * q * a) + q * q * q
+               : 2 * (2 * q * a * a * a + 3 * q * q * a * a + 3 * q * q * q * a) + 9 * q * q * q;
+   return per * e;
+}
+
+int tfem_pa_qdata(const tfem_pa *pa, double *host)
+{
+   return guard([&] {
+      need(pa, "PaData::d");
+      need(host, "PaData::d");
+      const size_t n = static_cast<size_t>(pa->ncomp) * pa->nqd * pa->ne_pad;
+      std::vector<double> dev(n);
+      TFEM_CUDA(cudaMemcpy(dev.data(), pa->qdata, sizeof(double) * n, cudaMemcpyDeviceToHost));
+      for (int64_t e = 0; e < pa->ne; e++)
+         for (int q = 0; q < pa->nqd; q++)
+            for (int c = 0; c < pa->ncomp; c++) {
+               const double v = pa->elem_major()
+                                   ? dev[(e * pa->ncomp + c) * pa->nqd + q]
+                                   : dev[(static_cast<int64_t>(c) * pa->nqd + q) * pa->ne_pad + e];
+               host[(e * pa->nqd + q) * pa->ncomp + c] = v;
+            }
+   });
+}
+
+int tfem_pa_basis(const tfem_pa *pa, double *B, double *G)
+{
+   return guard([&] {
+      need(pa, "tfem_pa_basis");
+      if (B) std::memcpy(B, pa->B.data(), sizeof(double) * pa->B.size());
+      if (G) std::memcpy(G, pa->G.data(), sizeof(double) * pa->G.size());
+   });
+}
+
+int tfem_pa_apply_local(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r,
+                        const tfem_vec *x, tfem_vec *y)
+{
+   return guard([&] {
+      need(ctx, "pa_apply_local");
+      need(pa, "pa_apply_local");
+      need(r, "pa_apply_local");
+      if (!x || !y || x->n != r->ndofs || y->n != r->ndofs)
+         invalid("pa_apply_local: size mismatch");
+      if (x->d == y->d) invalid("pa_apply_local: x and y must not alias");
+      ApplyFlags f;
+      pa_apply(ctx, pa, r, x->d, y->d, f);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+int tfem_pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, tfem_vec *diag)
+{
+   return guard([&] {
+      need(ctx, "pa_diagonal");
+      need(pa, "pa_diagonal");
+      need(r, "pa_diagonal");
+      check_vec(diag, r->ndofs, "pa_diagonal");
+      pa_diagonal(ctx, pa, r, diag->d);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+// ---------------------------------------------------------------- operator
+int tfem_operator_create(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa, const tfem_restriction *r,
+                         int64_t n_ess, const int32_t *ess, tfem_operator **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_operator_create");
+      need(r, "tfem_operator_create");
+      need(out, "tfem_operator_create");
+      if (n_pa < 1) invalid("tfem_operator_create: need at least one integrator");
+      auto *op = new tfem_operator;
+      op->ctx = ctx;
+      op->n = r->ndofs;
+      op->r = r;
+      for (int k = 0; k < n_pa; k++) {
+         if (!pa[k] || pa[k]->dim != r->dim || pa[k]->p != r->p || pa[k]->ne != r->ne) {
+            delete op;
+            invalid("forms: point factors were built for a different space");
+         }
+         op->pa.push_back(pa[k]);
+      }
+      try {
+         operator_set_ess(ctx, op, n_ess, ess);
+      } catch (...) {
+         operator_release(op);
+         throw;
+      }
+      *out = op;
+   });
+}
+
+int tfem_operator_create_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, const int32_t *cols,
+                             const double *vals, tfem_operator **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_operator_create_csr");
+      need(rowptr, "tfem_operator_create_csr");
+      need(out, "tfem_operator_create_csr");
+      *out = operator_csr(ctx, n, rowptr, cols, vals);
+   });
+}
+
+int tfem_operator_destroy(tfem_operator *op)
+{
+   return guard([&] {
+      if (op) operator_release(op);
+   });
+}
+
+int64_t tfem_operator_size(const tfem_operator *op) { return op ? op->n : 0; }
+
+int tfem_operator_mult(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *x, tfem_vec *y)
+{
+   return guard([&] {
+      need(ctx, "BilinearForm::mult_true");
+      need(op, "BilinearForm::mult_true");
+      if (!x || !y || x->n != op->n || y->n != op->n)
+         invalid("BilinearForm::mult_true: size mismatch");
+      if (x->d == y->d) invalid("BilinearForm::mult_true: x and y must not alias");
+      operator_mult(ctx, op, x->d, y->d, nullptr, nullptr);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+int tfem_operator_mult_async(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *x,
+                             tfem_vec *y)
+{
+   return guard([&] {
+      need(ctx, "BilinearForm::mult_true");
+      need(op, "BilinearForm::mult_true");
+      if (!x || !y || x->n != op->n || y->n != op->n)
+         invalid("BilinearForm::mult_true: size mismatch");
+      if (x->d == y->d) invalid("BilinearForm::mult_true: x and y must not alias");
+      operator_mult(ctx, op, x->d, y->d, nullptr, nullptr);
+   });
+}
+
+int tfem_operator_diagonal(tfem_ctx *ctx, const tfem_operator *op, tfem_vec *diag)
+{
+   return guard([&] {
+      need(ctx, "BilinearForm::diagonal_true");
+      need(op, "BilinearForm::diagonal_true");
+      check_vec(diag, op->n, "BilinearForm::diagonal_true");
+      operator_diagonal(ctx, op, diag->d);
+   });
+}
+
+// ---------------------------------------------------------------------- CG
+int tfem_cg_solve(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *b, double rel_tol,
+                  int max_iters, const tfem_vec *jacobi_diag, tfem_vec *x, tfem_cg_result *res,
+                  tfem_cg_callback cb, void *user)
+{
+   return guard([&] {
+      need(ctx, "cg_solve");
+      need(op, "cg_solve");
+      need(res, "cg_solve");
+      if (!b || b->n != op->n) invalid("cg_solve: operator/vector size mismatch");
+      if (!x || x->n != op->n) invalid("cg_solve: operator/vector size mismatch");
+      if (jacobi_diag && jacobi_diag->n != op->n)
+         invalid("cg_solve: preconditioner size mismatch");
+      if (x->d == b->d) invalid("cg_solve: x and b must not alias");
+      cg_solve(ctx, op, b->d, rel_tol, max_iters, jacobi_diag ? jacobi_diag->d : nullptr, x->d,
+               res, cb, user);
+   });
+}
+
+int tfem_cg_solve_host(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
+                       int max_iters, const double *jacobi_diag, double *x, tfem_cg_result *res)
+{
+   return guard([&] {
+      need(ctx, "cg_solve");
+      need(op, "cg_solve");
+      need(b, "cg_solve");
+      need(x, "cg_solve");
+      need(res, "cg_solve");
+      const int64_t n = op->n;
+      // Device staging buffers cached per (context, size).
+      static thread_local std::vector<std::pair<int64_t, double *>> cache;
+      auto buf = [&](int slot) -> double * {
+         if (cache.size() < 3) cache.resize(3, {0, nullptr});
+         if (cache[slot].first != n) {
+            cudaFree(cache[slot].second);
+            TFEM_CUDA(cudaMalloc(&cache[slot].second, sizeof(double) * n));
+            cache[slot].first = n;
+         }
+         return cache[slot].second;
+      };
+      double *db = buf(0), *dx = buf(1), *dd = jacobi_diag ? buf(2) : nullptr;
+      TFEM_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+      if (dd)
+         TFEM_CUDA(cudaMemcpyAsync(dd, jacobi_diag, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+      cg_solve(ctx, op, db, rel_tol, max_iters, dd, dx, res, nullptr, nullptr);
+      TFEM_CUDA(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+} // extern "C"

@@ -1,0 +1,610 @@
+// K5 / K6: operators and the device-resident Jacobi-PCG of cg_solve
+// (solvers.cpp:11-97).
+//
+// Per iteration (all on the device, batches of iterations replayed as one
+// CUDA graph, only a 4-byte stop flag read back per batch):
+//   1. q = A p            element kernel + shared-DOF scatter, fused p.q partials
+//   2. alpha kernel       1 block: pq = sum(partials), alpha = rz / pq
+//   3. update kernel      x' = x + alpha p, r -= alpha q, z = r / d,
+//                         partials of r.r and r.z
+//   4. beta kernel        1 block: ||r||, best-iterate bookkeeping, beta, stop test
+//   5. direction kernel   p = r / d + beta p
+// Vector updates use unfused multiply + add in the reference's order
+// (vector.cpp:20-23, solvers.cpp:84-87), so only the dot products differ from
+// the CPU (tree vs sequential sum).  The best iterate (solvers.cpp:78-81) costs
+// no copies: x rotates through three buffers and "best" is an index.
+#include "common.cuh"
+
+#include <cmath>
+#include <memory>
+#include <unordered_map>
+
+namespace tfem {
+
+void vec_axpy(tfem_ctx *ctx, double a, const double *x, double *y, int64_t n);
+
+namespace {
+
+constexpr int kVecThreads = 256;
+
+inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+// Fixed grid for vector kernels: deterministic partial count for a given n.
+inline unsigned vec_blocks(const tfem_ctx *ctx, int64_t n)
+{
+   const int64_t cap = static_cast<int64_t>(ctx->sm_count) * 8;
+   const int64_t need = (n + kVecThreads - 1) / kVecThreads;
+   return static_cast<unsigned>(need < cap ? (need > 0 ? need : 1) : cap);
+}
+
+__global__ void fill_kernel(double *d, int64_t n, double v)
+{
+   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+        i += (int64_t)gridDim.x * blockDim.x)
+      d[i] = v;
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+dot_kernel(const double *a, const double *b, int64_t n, double *partials)
+{
+   double s = 0.0;
+   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+        i += (int64_t)gridDim.x * blockDim.x)
+      s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
+   const double t = block_sum<kVecThreads>(s);
+   if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+// Deterministic fixed-order sum of `n` partials by one block.
+__device__ double sum_partials(const double *p, int64_t n)
+{
+   double s = 0.0;
+   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += p[i];
+   return block_sum<kVecThreads>(s);
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+reduce_kernel(const double *partials, int64_t n, int k, double *out)
+{
+   // k interleaved sums: partials laid out [k][n]
+   for (int j = 0; j < k; j++) {
+      const double s = sum_partials(partials + j * n, n);
+      if (threadIdx.x == 0) out[j] = s;
+      __syncthreads();
+   }
+}
+
+__global__ void axpy_kernel(double a, const double *x, double *y, int64_t n)
+{
+   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+        i += (int64_t)gridDim.x * blockDim.x)
+      y[i] = __dadd_rn(y[i], __dmul_rn(a, x[i]));
+}
+
+// y[ess] = x[ess] style helpers
+__global__ void set_bits_kernel(const int32_t *list, int64_t n, uint32_t *mask)
+{
+   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (i < n) atomicOr(mask + (list[i] >> 5), 1u << (list[i] & 31));
+}
+
+__global__ void set_values_kernel(const int32_t *list, int64_t n, double v, double *y)
+{
+   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (i < n) y[list[i]] = v;
+}
+
+// SparseMatrix::mult (sparse.cpp:75-87), thread per row, optional x.y partial.
+__global__ void __launch_bounds__(kVecThreads)
+csr_kernel(const int32_t *rowptr, const int32_t *cols, const double *vals, int64_t n,
+           const double *x, double *y, double *partials, const int *done)
+{
+   if (done && *done) return;
+   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   double dot = 0.0;
+   if (i < n) {
+      double s = 0.0;
+      for (int k = rowptr[i]; k < rowptr[i + 1]; k++) s = __dadd_rn(s, __dmul_rn(vals[k], x[cols[k]]));
+      y[i] = s;
+      dot = __dmul_rn(x[i], s);
+   }
+   if (partials) {
+      const double t = block_sum<kVecThreads>(dot);
+      if (threadIdx.x == 0) partials[blockIdx.x] = t;
+   }
+}
+
+// ----------------------------------------------------------------- CG
+struct CgState {
+   double rz, alpha, beta, rnorm, best_rnorm, target;
+   int it, max_iters, done, converged, iterations, status;
+   int cur, best;
+};
+
+__device__ __forceinline__ int next_buffer(int cur, int best)
+{
+   for (int k = 0; k < 3; k++)
+      if (k != cur && k != best) return k;
+   return 0;
+}
+
+// r = b, z = M r, p = z, x0 = 0; partials of r.r and r.z (solvers.cpp:43-58)
+__global__ void __launch_bounds__(kVecThreads)
+cg_init_kernel(const double *b, const double *diag, int64_t n, double *r, double *p, double *x,
+               double *partials /* [2][gridDim] */)
+{
+   double rr = 0.0, rz = 0.0;
+   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+        i += (int64_t)gridDim.x * blockDim.x) {
+      const double ri = b[i];
+      const double zi = diag ? __ddiv_rn(ri, diag[i]) : ri;
+      r[i] = ri;
+      p[i] = zi;
+      x[i] = 0.0;
+      rr = __dadd_rn(rr, __dmul_rn(ri, ri));
+      rz = __dadd_rn(rz, __dmul_rn(ri, zi));
+   }
+   const double a = block_sum<kVecThreads>(rr);
+   const double c = block_sum<kVecThreads>(rz);
+   if (threadIdx.x == 0) {
+      partials[blockIdx.x] = a;
+      partials[gridDim.x + blockIdx.x] = c;
+   }
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+cg_init_finish_kernel(const double *partials, int64_t nb, CgState *st)
+{
+   const double rr = sum_partials(partials, nb);
+   __syncthreads();
+   const double rz = sum_partials(partials + nb, nb);
+   if (threadIdx.x == 0) {
+      st->rz = rz;
+      st->rnorm = sqrt(rr);
+      st->best_rnorm = st->rnorm;
+      st->it = 0;
+      st->done = 0;
+      st->converged = 0;
+      st->iterations = 0;
+      st->status = 0;
+      st->cur = 0;
+      st->best = 0;
+      if (st->rnorm <= st->target) { // top of iteration 1 (solvers.cpp:61-65)
+         st->done = 1;
+         st->converged = 1;
+         st->iterations = 0;
+      }
+   }
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+cg_alpha_kernel(const double *partials, int64_t nb, CgState *st)
+{
+   if (st->done) return;
+   const double pq = sum_partials(partials, nb);
+   if (threadIdx.x == 0) {
+      const double alpha = st->rz / pq;
+      st->alpha = alpha;
+      if (!isfinite(alpha)) { // solvers.cpp:69-71
+         st->status = 1;
+         st->done = 1;
+      }
+   }
+}
+
+struct XBufs {
+   double *x[3];
+};
+
+__global__ void __launch_bounds__(kVecThreads)
+cg_update_kernel(const CgState *st, XBufs xb, const double *p, const double *q, double *r,
+                 const double *diag, int64_t n, double *partials /* [2][gridDim] */)
+{
+   if (st->done) return;
+   const double alpha = st->alpha, nalpha = -alpha;
+   const double *xc = xb.x[st->cur];
+   double *xn = xb.x[next_buffer(st->cur, st->best)];
+   double rr = 0.0, rz = 0.0;
+   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+        i += (int64_t)gridDim.x * blockDim.x) {
+      xn[i] = __dadd_rn(xc[i], __dmul_rn(alpha, p[i]));
+      const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, q[i]));
+      r[i] = ri;
+      const double zi = diag ? __ddiv_rn(ri, diag[i]) : ri;
+      rr = __dadd_rn(rr, __dmul_rn(ri, ri));
+      rz = __dadd_rn(rz, __dmul_rn(ri, zi));
+   }
+   const double a = block_sum<kVecThreads>(rr);
+   const double c = block_sum<kVecThreads>(rz);
+   if (threadIdx.x == 0) {
+      partials[blockIdx.x] = a;
+      partials[gridDim.x + blockIdx.x] = c;
+   }
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+cg_beta_kernel(const double *partials, int64_t nb, CgState *st)
+{
+   if (st->done) return;
+   const double rr = sum_partials(partials, nb);
+   __syncthreads();
+   const double rz_next = sum_partials(partials + nb, nb);
+   if (threadIdx.x != 0) return;
+   const double rnorm = sqrt(rr);
+   st->rnorm = rnorm;
+   if (!isfinite(rnorm)) { // solvers.cpp:74-77
+      st->status = 2;
+      st->done = 1;
+      return;
+   }
+   st->it += 1;
+   const int nxt = next_buffer(st->cur, st->best);
+   st->cur = nxt;
+   if (rnorm < st->best_rnorm) { // solvers.cpp:78-81
+      st->best_rnorm = rnorm;
+      st->best = nxt;
+   }
+   st->beta = rz_next / st->rz;
+   st->rz = rz_next;
+   if (rnorm <= st->target) { // checked at the top of the next iteration
+      st->done = 1;
+      st->converged = 1;
+      st->iterations = st->it;
+   } else if (st->it >= st->max_iters) {
+      st->done = 1;
+      st->converged = 0;
+      st->iterations = st->max_iters;
+   }
+}
+
+__global__ void cg_direction_kernel(const CgState *st, const double *r, const double *diag,
+                                    double *p, int64_t n)
+{
+   if (st->done) return;
+   const double beta = st->beta;
+   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+        i += (int64_t)gridDim.x * blockDim.x) {
+      const double zi = diag ? __ddiv_rn(r[i], diag[i]) : r[i];
+      p[i] = __dadd_rn(zi, __dmul_rn(beta, p[i]));
+   }
+}
+
+__global__ void diag_check_kernel(const double *d, int64_t n, int *bad)
+{
+   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+        i += (int64_t)gridDim.x * blockDim.x)
+      if (!(d[i] > 0.0)) *bad = 1;
+}
+
+template <typename T>
+T *dalloc(int64_t n)
+{
+   T *p = nullptr;
+   TFEM_CUDA(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(n > 0 ? n : 1)));
+   return p;
+}
+
+// Per-operator CG workspace, reused across solves (vectors + graph).
+struct Workspace {
+   int64_t n = 0;
+   double *r = nullptr, *p = nullptr, *q = nullptr, *xa = nullptr, *xb = nullptr;
+   double *part_op = nullptr, *part_vec = nullptr;
+   int64_t n_op_part = 0;
+   CgState *st = nullptr;
+   CgState *host_st = nullptr; // pinned
+   cudaGraphExec_t graph = nullptr;
+   const double *g_diag = nullptr, *g_x = nullptr;
+   int g_batch = 0;
+   int64_t g_launches = 0;
+   ~Workspace()
+   {
+      cudaFree(r);
+      cudaFree(p);
+      cudaFree(q);
+      cudaFree(xa);
+      cudaFree(xb);
+      cudaFree(part_op);
+      cudaFree(part_vec);
+      cudaFree(st);
+      if (host_st) cudaFreeHost(host_st);
+      if (graph) cudaGraphExecDestroy(graph);
+   }
+};
+
+std::unordered_map<const tfem_operator *, std::unique_ptr<Workspace>> &workspaces()
+{
+   static std::unordered_map<const tfem_operator *, std::unique_ptr<Workspace>> w;
+   return w;
+}
+
+int64_t op_partials(const tfem_operator *op)
+{
+   if (op->csr) return blocks_for(op->n, kVecThreads);
+   return pa_apply_partials(op->pa.back(), op->r);
+}
+
+Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
+{
+   auto &m = workspaces();
+   auto it = m.find(op);
+   if (it != m.end()) return *it->second;
+   auto w = std::make_unique<Workspace>();
+   w->n = op->n;
+   w->r = dalloc<double>(op->n);
+   w->p = dalloc<double>(op->n);
+   w->q = dalloc<double>(op->n);
+   w->xa = dalloc<double>(op->n);
+   w->xb = dalloc<double>(op->n);
+   w->n_op_part = op_partials(op);
+   w->part_op = dalloc<double>(w->n_op_part);
+   w->part_vec = dalloc<double>(2 * static_cast<int64_t>(ctx->sm_count) * 8);
+   w->st = dalloc<CgState>(1);
+   TFEM_CUDA(cudaMallocHost(&w->host_st, sizeof(CgState)));
+   auto &ref = *w;
+   m.emplace(op, std::move(w));
+   return ref;
+}
+
+// One CG iteration's launches (used eagerly and under stream capture).
+int64_t enqueue_iteration(tfem_ctx *ctx, const tfem_operator *op, Workspace &w, XBufs xb,
+                          const double *diag)
+{
+   const int64_t n = op->n;
+   int64_t launches = 0;
+   const int64_t before = ctx->launches;
+   const int64_t np = operator_mult(ctx, op, w.p, w.q, w.part_op, &w.st->done);
+   cg_alpha_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.part_op, np, w.st);
+   const unsigned vb = vec_blocks(ctx, n);
+   cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.p, w.q, w.r, diag, n,
+                                                         w.part_vec);
+   cg_beta_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.part_vec, vb, w.st);
+   cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.r, diag, w.p, n);
+   ctx->launched(4);
+   TFEM_CUDA(cudaGetLastError());
+   launches = ctx->launches - before;
+   return launches;
+}
+
+} // namespace
+
+void vec_fill(tfem_ctx *ctx, double *d, int64_t n, double v)
+{
+   fill_kernel<<<vec_blocks(ctx, n), kVecThreads, 0, ctx->stream>>>(d, n, v);
+   ctx->launched();
+   TFEM_CUDA(cudaGetLastError());
+}
+
+double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n)
+{
+   const unsigned nb = vec_blocks(ctx, n);
+   ctx->ensure_partials(nb + 1);
+   dot_kernel<<<nb, kVecThreads, 0, ctx->stream>>>(a, b, n, ctx->red.partials);
+   reduce_kernel<<<1, kVecThreads, 0, ctx->stream>>>(ctx->red.partials, nb, 1, ctx->scalars);
+   ctx->launched(2);
+   TFEM_CUDA(cudaGetLastError());
+   TFEM_CUDA(cudaMemcpyAsync(ctx->host_scalars, ctx->scalars, sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+   TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   return ctx->host_scalars[0];
+}
+
+void vec_axpy(tfem_ctx *ctx, double a, const double *x, double *y, int64_t n)
+{
+   axpy_kernel<<<vec_blocks(ctx, n), kVecThreads, 0, ctx->stream>>>(a, x, y, n);
+   ctx->launched();
+   TFEM_CUDA(cudaGetLastError());
+}
+
+void operator_set_ess(tfem_ctx *ctx, tfem_operator *op, int64_t n_ess, const int32_t *ess)
+{
+   op->n_ess = n_ess;
+   if (n_ess == 0) return;
+   for (int64_t i = 0; i < n_ess; i++) {
+      if (ess[i] < 0 || ess[i] >= op->n) invalid("form_linear_system: essential DOF out of range");
+      if (i > 0 && ess[i] <= ess[i - 1])
+         invalid("form_linear_system: essential list must be sorted and unique");
+   }
+   op->ess = dalloc<int32_t>(n_ess);
+   const int64_t words = (op->n + 31) / 32;
+   op->ess_mask = dalloc<uint32_t>(words);
+   TFEM_CUDA(cudaMemcpy(op->ess, ess, sizeof(int32_t) * n_ess, cudaMemcpyHostToDevice));
+   TFEM_CUDA(cudaMemsetAsync(op->ess_mask, 0, sizeof(uint32_t) * words, ctx->stream));
+   set_bits_kernel<<<blocks_for(n_ess, 256), 256, 0, ctx->stream>>>(op->ess, n_ess,
+                                                                   op->ess_mask);
+   ctx->launched();
+   TFEM_CUDA(cudaGetLastError());
+   TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+tfem_operator *operator_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, const int32_t *cols,
+                            const double *vals)
+{
+   if (n < 1) invalid("operator_create_csr: empty matrix");
+   auto *op = new tfem_operator;
+   op->ctx = ctx;
+   op->csr = true;
+   op->n = n;
+   const int64_t nnz = rowptr[n];
+   op->rowptr = dalloc<int32_t>(n + 1);
+   op->cols = dalloc<int32_t>(nnz);
+   op->vals = dalloc<double>(nnz);
+   TFEM_CUDA(cudaMemcpy(op->rowptr, rowptr, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice));
+   TFEM_CUDA(cudaMemcpy(op->cols, cols, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+   TFEM_CUDA(cudaMemcpy(op->vals, vals, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+   return op;
+}
+
+void operator_release(tfem_operator *op)
+{
+   workspaces().erase(op);
+   cudaFree(op->ess);
+   cudaFree(op->ess_mask);
+   cudaFree(op->rowptr);
+   cudaFree(op->cols);
+   cudaFree(op->vals);
+   delete op;
+}
+
+// mult_true / ConstrainedOperator::mult (forms.cpp:173-184, 527-543): the
+// integrators in insertion order, the first overwriting y, later ones
+// accumulating; essential DOFs masked on input for all and overwritten on
+// output by the last (which also produces the fused x . y partials).
+int64_t operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, double *y,
+                      double *dot_partials, const int *done)
+{
+   if (op->csr) {
+      csr_kernel<<<blocks_for(op->n, kVecThreads), kVecThreads, 0, ctx->stream>>>(
+         op->rowptr, op->cols, op->vals, op->n, x, y, dot_partials, done);
+      ctx->launched();
+      TFEM_CUDA(cudaGetLastError());
+      return blocks_for(op->n, kVecThreads);
+   }
+   int64_t np = 0;
+   for (size_t k = 0; k < op->pa.size(); k++) {
+      ApplyFlags f;
+      f.overwrite = (k == 0);
+      f.mask_in = op->ess_mask;
+      const bool last = (k + 1 == op->pa.size());
+      f.ess_out = last ? op->ess_mask : nullptr;
+      f.dot_partials = last ? dot_partials : nullptr;
+      f.done = done;
+      np = pa_apply(ctx, op->pa[k], op->r, x, y, f);
+   }
+   return np;
+}
+
+void operator_diagonal(tfem_ctx *ctx, const tfem_operator *op, double *diag)
+{
+   if (op->csr) invalid("operator_diagonal: not available for CSR operators");
+   // diagonal_true (forms.cpp:545-557): each integrator's diagonal from zero,
+   // then d.axpy(1.0, one) in insertion order.
+   vec_fill(ctx, diag, op->n, 0.0);
+   if (op->pa.size() == 1) {
+      pa_diagonal(ctx, op->pa[0], op->r, diag);
+   } else {
+      double *one = dalloc<double>(op->n);
+      for (const tfem_pa *pa : op->pa) {
+         vec_fill(ctx, one, op->n, 0.0);
+         pa_diagonal(ctx, pa, op->r, one);
+         vec_axpy(ctx, 1.0, one, diag, op->n);
+      }
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(one);
+   }
+   if (op->n_ess > 0) {
+      set_values_kernel<<<blocks_for(op->n_ess, 256), 256, 0, ctx->stream>>>(op->ess, op->n_ess,
+                                                                            1.0, diag);
+      ctx->launched();
+   }
+   TFEM_CUDA(cudaGetLastError());
+   TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
+              int max_iters, const double *diag, double *x, tfem_cg_result *res,
+              tfem_cg_callback cb, void *user)
+{
+   const int64_t n = op->n;
+   res->iterations = 0;
+   res->converged = 0;
+   res->final_norm = 0.0;
+   res->initial_norm = 0.0;
+   if (diag) { // solvers.cpp:19-29
+      int *bad = dalloc<int>(1);
+      TFEM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+      diag_check_kernel<<<vec_blocks(ctx, n), kVecThreads, 0, ctx->stream>>>(diag, n, bad);
+      ctx->launched();
+      int hb = 0;
+      TFEM_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(bad);
+      if (hb) invalid("cg_solve: Jacobi diagonal must be strictly positive");
+   }
+   Workspace &w = workspace_for(ctx, op);
+   const double bnorm = std::sqrt(vec_dot(ctx, b, b, n));
+   res->initial_norm = bnorm;
+   if (!std::isfinite(bnorm)) runtime("cg_solve: right-hand side is not finite");
+   if (bnorm == 0.0) { // solvers.cpp:37-41
+      vec_fill(ctx, x, n, 0.0);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+      res->converged = 1;
+      return;
+   }
+   CgState init{};
+   init.target = rel_tol * bnorm;
+   init.max_iters = max_iters;
+   TFEM_CUDA(cudaMemcpyAsync(w.st, &init, sizeof(CgState), cudaMemcpyHostToDevice, ctx->stream));
+   const unsigned vb = vec_blocks(ctx, n);
+   cg_init_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(b, diag, n, w.r, w.p, x, w.part_vec);
+   cg_init_finish_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.part_vec, vb, w.st);
+   ctx->launched(2);
+   TFEM_CUDA(cudaGetLastError());
+   const XBufs xb{{x, w.xa, w.xb}};
+
+   auto read_state = [&]() {
+      TFEM_CUDA(cudaMemcpyAsync(w.host_st, w.st, sizeof(CgState), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+      return *w.host_st;
+   };
+
+   CgState hs = read_state();
+   if (max_iters <= 0 && !hs.done) {
+      // for-loop never runs (solvers.cpp:60, 89-96): x = best = 0
+      res->iterations = max_iters;
+      res->final_norm = hs.rnorm;
+      return;
+   }
+   if (cb) {
+      std::vector<double> hx(n);
+      while (!hs.done) {
+         enqueue_iteration(ctx, op, w, xb, diag);
+         hs = read_state();
+         if (hs.status == 0 && hs.it > 0) {
+            TFEM_CUDA(cudaMemcpy(hx.data(), xb.x[hs.cur], sizeof(double) * n,
+                                 cudaMemcpyDeviceToHost));
+            cb(hs.it, hx.data(), n, user);
+         }
+      }
+   } else {
+      // Batches of iterations as one graph; the batch length keeps the
+      // per-batch host round trip small against the work it covers.
+      const int batch = n >= (1 << 22) ? 4 : 16;
+      if (!w.graph || w.g_diag != diag || w.g_x != x || w.g_batch != batch) {
+         if (w.graph) {
+            cudaGraphExecDestroy(w.graph);
+            w.graph = nullptr;
+         }
+         cudaGraph_t g;
+         const int64_t before = ctx->launches;
+         TFEM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+         for (int k = 0; k < batch; k++) enqueue_iteration(ctx, op, w, xb, diag);
+         TFEM_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+         w.g_launches = ctx->launches - before;
+         ctx->launches = before;
+         TFEM_CUDA(cudaGraphInstantiate(&w.graph, g, 0));
+         cudaGraphDestroy(g);
+         w.g_diag = diag;
+         w.g_x = x;
+         w.g_batch = batch;
+      }
+      while (!hs.done) {
+         TFEM_CUDA(cudaGraphLaunch(w.graph, ctx->stream));
+         ctx->launched(w.g_launches);
+         hs = read_state();
+      }
+   }
+   if (hs.status == 1) runtime("cg_solve: breakdown (non-finite step)");
+   if (hs.status == 2) runtime("cg_solve: breakdown (non-finite residual)");
+   res->iterations = hs.iterations;
+   res->converged = hs.converged;
+   res->final_norm = hs.rnorm;
+   const int pick = hs.converged ? hs.cur : hs.best; // solvers.cpp:89-96
+   if (xb.x[pick] != x) {
+      TFEM_CUDA(cudaMemcpyAsync(x, xb.x[pick], sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   }
+}
+
+} // namespace tfem

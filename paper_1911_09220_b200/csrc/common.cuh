@@ -1,0 +1,232 @@
+// Internal types and helpers of libtfem_cuda.so (not part of the C ABI).
+#pragma once
+
+#include "tfem_cuda.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace tfem {
+
+// ----------------------------------------------------------------- errors
+// Exceptions inside the library map 1:1 onto the reference's exception
+// classes and are converted to status codes at the C boundary (capi.cu).
+struct Error : std::runtime_error {
+   int code;
+   Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void invalid(const std::string &m) { throw Error(TFEM_INVALID_ARGUMENT, m); }
+[[noreturn]] inline void runtime(const std::string &m) { throw Error(TFEM_RUNTIME_ERROR, m); }
+[[noreturn]] inline void logic(const std::string &m) { throw Error(TFEM_LOGIC_ERROR, m); }
+
+inline void cuda_check(cudaError_t e, const char *what)
+{
+   if (e != cudaSuccess) {
+      throw Error(TFEM_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+   }
+}
+#define TFEM_CUDA(call) ::tfem::cuda_check((call), #call)
+
+// Flag bit on an element-map entry: the DOF has exactly one element slot, so
+// the element kernel owns it and writes it directly (no E-vector round trip).
+constexpr uint32_t kExclusive = 0x80000000u;
+constexpr uint32_t kDofMask = 0x7fffffffu;
+
+constexpr int kMaxP = 8;
+constexpr int kMaxQ = 10;
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// Device data layout of an (dim, p) space.  Low-order 2D runs one element per
+// thread: slot-major element map [nd][ne_pad] and point-major qdata planes
+// [(c*nqd+q)][ne_pad] (element fastest, coalesced).  3D and 2D p >= 4 run one
+// element per thread group: element-major map [e][nd] and qdata [e][c][q].
+inline bool elem_major_layout(int dim, int p) { return dim == 3 || p >= 4; }
+
+// Scratch for block partials of fused dot products and the last-block
+// ticket.  One per context; every reduction uses a fixed grid so the result
+// is deterministic run to run.
+struct Reducer {
+   double *partials = nullptr; // [cap]
+   int64_t cap = 0;
+   unsigned int *ticket = nullptr;
+};
+
+} // namespace tfem
+
+struct tfem_ctx {
+   int device = 0;
+   cudaStream_t stream = nullptr;
+   int numerics = TFEM_NUMERICS_REFERENCE;
+   int sm_count = 148;
+   int64_t launches = 0;
+   tfem::Reducer red;
+   double *scalars = nullptr;      // device scratch for small results
+   double *host_scalars = nullptr; // pinned mirror
+   void ensure_partials(int64_t n);
+   void launched(int64_t n = 1) { launches += n; }
+};
+
+struct tfem_vec {
+   tfem_ctx *ctx = nullptr;
+   double *d = nullptr;
+   int64_t n = 0;
+   bool owns = true;
+};
+
+struct tfem_restriction {
+   tfem_ctx *ctx = nullptr;
+   int dim = 2, p = 1, nd = 4; // nd = (p+1)^dim
+   int64_t ne = 0, ne_pad = 0, ndofs = 0;
+   // Element map with the kExclusive flag, layout elem_major_layout(dim, p):
+   // slot-major [nd][ne_pad] or element-major [ne_pad][nd]; a `slot` indexes
+   // both gmap and the E-vector.
+   bool elem_major = false;
+   uint32_t *gmap = nullptr;
+   int64_t n_shared = 0;        // DOFs with >= 2 element slots
+   int32_t *shared_dofs = nullptr;
+   int32_t *shared_off = nullptr; // n_shared + 1
+   uint32_t *shared_slots = nullptr; // gmap / E-vector slots, sorted by element
+   double *evec = nullptr;       // E-vector scratch, gmap layout (lazy)
+   bool cartesian = false;
+   int n[3] = {0, 0, 0};
+   double *ensure_evec();
+};
+
+struct tfem_geometry {
+   tfem_ctx *ctx = nullptr;
+   int dim = 2, order = 1;
+   int64_t ne = 0;
+   double *ctrl = nullptr; // [e][l][dim] (null for Cartesian)
+   bool cartesian = false;
+   int n[3] = {0, 0, 0};
+   double ext[3] = {1.0, 1.0, 1.0};
+};
+
+struct tfem_pa {
+   tfem_ctx *ctx = nullptr;
+   int kind = TFEM_DIFFUSION, dim = 2, p = 1, nq = 3, rule = TFEM_GAUSS_LEGENDRE;
+   int ncomp = 3, nqd = 9;
+   int64_t ne = 0, ne_pad = 0;
+   // elem_major_layout(dim, p) ? [e][c][q] : planes [(c * nqd + q)][ne_pad]
+   double *qdata = nullptr;
+   bool elem_major() const { return tfem::elem_major_layout(dim, p); }
+   std::vector<double> B, G; // nq x (p+1)
+};
+
+struct tfem_operator {
+   tfem_ctx *ctx = nullptr;
+   bool csr = false;
+   int64_t n = 0;
+   std::vector<tfem_pa *> pa;
+   const tfem_restriction *r = nullptr;
+   int64_t n_ess = 0;
+   int32_t *ess = nullptr;      // sorted list
+   uint32_t *ess_mask = nullptr; // bitmap over DOFs
+   int32_t *rowptr = nullptr, *cols = nullptr;
+   double *vals = nullptr;
+};
+
+namespace tfem {
+
+// Host-side 1D tables (host_basis.cpp).
+std::vector<double> gauss_points(int rule, int n, std::vector<double> *weights);
+void basis_nodes(int p, int node_kind, std::vector<double> &nodes, std::vector<double> &bary);
+void basis_eval(const std::vector<double> &nodes, const std::vector<double> &bary, double x,
+                double *values, double *derivs);
+void eval_matrices(int p, int node_kind, int nq, int rule, double *B, double *G);
+
+// Launch helpers implemented per translation unit.
+void vec_fill(tfem_ctx *ctx, double *d, int64_t n, double v);
+double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n);
+
+// Restriction / layout (restriction.cu)
+tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne, int64_t ndofs,
+                                       bool elem_major, uint32_t *d_gmap_raw /* owned */);
+void restriction_mult_transpose(tfem_ctx *ctx, const tfem_restriction *r, const double *e,
+                                double *l);
+
+// PA kernels (apply.cu)
+struct ApplyFlags {
+   bool overwrite = false;   // y = (else y +=)
+   const uint32_t *mask_in = nullptr;  // zero gathered essential DOFs
+   const uint32_t *ess_out = nullptr;  // y[ess] = x[ess]
+   double *dot_partials = nullptr;     // per-block partials of x . y
+   const int *done = nullptr;          // device flag: skip when set (CG)
+};
+// Launches the element kernel and (if needed) the shared-DOF scatter.
+// Returns the number of dot partials written (element blocks + scatter
+// blocks) when flags.dot_partials is set.
+int64_t pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const double *x,
+                 double *y, const ApplyFlags &f);
+int64_t pa_apply_partials(const tfem_pa *pa, const tfem_restriction *r);
+void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, double *diag);
+
+// Setup (setup.cu)
+tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq, int rule,
+                  const double *coeff_host, double coeff_const, int64_t *bad_elem);
+void geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq, int rule, double *host_xyz);
+
+// Operators / CG (cg.cu)
+// Returns the number of dot partials written when dot_partials is set.
+int64_t operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, double *y,
+                      double *dot_partials, const int *done);
+void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
+              int max_iters, const double *diag, double *x, tfem_cg_result *res,
+              tfem_cg_callback cb, void *user);
+
+} // namespace tfem
+
+// ------------------------------------------------------------ device side
+#ifdef __CUDACC__
+namespace tfem {
+
+__device__ __forceinline__ bool bit_set(const uint32_t *mask, uint32_t d)
+{
+   return (__ldg(mask + (d >> 5)) >> (d & 31)) & 1u;
+}
+
+// Block-wide sum with a fixed shape: warp shuffles, then warp 0.  Valid in
+// thread 0 only.  Deterministic for a fixed blockDim.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v)
+{
+   static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+   __shared__ double warp_part[NT / 32];
+#pragma unroll
+   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+   if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = v;
+   __syncthreads();
+   double s = 0.0;
+   if (threadIdx.x < 32) {
+      s = threadIdx.x < NT / 32 ? warp_part[threadIdx.x] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+   }
+   __syncthreads(); // warp_part may be reused by the next call
+   return s;
+}
+
+// Exact (reference-order, unfused) or fused arithmetic.
+template <bool EXACT>
+__device__ __forceinline__ double mul(double a, double b)
+{
+   return EXACT ? __dmul_rn(a, b) : a * b;
+}
+template <bool EXACT>
+__device__ __forceinline__ double add(double a, double b)
+{
+   return EXACT ? __dadd_rn(a, b) : a + b;
+}
+template <bool EXACT>
+__device__ __forceinline__ double mac(double acc, double a, double b)
+{
+   return EXACT ? __dadd_rn(acc, __dmul_rn(a, b)) : fma(a, b, acc);
+}
+
+} // namespace tfem
+#endif

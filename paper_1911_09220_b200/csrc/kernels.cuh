@@ -1,0 +1,47 @@
+// Shared definitions of the element kernels (apply2d_reg.cu, apply_grp.cu)
+// and their dispatch (apply.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace tfem {
+
+struct Tables {
+   double B[kMaxQ][kMaxP + 1];
+   double G[kMaxQ][kMaxP + 1];
+};
+
+struct ApplyArgs {
+   Tables t;
+   int64_t ne, ne_pad;
+   int nd;
+   const uint32_t *gmap;
+   const double *qdata;
+   const double *x;
+   double *y;
+   double *evec;
+   int overwrite;
+   const uint32_t *mask_in;
+   const uint32_t *ess_out;
+   double *partials;
+   const int *done; // CG stop flag: skip the work once the solve has ended
+};
+
+using Launch = void (*)(const ApplyArgs &, cudaStream_t, unsigned);
+
+struct KernelPick {
+   Launch launch = nullptr;
+   int elems_per_block = 1;
+   int threads = 128;
+};
+
+constexpr int kElemThreads2D = 128;
+
+// Register-resident thread-per-element kernels: 2D, p <= 3.
+KernelPick pick_apply2d_reg(int p, int nq, int kind, bool exact);
+// Thread-group-per-element kernels through shared memory: 2D p >= 4, 3D.
+KernelPick pick_apply_grp(int dim, int p, int nq, int kind, bool exact);
+
+constexpr __host__ __device__ int round32(int v) { return ((v + 31) / 32) * 32; }
+
+} // namespace tfem
