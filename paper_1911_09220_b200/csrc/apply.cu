@@ -16,32 +16,104 @@ constexpr int kScatterThreads = 256;
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 // --------------------------------------------------------------- scatter
-// Shared DOFs: y[d] (+)= sum of E-vector slots in ascending element order,
-// essential overwrite and the fused x . y partial.
+// Shared DOFs, one thread per DOF, bucketed by slot count c (ELL rows, one
+// vector load for the row): y[d] (+)= sum of its E-vector slots in ascending
+// element order, y[ess] = x[ess], fused x . y partial.  One launch covers all
+// buckets; each block belongs to one bucket (uniform switch).
+struct BucketArgs {
+   int nb;
+   int c[tfem_restriction::kMaxBuckets];
+   int64_t n[tfem_restriction::kMaxBuckets];
+   const int32_t *dofs[tfem_restriction::kMaxBuckets];
+   const uint32_t *slots[tfem_restriction::kMaxBuckets];
+   int64_t start[tfem_restriction::kMaxBuckets + 1]; // first block of each bucket
+};
+
+template <int C>
+__device__ __forceinline__ void load_row(const uint32_t *__restrict__ row, uint32_t (&sl)[C])
+{
+   if constexpr (C == 2) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2 *>(row));
+      sl[0] = v.x;
+      sl[1] = v.y;
+   } else if constexpr (C == 4 || C == 8) {
+#pragma unroll
+      for (int k = 0; k < C; k += 4) {
+         const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row) + k / 4);
+         sl[k] = v.x;
+         sl[k + 1] = v.y;
+         sl[k + 2] = v.z;
+         sl[k + 3] = v.w;
+      }
+   } else {
+#pragma unroll
+      for (int k = 0; k < C; k++) sl[k] = __ldg(row + k);
+   }
+}
+
+template <bool EXACT, int C>
+__device__ __forceinline__ double scatter_row(const BucketArgs &B, int b, int64_t s,
+                                              const double *__restrict__ evec,
+                                              const double *__restrict__ x, double *y,
+                                              int overwrite, const uint32_t *ess_out, bool want_dot)
+{
+   const int32_t d = __ldg(B.dofs[b] + s);
+   uint32_t sl[C];
+   load_row<C>(B.slots[b] + s * C, sl);
+   double v[C];
+#pragma unroll
+   for (int k = 0; k < C; k++) v[k] = __ldg(evec + sl[k]);
+   double acc = overwrite ? v[0] : add<EXACT>(y[d], v[0]);
+#pragma unroll
+   for (int k = 1; k < C; k++) acc = add<EXACT>(acc, v[k]);
+   if (ess_out && bit_set(ess_out, d)) acc = __ldg(x + d);
+   y[d] = acc;
+   return want_dot ? mul<EXACT>(__ldg(x + d), acc) : 0.0;
+}
+
 template <bool EXACT>
 __global__ void __launch_bounds__(kScatterThreads)
-scatter_kernel(const int32_t *__restrict__ dofs, const int32_t *__restrict__ off,
-               const uint32_t *__restrict__ slots, int64_t n_shared,
-               const double *__restrict__ evec, const double *__restrict__ x, double *y,
-               int overwrite, const uint32_t *ess_out, double *partials, const int *done)
+scatter_kernel(const BucketArgs B, const double *__restrict__ evec, const double *__restrict__ x,
+               double *y, int overwrite, const uint32_t *ess_out, DotSink dot, const int *done)
 {
    if (done && *done) return;
-   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-   double dot = 0.0;
-   if (s < n_shared) {
-      const int32_t d = __ldg(dofs + s);
-      const int beg = __ldg(off + s), end = __ldg(off + s + 1);
-      double acc = __ldg(evec + __ldg(slots + beg));
-      if (!overwrite) acc = add<EXACT>(y[d], acc);
-      for (int k = beg + 1; k < end; k++) acc = add<EXACT>(acc, __ldg(evec + __ldg(slots + k)));
-      if (ess_out && bit_set(ess_out, d)) acc = __ldg(x + d);
-      y[d] = acc;
-      if (partials) dot = mul<EXACT>(__ldg(x + d), acc);
+   int b = 0;
+   while (b + 1 < B.nb && (int64_t)blockIdx.x >= B.start[b + 1]) b++;
+   const int64_t s = ((int64_t)blockIdx.x - B.start[b]) * kScatterThreads + threadIdx.x;
+   double dv = 0.0;
+   if (s < B.n[b]) {
+      const bool wd = static_cast<bool>(dot);
+      switch (B.c[b]) {
+      case 2: dv = scatter_row<EXACT, 2>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
+      case 3: dv = scatter_row<EXACT, 3>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
+      case 4: dv = scatter_row<EXACT, 4>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
+      case 5: dv = scatter_row<EXACT, 5>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
+      case 6: dv = scatter_row<EXACT, 6>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
+      case 7: dv = scatter_row<EXACT, 7>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
+      case 8: dv = scatter_row<EXACT, 8>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
+      }
    }
-   if (partials) {
-      const double t = block_sum<kScatterThreads>(dot);
-      if (threadIdx.x == 0) partials[blockIdx.x] = t;
+   if (dot) {
+      const double v[1] = {dv};
+      emit<kScatterThreads, 1>(dot, v);
    }
+}
+
+BucketArgs bucket_args(const tfem_restriction *r)
+{
+   BucketArgs B{};
+   B.nb = r->n_buckets;
+   int64_t blk = 0;
+   for (int b = 0; b < r->n_buckets; b++) {
+      B.c[b] = r->buckets[b].c;
+      B.n[b] = r->buckets[b].n;
+      B.dofs[b] = r->buckets[b].dofs;
+      B.slots[b] = r->buckets[b].slots;
+      B.start[b] = blk;
+      blk += blocks_for(r->buckets[b].n, kScatterThreads);
+   }
+   B.start[r->n_buckets] = blk;
+   return B;
 }
 
 // -------------------------------------------------------------- diagonal
@@ -138,13 +210,36 @@ unsigned elem_blocks(const KernelPick &k, int64_t ne) { return blocks_for(ne, k.
 
 } // namespace
 
-int64_t pa_apply_partials(const tfem_pa *pa, const tfem_restriction *r)
+int64_t scatter_grid(const tfem_restriction *r) { return bucket_args(r).start[r->n_buckets]; }
+
+int64_t scatter_shared(tfem_ctx *ctx, const tfem_restriction *r, const double *evec,
+                       const double *x, double *y, bool overwrite, const uint32_t *ess_out,
+                       const DotSink *dot, const int *done, bool exact)
 {
-   return elem_blocks(pick(pa->ctx, pa), pa->ne) + blocks_for(r->n_shared, kScatterThreads);
+   const BucketArgs B = bucket_args(r);
+   const int64_t grid = B.start[r->n_buckets];
+   if (grid == 0) return 0;
+   const DotSink sink = dot ? *dot : DotSink{};
+   if (exact)
+      scatter_kernel<true><<<(unsigned)grid, kScatterThreads, 0, ctx->stream>>>(
+         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done);
+   else
+      scatter_kernel<false><<<(unsigned)grid, kScatterThreads, 0, ctx->stream>>>(
+         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done);
+   ctx->launched();
+   TFEM_CUDA(cudaGetLastError());
+   return grid;
 }
 
-int64_t pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const double *x,
-                 double *y, const ApplyFlags &f)
+void pa_apply_grids(const tfem_pa *pa, const tfem_restriction *r, int64_t *g_elem,
+                    int64_t *g_scatter)
+{
+   *g_elem = elem_blocks(pick(pa->ctx, pa), pa->ne);
+   *g_scatter = scatter_grid(r);
+}
+
+void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const double *x,
+              double *y, const ApplyFlags &f)
 {
    if (pa->dim != r->dim || pa->p != r->p || pa->ne != r->ne)
       invalid("forms: point factors were built for a different space");
@@ -163,29 +258,14 @@ int64_t pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, co
    a.overwrite = f.overwrite ? 1 : 0;
    a.mask_in = f.mask_in;
    a.ess_out = f.ess_out;
-   a.partials = f.dot_partials;
+   a.dot = f.dot;
    a.done = f.done;
-   const unsigned nb = elem_blocks(k, pa->ne);
-   k.launch(a, ctx->stream, nb);
+   k.launch(a, ctx->stream, elem_blocks(k, pa->ne));
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
-   int64_t n_part = nb;
-   if (r->n_shared > 0) {
-      const unsigned sb = blocks_for(r->n_shared, kScatterThreads);
-      double *sp = f.dot_partials ? f.dot_partials + nb : nullptr;
-      if (exact)
-         scatter_kernel<true><<<sb, kScatterThreads, 0, ctx->stream>>>(
-            r->shared_dofs, r->shared_off, r->shared_slots, r->n_shared, a.evec, x, y,
-            a.overwrite, f.ess_out, sp, f.done);
-      else
-         scatter_kernel<false><<<sb, kScatterThreads, 0, ctx->stream>>>(
-            r->shared_dofs, r->shared_off, r->shared_slots, r->n_shared, a.evec, x, y,
-            a.overwrite, f.ess_out, sp, f.done);
-      ctx->launched();
-      TFEM_CUDA(cudaGetLastError());
-      n_part += sb;
-   }
-   return n_part;
+   if (r->n_shared > 0)
+      scatter_shared(ctx, r, a.evec, x, y, f.overwrite, f.ess_out,
+                     f.dot_scatter ? &f.dot_scatter : nullptr, f.done, exact);
 }
 
 void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, double *diag)
@@ -205,14 +285,8 @@ void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, do
                                                  pa->qdata, r->gmap, elem_major, evec, diag);
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
-   if (r->n_shared > 0) {
-      const unsigned sb = blocks_for(r->n_shared, kScatterThreads);
-      scatter_kernel<true><<<sb, kScatterThreads, 0, ctx->stream>>>(
-         r->shared_dofs, r->shared_off, r->shared_slots, r->n_shared, evec, nullptr, diag, 0,
-         nullptr, nullptr, nullptr);
-      ctx->launched();
-      TFEM_CUDA(cudaGetLastError());
-   }
+   if (r->n_shared > 0)
+      scatter_shared(ctx, r, evec, nullptr, diag, false, nullptr, nullptr, nullptr, true);
 }
 
 } // namespace tfem

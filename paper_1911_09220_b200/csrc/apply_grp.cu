@@ -132,21 +132,14 @@ __global__ void apply2d_grp_kernel(const ApplyArgs a)
          if (!a.overwrite) r = add<EXACT>(a.y[d], r);
          if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
          a.y[d] = r;
-         if (a.partials) dot = mul<EXACT>(__ldg(a.x + d), r);
+         if (a.dot) dot = mul<EXACT>(__ldg(a.x + d), r);
       } else {
          a.evec[e * ND + t] = r;
       }
    }
-   if (a.partials) {
-      __shared__ double part[32];
-      for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
-      if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = dot;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-         double s = 0.0;
-         for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += part[w];
-         a.partials[blockIdx.x] = s;
-      }
+   if (a.dot) {
+      const double v[1] = {dot};
+      emit<NT * groups_for(NT), 1>(a.dot, v);
    }
 }
 
@@ -303,27 +296,18 @@ __global__ void apply3d_kernel(const ApplyArgs a)
             if (!a.overwrite) r += a.y[d];
             if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
             a.y[d] = r;
-            if (a.partials) dot = fma(__ldg(a.x + d), r, dot);
+            if (a.dot) dot = fma(__ldg(a.x + d), r, dot);
          } else {
             a.evec[e * ND + i] = r;
          }
       }
    }
-   if (a.partials) {
-      __shared__ double part[32];
-      for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
-      if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = dot;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-         double s = 0.0;
-         for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += part[w];
-         a.partials[blockIdx.x] = s;
-      }
+   if (a.dot) {
+      const double v[1] = {dot};
+      emit<NT * groups_for(NT), 1>(a.dot, v);
    }
 }
 
-// Elements per block so a block has ~256 threads.
-constexpr int groups_for(int nt) { return nt >= 256 ? 1 : 256 / nt; }
 
 template <typename K>
 void set_smem(K kernel, size_t bytes)

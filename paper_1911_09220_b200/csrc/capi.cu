@@ -564,7 +564,7 @@ int tfem_operator_mult(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *x
       if (!x || !y || x->n != op->n || y->n != op->n)
          invalid("BilinearForm::mult_true: size mismatch");
       if (x->d == y->d) invalid("BilinearForm::mult_true: x and y must not alias");
-      operator_mult(ctx, op, x->d, y->d, nullptr, nullptr);
+      operator_mult(ctx, op, x->d, y->d, nullptr, nullptr, nullptr);
       TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
    });
 }
@@ -578,7 +578,7 @@ int tfem_operator_mult_async(tfem_ctx *ctx, const tfem_operator *op, const tfem_
       if (!x || !y || x->n != op->n || y->n != op->n)
          invalid("BilinearForm::mult_true: size mismatch");
       if (x->d == y->d) invalid("BilinearForm::mult_true: x and y must not alias");
-      operator_mult(ctx, op, x->d, y->d, nullptr, nullptr);
+      operator_mult(ctx, op, x->d, y->d, nullptr, nullptr, nullptr);
    });
 }
 

@@ -45,33 +45,29 @@ __global__ void fill_kernel(double *d, int64_t n, double v)
 }
 
 __global__ void __launch_bounds__(kVecThreads)
-dot_kernel(const double *a, const double *b, int64_t n, double *partials)
+dot_kernel(const double *__restrict__ a, const double *__restrict__ b, int64_t n, DotSink sink)
 {
    double s = 0.0;
    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
         i += (int64_t)gridDim.x * blockDim.x)
       s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
-   const double t = block_sum<kVecThreads>(s);
-   if (threadIdx.x == 0) partials[blockIdx.x] = t;
+   const double v[1] = {s};
+   emit<kVecThreads, 1>(sink, v);
 }
 
-// Deterministic fixed-order sum of `n` partials by one block.
-__device__ double sum_partials(const double *p, int64_t n)
+// Fixed-order fold of `n` chunk sums by one block (valid in thread 0).
+__device__ double fold(const double *p, int64_t n)
 {
    double s = 0.0;
-   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += p[i];
+   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += __ldcg(p + i);
    return block_sum<kVecThreads>(s);
 }
 
 __global__ void __launch_bounds__(kVecThreads)
-reduce_kernel(const double *partials, int64_t n, int k, double *out)
+fold_kernel(const double *chunks, int64_t n, double *out)
 {
-   // k interleaved sums: partials laid out [k][n]
-   for (int j = 0; j < k; j++) {
-      const double s = sum_partials(partials + j * n, n);
-      if (threadIdx.x == 0) out[j] = s;
-      __syncthreads();
-   }
+   const double s = fold(chunks, n);
+   if (threadIdx.x == 0) out[0] = s;
 }
 
 __global__ void axpy_kernel(double a, const double *x, double *y, int64_t n)
@@ -81,7 +77,6 @@ __global__ void axpy_kernel(double a, const double *x, double *y, int64_t n)
       y[i] = __dadd_rn(y[i], __dmul_rn(a, x[i]));
 }
 
-// y[ess] = x[ess] style helpers
 __global__ void set_bits_kernel(const int32_t *list, int64_t n, uint32_t *mask)
 {
    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -97,7 +92,7 @@ __global__ void set_values_kernel(const int32_t *list, int64_t n, double v, doub
 // SparseMatrix::mult (sparse.cpp:75-87), thread per row, optional x.y partial.
 __global__ void __launch_bounds__(kVecThreads)
 csr_kernel(const int32_t *rowptr, const int32_t *cols, const double *vals, int64_t n,
-           const double *x, double *y, double *partials, const int *done)
+           const double *x, double *y, DotSink sink, const int *done)
 {
    if (done && *done) return;
    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -108,9 +103,9 @@ csr_kernel(const int32_t *rowptr, const int32_t *cols, const double *vals, int64
       y[i] = s;
       dot = __dmul_rn(x[i], s);
    }
-   if (partials) {
-      const double t = block_sum<kVecThreads>(dot);
-      if (threadIdx.x == 0) partials[blockIdx.x] = t;
+   if (sink) {
+      const double v[1] = {dot};
+      emit<kVecThreads, 1>(sink, v);
    }
 }
 
@@ -130,8 +125,9 @@ __device__ __forceinline__ int next_buffer(int cur, int best)
 
 // r = b, z = M r, p = z, x0 = 0; partials of r.r and r.z (solvers.cpp:43-58)
 __global__ void __launch_bounds__(kVecThreads)
-cg_init_kernel(const double *b, const double *diag, int64_t n, double *r, double *p, double *x,
-               double *partials /* [2][gridDim] */)
+cg_init_kernel(const double *__restrict__ b, const double *__restrict__ diag, int64_t n,
+               double *__restrict__ r, double *__restrict__ p, double *__restrict__ x,
+               DotSink sink)
 {
    double rr = 0.0, rz = 0.0;
    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -144,20 +140,15 @@ cg_init_kernel(const double *b, const double *diag, int64_t n, double *r, double
       rr = __dadd_rn(rr, __dmul_rn(ri, ri));
       rz = __dadd_rn(rz, __dmul_rn(ri, zi));
    }
-   const double a = block_sum<kVecThreads>(rr);
-   const double c = block_sum<kVecThreads>(rz);
-   if (threadIdx.x == 0) {
-      partials[blockIdx.x] = a;
-      partials[gridDim.x + blockIdx.x] = c;
-   }
+   const double v[2] = {rr, rz};
+   emit<kVecThreads, 2>(sink, v);
 }
 
 __global__ void __launch_bounds__(kVecThreads)
-cg_init_finish_kernel(const double *partials, int64_t nb, CgState *st)
+cg_init_finish_kernel(const double *chunks, int64_t nch, CgState *st)
 {
-   const double rr = sum_partials(partials, nb);
-   __syncthreads();
-   const double rz = sum_partials(partials + nb, nb);
+   const double rr = fold(chunks, nch);
+   const double rz = fold(chunks + nch, nch);
    if (threadIdx.x == 0) {
       st->rz = rz;
       st->rnorm = sqrt(rr);
@@ -177,11 +168,15 @@ cg_init_finish_kernel(const double *partials, int64_t nb, CgState *st)
    }
 }
 
+// pq = (element-kernel chunks) + (scatter chunks) in a fixed order.
 __global__ void __launch_bounds__(kVecThreads)
-cg_alpha_kernel(const double *partials, int64_t nb, CgState *st)
+cg_alpha_kernel(const double *ch_a, int64_t na, const double *ch_b, int64_t nb, CgState *st)
 {
    if (st->done) return;
-   const double pq = sum_partials(partials, nb);
+   double s = 0.0;
+   for (int64_t i = threadIdx.x; i < na + nb; i += blockDim.x)
+      s += __ldcg(i < na ? ch_a + i : ch_b + (i - na));
+   const double pq = block_sum<kVecThreads>(s);
    if (threadIdx.x == 0) {
       const double alpha = st->rz / pq;
       st->alpha = alpha;
@@ -196,17 +191,45 @@ struct XBufs {
    double *x[3];
 };
 
+constexpr int kUnroll = 4;
+
+// x' = x + alpha p, r -= alpha q, z = r / d; partials of r.r, r.z.  Four
+// independent elements per trip keep ~20 loads in flight per thread.
 __global__ void __launch_bounds__(kVecThreads)
-cg_update_kernel(const CgState *st, XBufs xb, const double *p, const double *q, double *r,
-                 const double *diag, int64_t n, double *partials /* [2][gridDim] */)
+cg_update_kernel(const CgState *st, XBufs xb, const double *__restrict__ p,
+                 const double *__restrict__ q, double *__restrict__ r,
+                 const double *__restrict__ diag, int64_t n, DotSink sink)
 {
    if (st->done) return;
    const double alpha = st->alpha, nalpha = -alpha;
-   const double *xc = xb.x[st->cur];
-   double *xn = xb.x[next_buffer(st->cur, st->best)];
+   const double *__restrict__ xc = xb.x[st->cur];
+   double *__restrict__ xn = xb.x[next_buffer(st->cur, st->best)];
    double rr = 0.0, rz = 0.0;
-   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-        i += (int64_t)gridDim.x * blockDim.x) {
+   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+      double xv[kUnroll], pv[kUnroll], rv[kUnroll], qv[kUnroll], dv[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+         const int64_t j = i + u * stride;
+         xv[u] = xc[j];
+         pv[u] = p[j];
+         rv[u] = r[j];
+         qv[u] = q[j];
+         dv[u] = diag ? diag[j] : 1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+         const int64_t j = i + u * stride;
+         xn[j] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));
+         const double ri = __dadd_rn(rv[u], __dmul_rn(nalpha, qv[u]));
+         r[j] = ri;
+         const double zi = diag ? __ddiv_rn(ri, dv[u]) : ri;
+         rr = __dadd_rn(rr, __dmul_rn(ri, ri));
+         rz = __dadd_rn(rz, __dmul_rn(ri, zi));
+      }
+   }
+   for (; i < n; i += stride) {
       xn[i] = __dadd_rn(xc[i], __dmul_rn(alpha, p[i]));
       const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, q[i]));
       r[i] = ri;
@@ -214,21 +237,16 @@ cg_update_kernel(const CgState *st, XBufs xb, const double *p, const double *q, 
       rr = __dadd_rn(rr, __dmul_rn(ri, ri));
       rz = __dadd_rn(rz, __dmul_rn(ri, zi));
    }
-   const double a = block_sum<kVecThreads>(rr);
-   const double c = block_sum<kVecThreads>(rz);
-   if (threadIdx.x == 0) {
-      partials[blockIdx.x] = a;
-      partials[gridDim.x + blockIdx.x] = c;
-   }
+   const double v[2] = {rr, rz};
+   emit<kVecThreads, 2>(sink, v);
 }
 
 __global__ void __launch_bounds__(kVecThreads)
-cg_beta_kernel(const double *partials, int64_t nb, CgState *st)
+cg_beta_kernel(const double *chunks, int64_t nch, CgState *st)
 {
    if (st->done) return;
-   const double rr = sum_partials(partials, nb);
-   __syncthreads();
-   const double rz_next = sum_partials(partials + nb, nb);
+   const double rr = fold(chunks, nch);
+   const double rz_next = fold(chunks + nch, nch);
    if (threadIdx.x != 0) return;
    const double rnorm = sqrt(rr);
    st->rnorm = rnorm;
@@ -257,13 +275,31 @@ cg_beta_kernel(const double *partials, int64_t nb, CgState *st)
    }
 }
 
-__global__ void cg_direction_kernel(const CgState *st, const double *r, const double *diag,
-                                    double *p, int64_t n)
+// p = z + beta p with z = r / d (solvers.cpp:84-87)
+__global__ void __launch_bounds__(kVecThreads)
+cg_direction_kernel(const CgState *st, const double *__restrict__ r,
+                    const double *__restrict__ diag, double *__restrict__ p, int64_t n)
 {
    if (st->done) return;
    const double beta = st->beta;
-   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-        i += (int64_t)gridDim.x * blockDim.x) {
+   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+      double rv[kUnroll], dv[kUnroll], pv[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+         const int64_t j = i + u * stride;
+         rv[u] = r[j];
+         dv[u] = diag ? diag[j] : 1.0;
+         pv[u] = p[j];
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+         const double zi = diag ? __ddiv_rn(rv[u], dv[u]) : rv[u];
+         p[i + u * stride] = __dadd_rn(zi, __dmul_rn(beta, pv[u]));
+      }
+   }
+   for (; i < n; i += stride) {
       const double zi = diag ? __ddiv_rn(r[i], diag[i]) : r[i];
       p[i] = __dadd_rn(zi, __dmul_rn(beta, p[i]));
    }
@@ -284,12 +320,33 @@ T *dalloc(int64_t n)
    return p;
 }
 
+// Device storage of a DotSink for `grid` blocks and `nv` values per block.
+struct SinkStore {
+   DotSink s;
+   int64_t grid = 0, nch = 0;
+   void alloc(int64_t g, int nv)
+   {
+      grid = g;
+      nch = n_chunks(g);
+      s.partials = dalloc<double>(nv * g);
+      s.chunks = dalloc<double>(nv * nch);
+      s.tickets = dalloc<unsigned>(nch);
+      TFEM_CUDA(cudaMemset(s.tickets, 0, sizeof(unsigned) * nch));
+   }
+   void release()
+   {
+      cudaFree(s.partials);
+      cudaFree(s.chunks);
+      cudaFree(s.tickets);
+      s = DotSink{};
+   }
+};
+
 // Per-operator CG workspace, reused across solves (vectors + graph).
 struct Workspace {
    int64_t n = 0;
    double *r = nullptr, *p = nullptr, *q = nullptr, *xa = nullptr, *xb = nullptr;
-   double *part_op = nullptr, *part_vec = nullptr;
-   int64_t n_op_part = 0;
+   SinkStore s_elem, s_scatter, s_vec;
    CgState *st = nullptr;
    CgState *host_st = nullptr; // pinned
    cudaGraphExec_t graph = nullptr;
@@ -303,8 +360,9 @@ struct Workspace {
       cudaFree(q);
       cudaFree(xa);
       cudaFree(xb);
-      cudaFree(part_op);
-      cudaFree(part_vec);
+      s_elem.release();
+      s_scatter.release();
+      s_vec.release();
       cudaFree(st);
       if (host_st) cudaFreeHost(host_st);
       if (graph) cudaGraphExecDestroy(graph);
@@ -315,12 +373,6 @@ std::unordered_map<const tfem_operator *, std::unique_ptr<Workspace>> &workspace
 {
    static std::unordered_map<const tfem_operator *, std::unique_ptr<Workspace>> w;
    return w;
-}
-
-int64_t op_partials(const tfem_operator *op)
-{
-   if (op->csr) return blocks_for(op->n, kVecThreads);
-   return pa_apply_partials(op->pa.back(), op->r);
 }
 
 Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
@@ -335,9 +387,17 @@ Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
    w->q = dalloc<double>(op->n);
    w->xa = dalloc<double>(op->n);
    w->xb = dalloc<double>(op->n);
-   w->n_op_part = op_partials(op);
-   w->part_op = dalloc<double>(w->n_op_part);
-   w->part_vec = dalloc<double>(2 * static_cast<int64_t>(ctx->sm_count) * 8);
+   if (op->csr) {
+      w->s_elem.alloc(blocks_for(op->n, kVecThreads), 1);
+   } else {
+      // everything the iteration touches must exist before graph capture
+      if (op->r->n_shared > 0) const_cast<tfem_restriction *>(op->r)->ensure_evec();
+      int64_t ge = 0, gs = 0;
+      pa_apply_grids(op->pa.back(), op->r, &ge, &gs);
+      w->s_elem.alloc(ge, 1);
+      if (gs > 0) w->s_scatter.alloc(gs, 1);
+   }
+   w->s_vec.alloc(vec_blocks(ctx, op->n), 2);
    w->st = dalloc<CgState>(1);
    TFEM_CUDA(cudaMallocHost(&w->host_st, sizeof(CgState)));
    auto &ref = *w;
@@ -346,23 +406,22 @@ Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
 }
 
 // One CG iteration's launches (used eagerly and under stream capture).
-int64_t enqueue_iteration(tfem_ctx *ctx, const tfem_operator *op, Workspace &w, XBufs xb,
-                          const double *diag)
+void enqueue_iteration(tfem_ctx *ctx, const tfem_operator *op, Workspace &w, XBufs xb,
+                       const double *diag)
 {
    const int64_t n = op->n;
-   int64_t launches = 0;
-   const int64_t before = ctx->launches;
-   const int64_t np = operator_mult(ctx, op, w.p, w.q, w.part_op, &w.st->done);
-   cg_alpha_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.part_op, np, w.st);
+   operator_mult(ctx, op, w.p, w.q, &w.s_elem.s, w.s_scatter.grid ? &w.s_scatter.s : nullptr,
+                 &w.st->done);
+   cg_alpha_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_elem.s.chunks, w.s_elem.nch,
+                                                       w.s_scatter.s.chunks, w.s_scatter.nch,
+                                                       w.st);
    const unsigned vb = vec_blocks(ctx, n);
    cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.p, w.q, w.r, diag, n,
-                                                         w.part_vec);
-   cg_beta_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.part_vec, vb, w.st);
+                                                         w.s_vec.s);
+   cg_beta_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, w.st);
    cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.r, diag, w.p, n);
    ctx->launched(4);
    TFEM_CUDA(cudaGetLastError());
-   launches = ctx->launches - before;
-   return launches;
 }
 
 } // namespace
@@ -376,10 +435,17 @@ void vec_fill(tfem_ctx *ctx, double *d, int64_t n, double v)
 
 double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n)
 {
+   static thread_local std::unordered_map<int64_t, SinkStore> sinks;
    const unsigned nb = vec_blocks(ctx, n);
-   ctx->ensure_partials(nb + 1);
-   dot_kernel<<<nb, kVecThreads, 0, ctx->stream>>>(a, b, n, ctx->red.partials);
-   reduce_kernel<<<1, kVecThreads, 0, ctx->stream>>>(ctx->red.partials, nb, 1, ctx->scalars);
+   auto it = sinks.find(nb);
+   if (it == sinks.end()) {
+      SinkStore st;
+      st.alloc(nb, 1);
+      it = sinks.emplace(nb, st).first;
+   }
+   const SinkStore &s = it->second;
+   dot_kernel<<<nb, kVecThreads, 0, ctx->stream>>>(a, b, n, s.s);
+   fold_kernel<<<1, kVecThreads, 0, ctx->stream>>>(s.s.chunks, s.nch, ctx->scalars);
    ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
    TFEM_CUDA(cudaMemcpyAsync(ctx->host_scalars, ctx->scalars, sizeof(double),
@@ -449,28 +515,27 @@ void operator_release(tfem_operator *op)
 // integrators in insertion order, the first overwriting y, later ones
 // accumulating; essential DOFs masked on input for all and overwritten on
 // output by the last (which also produces the fused x . y partials).
-int64_t operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, double *y,
-                      double *dot_partials, const int *done)
+void operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, double *y,
+                   const DotSink *dot_elem, const DotSink *dot_scatter, const int *done)
 {
    if (op->csr) {
       csr_kernel<<<blocks_for(op->n, kVecThreads), kVecThreads, 0, ctx->stream>>>(
-         op->rowptr, op->cols, op->vals, op->n, x, y, dot_partials, done);
+         op->rowptr, op->cols, op->vals, op->n, x, y, dot_elem ? *dot_elem : DotSink{}, done);
       ctx->launched();
       TFEM_CUDA(cudaGetLastError());
-      return blocks_for(op->n, kVecThreads);
+      return;
    }
-   int64_t np = 0;
    for (size_t k = 0; k < op->pa.size(); k++) {
       ApplyFlags f;
       f.overwrite = (k == 0);
       f.mask_in = op->ess_mask;
       const bool last = (k + 1 == op->pa.size());
       f.ess_out = last ? op->ess_mask : nullptr;
-      f.dot_partials = last ? dot_partials : nullptr;
+      if (last && dot_elem) f.dot = *dot_elem;
+      if (last && dot_scatter) f.dot_scatter = *dot_scatter;
       f.done = done;
-      np = pa_apply(ctx, op->pa[k], op->r, x, y, f);
+      pa_apply(ctx, op->pa[k], op->r, x, y, f);
    }
-   return np;
 }
 
 void operator_diagonal(tfem_ctx *ctx, const tfem_operator *op, double *diag)
@@ -535,8 +600,8 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
    init.max_iters = max_iters;
    TFEM_CUDA(cudaMemcpyAsync(w.st, &init, sizeof(CgState), cudaMemcpyHostToDevice, ctx->stream));
    const unsigned vb = vec_blocks(ctx, n);
-   cg_init_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(b, diag, n, w.r, w.p, x, w.part_vec);
-   cg_init_finish_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.part_vec, vb, w.st);
+   cg_init_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(b, diag, n, w.r, w.p, x, w.s_vec.s);
+   cg_init_finish_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, w.st);
    ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
    const XBufs xb{{x, w.xa, w.xb}};

@@ -87,10 +87,18 @@ struct tfem_restriction {
    // both gmap and the E-vector.
    bool elem_major = false;
    uint32_t *gmap = nullptr;
-   int64_t n_shared = 0;        // DOFs with >= 2 element slots
-   int32_t *shared_dofs = nullptr;
-   int32_t *shared_off = nullptr; // n_shared + 1
-   uint32_t *shared_slots = nullptr; // gmap / E-vector slots, sorted by element
+   // DOFs with >= 2 element slots, bucketed by slot count c (ELL per
+   // bucket): dofs[n] ascending, slots[n][c] sorted by element.
+   struct Bucket {
+      int c = 0;
+      int64_t n = 0;
+      int32_t *dofs = nullptr;
+      uint32_t *slots = nullptr; // gmap / E-vector slots
+   };
+   static constexpr int kMaxBuckets = 7; // c = 2..8
+   int n_buckets = 0;
+   Bucket buckets[kMaxBuckets];
+   int64_t n_shared = 0;
    double *evec = nullptr;       // E-vector scratch, gmap layout (lazy)
    bool cartesian = false;
    int n[3] = {0, 0, 0};
@@ -133,6 +141,17 @@ struct tfem_operator {
 
 namespace tfem {
 
+constexpr int kChunk = 32;
+
+struct DotSink {
+   double *partials = nullptr;   // [nv][grid]
+   double *chunks = nullptr;     // [nv][n_chunks]
+   unsigned *tickets = nullptr;  // [n_chunks], zero between launches
+   __host__ __device__ explicit operator bool() const { return partials != nullptr; }
+};
+
+__host__ __device__ inline int64_t n_chunks(int64_t grid) { return (grid + kChunk - 1) / kChunk; }
+
 // Host-side 1D tables (host_basis.cpp).
 std::vector<double> gauss_points(int rule, int n, std::vector<double> *weights);
 void basis_nodes(int p, int node_kind, std::vector<double> &nodes, std::vector<double> &bary);
@@ -150,20 +169,29 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
 void restriction_mult_transpose(tfem_ctx *ctx, const tfem_restriction *r, const double *e,
                                 double *l);
 
+// Shared-DOF scatter over the buckets (apply.cu): y[d] (+)= sum of the
+// E-vector slots of d in ascending element order; y[ess] = x[ess]; fused
+// x . y partials.  Returns the grid size (for the dot sink).
+int64_t scatter_shared(tfem_ctx *ctx, const tfem_restriction *r, const double *evec,
+                       const double *x, double *y, bool overwrite, const uint32_t *ess_out,
+                       const DotSink *dot, const int *done, bool exact);
+int64_t scatter_grid(const tfem_restriction *r);
+
 // PA kernels (apply.cu)
 struct ApplyFlags {
    bool overwrite = false;   // y = (else y +=)
    const uint32_t *mask_in = nullptr;  // zero gathered essential DOFs
    const uint32_t *ess_out = nullptr;  // y[ess] = x[ess]
-   double *dot_partials = nullptr;     // per-block partials of x . y
+   DotSink dot;                        // element-kernel x . y partials
+   DotSink dot_scatter;                // scatter-kernel x . y partials
    const int *done = nullptr;          // device flag: skip when set (CG)
 };
 // Launches the element kernel and (if needed) the shared-DOF scatter.
-// Returns the number of dot partials written (element blocks + scatter
-// blocks) when flags.dot_partials is set.
-int64_t pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const double *x,
-                 double *y, const ApplyFlags &f);
-int64_t pa_apply_partials(const tfem_pa *pa, const tfem_restriction *r);
+void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const double *x,
+              double *y, const ApplyFlags &f);
+// Grid sizes of the two launches of pa_apply (element kernel, scatter).
+void pa_apply_grids(const tfem_pa *pa, const tfem_restriction *r, int64_t *g_elem,
+                    int64_t *g_scatter);
 void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, double *diag);
 
 // Setup (setup.cu)
@@ -172,9 +200,9 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
 void geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq, int rule, double *host_xyz);
 
 // Operators / CG (cg.cu)
-// Returns the number of dot partials written when dot_partials is set.
-int64_t operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, double *y,
-                      double *dot_partials, const int *done);
+// With dot sinks set, the last integrator's launches emit x . y partials.
+void operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, double *y,
+                   const DotSink *dot_elem, const DotSink *dot_scatter, const int *done);
 void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
               int max_iters, const double *diag, double *x, tfem_cg_result *res,
               tfem_cg_callback cb, void *user);
@@ -209,6 +237,42 @@ __device__ __forceinline__ double block_sum(double v)
    }
    __syncthreads(); // warp_part may be reused by the next call
    return s;
+}
+
+// Deterministic two-level reduction of per-block values.  Every block writes
+// its block sums to partials[k][blockIdx]; the last block to finish in each
+// chunk of kChunk consecutive blocks (atomic ticket) folds the chunk's
+// partials in block order into chunks[k][chunk] and re-arms the ticket.  The
+// consumer then folds the few hundred chunk sums in a fixed order.  No
+// floating-point atomics anywhere, so results are bit-reproducible.
+template <int NT, int NV>
+__device__ __forceinline__ void emit(const DotSink &s, const double (&v)[NV])
+{
+   double tot[NV];
+#pragma unroll
+   for (int k = 0; k < NV; k++) tot[k] = block_sum<NT>(v[k]);
+   __shared__ int is_last;
+   const unsigned G = gridDim.x, chunk = blockIdx.x / kChunk;
+   if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; k++) s.partials[k * (int64_t)G + blockIdx.x] = tot[k];
+      __threadfence();
+      const unsigned nb = min((unsigned)kChunk, G - chunk * kChunk);
+      is_last = atomicAdd(s.tickets + chunk, 1u) == nb - 1;
+   }
+   __syncthreads();
+   if (is_last && threadIdx.x == 0) {
+      __threadfence();
+      const unsigned nb = min((unsigned)kChunk, G - chunk * kChunk);
+      const int64_t nch = n_chunks(G);
+#pragma unroll
+      for (int k = 0; k < NV; k++) {
+         double a = 0.0;
+         for (unsigned j = 0; j < nb; j++) a += __ldcg(s.partials + k * (int64_t)G + chunk * kChunk + j);
+         s.chunks[k * nch + chunk] = a;
+      }
+      s.tickets[chunk] = 0u;
+   }
 }
 
 // Exact (reference-order, unfused) or fused arithmetic.

@@ -23,7 +23,7 @@ struct ApplyArgs {
    int overwrite;
    const uint32_t *mask_in;
    const uint32_t *ess_out;
-   double *partials;
+   DotSink dot;     // fused x . y partials (CG's p . q)
    const int *done; // CG stop flag: skip the work once the solve has ended
 };
 
@@ -43,5 +43,8 @@ KernelPick pick_apply2d_reg(int p, int nq, int kind, bool exact);
 KernelPick pick_apply_grp(int dim, int p, int nq, int kind, bool exact);
 
 constexpr __host__ __device__ int round32(int v) { return ((v + 31) / 32) * 32; }
+
+// Elements per block of the group kernels so a block has ~256 threads.
+constexpr __host__ __device__ int groups_for(int nt) { return nt >= 256 ? 1 : 256 / nt; }
 
 } // namespace tfem

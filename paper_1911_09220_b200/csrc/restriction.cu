@@ -153,16 +153,6 @@ __global__ void count_kernel(const uint32_t *gmap, Layout L, int32_t *counts)
    atomicAdd(counts + (gmap[L.live(t)] & kDofMask), 1);
 }
 
-__global__ void flag_kernel(const int32_t *counts, int64_t ndofs, int32_t *is_shared,
-                            int32_t *shared_count)
-{
-   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-   if (d >= ndofs) return;
-   const int c = counts[d];
-   is_shared[d] = c >= 2 ? 1 : 0;
-   shared_count[d] = c >= 2 ? c : 0;
-}
-
 __global__ void mark_exclusive_kernel(uint32_t *gmap, Layout L, const int32_t *counts)
 {
    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -172,54 +162,58 @@ __global__ void mark_exclusive_kernel(uint32_t *gmap, Layout L, const int32_t *c
    if (counts[g & kDofMask] == 1) gmap[s] = g | kExclusive;
 }
 
-// rank[d] = position of shared DOF d in the compact list (from the scan of
-// is_shared), slot_base[d] = offset of its slot list.
-__global__ void fill_slots_kernel(const uint32_t *gmap, Layout L, const int32_t *rank,
-                                  const int32_t *is_shared, const int32_t *off, int32_t *fill,
-                                  uint32_t *slots)
+__global__ void flag_count_kernel(const int32_t *counts, int64_t ndofs, int c, int32_t *flag)
+{
+   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (d < ndofs) flag[d] = counts[d] == c ? 1 : 0;
+}
+
+// Position of every shared DOF inside its bucket: bucket_of[d] / rank[d].
+__global__ void rank_kernel(const int32_t *flag, const int32_t *scan, int64_t ndofs, int b,
+                            int8_t *bucket_of, int32_t *rank, int32_t *dofs)
+{
+   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (d >= ndofs || !flag[d]) return;
+   bucket_of[d] = static_cast<int8_t>(b);
+   rank[d] = scan[d];
+   dofs[scan[d]] = static_cast<int32_t>(d);
+}
+
+struct BucketPtrs {
+   int c[tfem_restriction::kMaxBuckets];
+   uint32_t *slots[tfem_restriction::kMaxBuckets];
+};
+
+__global__ void fill_slots_kernel(const uint32_t *gmap, Layout L, const int8_t *bucket_of,
+                                  const int32_t *rank, int32_t *fill, BucketPtrs bp)
 {
    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    if (t >= L.ne * L.nd) return;
    const int64_t s = L.live(t);
    const uint32_t d = gmap[s] & kDofMask;
-   if (!is_shared[d]) return;
-   const int r = rank[d];
-   const int pos = off[r] + atomicAdd(fill + r, 1);
-   slots[pos] = static_cast<uint32_t>(s);
+   const int b = bucket_of[d];
+   if (b < 0) return;
+   const int c = bp.c[b];
+   const int pos = atomicAdd(fill + d, 1);
+   bp.slots[b][(int64_t)rank[d] * c + pos] = static_cast<uint32_t>(s);
 }
 
-__global__ void compact_shared_kernel(const int32_t *is_shared, const int32_t *rank,
-                                      int64_t ndofs, int32_t *shared_dofs)
-{
-   const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-   if (d >= ndofs || !is_shared[d]) return;
-   shared_dofs[rank[d]] = static_cast<int32_t>(d);
-}
-
-__global__ void gather_off_kernel(const int32_t *sd, const int32_t *full, int64_t ns,
-                                  int32_t *out)
+// Rows are tiny (c <= 8): insertion-sort each by element so the scatter adds
+// contributions in ascending element order (forms.cpp:289-295).
+__global__ void sort_rows_kernel(uint32_t *slots, int64_t n, int c, Layout L)
 {
    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-   if (s < ns) out[s] = full[sd[s]];
-}
-
-// Slot lists are tiny (<= 2^dim); insertion-sort each by element so the
-// scatter adds contributions in ascending element order.
-__global__ void sort_slots_kernel(const int32_t *off, int64_t n_shared, Layout L,
-                                  uint32_t *slots)
-{
-   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-   if (s >= n_shared) return;
-   const int beg = off[s], end = off[s + 1];
-   for (int a = beg + 1; a < end; a++) {
-      const uint32_t v = slots[a];
+   if (s >= n) return;
+   uint32_t *row = slots + s * c;
+   for (int a = 1; a < c; a++) {
+      const uint32_t v = row[a];
       const int64_t key = L.elem_of(v);
       int b = a - 1;
-      while (b >= beg && L.elem_of(slots[b]) > key) {
-         slots[b + 1] = slots[b];
+      while (b >= 0 && L.elem_of(row[b]) > key) {
+         row[b + 1] = row[b];
          b--;
       }
-      slots[b + 1] = v;
+      row[b + 1] = v;
    }
 }
 
@@ -242,19 +236,12 @@ __global__ void exclusive_add_kernel(const uint32_t *gmap, Layout L,
    if (g & kExclusive) l[g & kDofMask] += evec[t];
 }
 
-__global__ void shared_add_kernel(const int32_t *shared_dofs, const int32_t *off,
-                                  const uint32_t *slots, int64_t n_shared, Layout L,
-                                  const double *evec /* [e][i] */, double *l)
+// API E-vector [e][i] -> internal gmap layout.
+__global__ void to_internal_kernel(Layout L, const double *api, double *evec)
 {
-   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-   if (s >= n_shared) return;
-   const int32_t d = shared_dofs[s];
-   double acc = l[d];
-   for (int k = off[s]; k < off[s + 1]; k++) {
-      const uint32_t slot = slots[k];
-      acc += evec[L.elem_of(slot) * L.nd + L.local_of(slot)];
-   }
-   l[d] = acc;
+   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (t >= L.ne * L.nd) return;
+   evec[L.slot(static_cast<int>(t % L.nd), t / L.nd)] = api[t];
 }
 
 // Boundary of a Cartesian mesh: DOFs at lattice positions on the domain
@@ -320,58 +307,57 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
    const Layout L{elem_major, r->nd, ne, r->ne_pad};
    cudaStream_t s = ctx->stream;
 
-   int32_t *counts = dalloc<int32_t>(ndofs), *is_shared = dalloc<int32_t>(ndofs);
-   int32_t *shared_count = dalloc<int32_t>(ndofs), *rank = dalloc<int32_t>(ndofs + 1);
-   int32_t *slot_off_full = dalloc<int32_t>(ndofs + 1);
+   int32_t *counts = dalloc<int32_t>(ndofs), *flag = dalloc<int32_t>(ndofs);
+   int32_t *scan = dalloc<int32_t>(ndofs), *rank = dalloc<int32_t>(ndofs);
+   int8_t *bucket_of = dalloc<int8_t>(ndofs);
    TFEM_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * ndofs, s));
+   TFEM_CUDA(cudaMemsetAsync(bucket_of, 0xff, ndofs, s));
    count_kernel<<<blocks_for(nslots), kThreads, 0, s>>>(gmap, L, counts);
-   flag_kernel<<<blocks_for(ndofs), kThreads, 0, s>>>(counts, ndofs, is_shared, shared_count);
    mark_exclusive_kernel<<<blocks_for(nslots), kThreads, 0, s>>>(gmap, L, counts);
-   ctx->launched(3);
-   TFEM_CUDA(cudaGetLastError());
-   exclusive_scan(ctx, is_shared, rank, ndofs);
-   exclusive_scan(ctx, shared_count, slot_off_full, ndofs);
-   int32_t last_rank = 0, last_flag = 0, last_off = 0, last_cnt = 0;
-   TFEM_CUDA(cudaMemcpy(&last_rank, rank + ndofs - 1, 4, cudaMemcpyDeviceToHost));
-   TFEM_CUDA(cudaMemcpy(&last_flag, is_shared + ndofs - 1, 4, cudaMemcpyDeviceToHost));
-   TFEM_CUDA(cudaMemcpy(&last_off, slot_off_full + ndofs - 1, 4, cudaMemcpyDeviceToHost));
-   TFEM_CUDA(cudaMemcpy(&last_cnt, shared_count + ndofs - 1, 4, cudaMemcpyDeviceToHost));
-   r->n_shared = last_rank + last_flag;
-   const int64_t n_shared_slots = static_cast<int64_t>(last_off) + last_cnt;
-
-   r->shared_dofs = dalloc<int32_t>(r->n_shared);
-   r->shared_off = dalloc<int32_t>(r->n_shared + 1);
-   r->shared_slots = dalloc<uint32_t>(n_shared_slots);
-   compact_shared_kernel<<<blocks_for(ndofs), kThreads, 0, s>>>(is_shared, rank, ndofs,
-                                                               r->shared_dofs);
-   // shared_off[rank[d]] = slot_off_full[d]; the last entry is the total.
-   if (r->n_shared > 0) {
-      gather_off_kernel<<<blocks_for(r->n_shared), kThreads, 0, s>>>(
-         r->shared_dofs, slot_off_full, r->n_shared, r->shared_off);
-      ctx->launched();
-   }
-   {
-      const int32_t total = static_cast<int32_t>(n_shared_slots);
-      TFEM_CUDA(cudaMemcpyAsync(r->shared_off + r->n_shared, &total, 4, cudaMemcpyHostToDevice, s));
-      TFEM_CUDA(cudaStreamSynchronize(s));
-   }
-   TFEM_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (r->n_shared > 0 ? r->n_shared : 1), s));
-   fill_slots_kernel<<<blocks_for(nslots), kThreads, 0, s>>>(gmap, L, rank, is_shared,
-                                                            r->shared_off, counts,
-                                                            r->shared_slots);
-   if (r->n_shared > 0) {
-      sort_slots_kernel<<<blocks_for(r->n_shared), kThreads, 0, s>>>(r->shared_off, r->n_shared,
-                                                                     L, r->shared_slots);
-      ctx->launched();
-   }
    ctx->launched(2);
+   TFEM_CUDA(cudaGetLastError());
+   BucketPtrs bp{};
+   const int cmax = dim == 2 ? 4 : 8;
+   for (int c = 2; c <= cmax; c++) {
+      flag_count_kernel<<<blocks_for(ndofs), kThreads, 0, s>>>(counts, ndofs, c, flag);
+      ctx->launched();
+      exclusive_scan(ctx, flag, scan, ndofs);
+      int32_t last_scan = 0, last_flag = 0;
+      TFEM_CUDA(cudaMemcpy(&last_scan, scan + ndofs - 1, 4, cudaMemcpyDeviceToHost));
+      TFEM_CUDA(cudaMemcpy(&last_flag, flag + ndofs - 1, 4, cudaMemcpyDeviceToHost));
+      const int64_t n = static_cast<int64_t>(last_scan) + last_flag;
+      if (n == 0) continue;
+      const int b = r->n_buckets++;
+      auto &bk = r->buckets[b];
+      bk.c = c;
+      bk.n = n;
+      bk.dofs = dalloc<int32_t>(n);
+      bk.slots = dalloc<uint32_t>(n * c);
+      rank_kernel<<<blocks_for(ndofs), kThreads, 0, s>>>(flag, scan, ndofs, b, bucket_of, rank,
+                                                        bk.dofs);
+      ctx->launched();
+      bp.c[b] = c;
+      bp.slots[b] = bk.slots;
+      r->n_shared += n;
+   }
+   TFEM_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * ndofs, s));
+   if (r->n_buckets > 0) {
+      fill_slots_kernel<<<blocks_for(nslots), kThreads, 0, s>>>(gmap, L, bucket_of, rank, counts,
+                                                               bp);
+      ctx->launched();
+      for (int b = 0; b < r->n_buckets; b++) {
+         sort_rows_kernel<<<blocks_for(r->buckets[b].n), kThreads, 0, s>>>(
+            r->buckets[b].slots, r->buckets[b].n, r->buckets[b].c, L);
+         ctx->launched();
+      }
+   }
    TFEM_CUDA(cudaGetLastError());
    TFEM_CUDA(cudaStreamSynchronize(s));
    cudaFree(counts);
-   cudaFree(is_shared);
-   cudaFree(shared_count);
+   cudaFree(flag);
+   cudaFree(scan);
    cudaFree(rank);
-   cudaFree(slot_off_full);
+   cudaFree(bucket_of);
    return r;
 }
 
@@ -381,10 +367,13 @@ void restriction_mult_transpose(tfem_ctx *ctx, const tfem_restriction *r, const 
    const int64_t nslots = r->ne * r->nd;
    const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad};
    exclusive_add_kernel<<<blocks_for(nslots), kThreads, 0, ctx->stream>>>(r->gmap, L, e, l);
-   if (r->n_shared > 0)
-      shared_add_kernel<<<blocks_for(r->n_shared), kThreads, 0, ctx->stream>>>(
-         r->shared_dofs, r->shared_off, r->shared_slots, r->n_shared, L, e, l);
-   ctx->launched(2);
+   ctx->launched();
+   if (r->n_shared > 0) {
+      double *ev = const_cast<tfem_restriction *>(r)->ensure_evec();
+      to_internal_kernel<<<blocks_for(nslots), kThreads, 0, ctx->stream>>>(L, e, ev);
+      ctx->launched();
+      scatter_shared(ctx, r, ev, nullptr, l, false, nullptr, nullptr, nullptr, false);
+   }
    TFEM_CUDA(cudaGetLastError());
 }
 
@@ -472,9 +461,10 @@ void restriction_destroy(tfem_restriction *r)
 {
    if (!r) return;
    cudaFree(r->gmap);
-   cudaFree(r->shared_dofs);
-   cudaFree(r->shared_off);
-   cudaFree(r->shared_slots);
+   for (int b = 0; b < r->n_buckets; b++) {
+      cudaFree(r->buckets[b].dofs);
+      cudaFree(r->buckets[b].slots);
+   }
    cudaFree(r->evec);
    delete r;
 }
