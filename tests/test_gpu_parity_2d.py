@@ -333,3 +333,49 @@ def test_restriction_roundtrip(dev):
         for i in range(dofs.shape[1]):
             want[dofs[k, i]] += ev[k * dofs.shape[1] + i]
     assert (y.numpy() == want).all()
+
+
+def test_full_size_bp3_bitwise(dev):
+    """BASELINE configs[1] size (make_cartesian(1054, 1054), p = 3,
+    10,004,569 DOFs): device qdata, operator action and diagonal equal the C
+    restatement (itself bit-equal to the reference) bit for bit."""
+    n, p = (1054, 1054), 3
+    sp = tf.FeSpace.cartesian(dev, n, p)
+    assert sp.n_dofs == 10_004_569
+    a = tf.BilinearForm(sp)
+    a.add_diffusion(1.0)
+    a.assemble()
+    x = rng_vec(sp.n_dofs, 42)
+    y = tf.Vector(dev, sp.n_dofs)
+    a.mult_true(x, y)
+    oc = OrcCartesian(2, n, p)
+    qd = oc.setup("diffusion")
+    assert (a.pa_data()[0].qdata() == qd).all()
+    assert (y.numpy() == oc.apply("diffusion", qd, x)).all()
+    assert (a.diagonal_true().numpy() == oc.diagonal("diffusion", qd)).all()
+
+
+def test_full_size_properties(dev):
+    """Size-independent checks at full size: constants annihilated, symmetry,
+    mass integrates the area, repeated applications bit-identical."""
+    n, p = (1054, 1054), 3
+    sp = tf.FeSpace.cartesian(dev, n, p, extents=(2.0, 0.5))
+    a = tf.BilinearForm(sp)
+    a.add_diffusion(1.0)
+    a.assemble()
+    y = tf.Vector(dev, sp.n_dofs)
+    a.mult_true(tf.Vector(dev, sp.n_dofs, 1.0), y)
+    assert np.abs(y.numpy()).max() <= 1e-11
+    x1, x2 = rng_vec(sp.n_dofs, 1), rng_vec(sp.n_dofs, 2)
+    y1, y2 = tf.Vector(dev, sp.n_dofs), tf.Vector(dev, sp.n_dofs)
+    a.mult_true(x1, y1)
+    a.mult_true(x2, y2)
+    assert x2 @ y1.numpy() == pytest.approx(x1 @ y2.numpy(), rel=1e-11)
+    first = y1.numpy()
+    a.mult_true(x1, y1)
+    assert (y1.numpy() == first).all()
+    m = tf.BilinearForm(sp)
+    m.add_mass(1.0)
+    m.assemble()
+    m.mult_true(tf.Vector(dev, sp.n_dofs, 1.0), y)
+    assert y.numpy().sum() == pytest.approx(1.0, rel=1e-12)
