@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--impl", default="tfem", choices=["tfem", "reference"])
     ap.add_argument("--dim", type=int, default=2)
     ap.add_argument("--order", type=int, default=3)
-    ap.add_argument("--n", type=int, default=0, help="cells per axis (0: ~10M DOFs)")
+    ap.add_argument("--cells", type=int, default=0, help="cells per axis (0: ~10M DOFs)")
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--numerics", default="reference", choices=["reference", "fma"])
     ap.add_argument("--cpu-iters", type=int, default=4)
@@ -68,7 +68,7 @@ def default_n(dim, p):
 
 
 def workload(args):
-    n = args.n or default_n(args.dim, args.order)
+    n = args.cells or default_n(args.dim, args.order)
     p = args.order
     ndofs = (n * p + 1) ** args.dim
     ne = n ** args.dim

@@ -147,6 +147,12 @@ int tfem_geometry_create(tfem_ctx *ctx, int dim, int order, int64_t n_elem,
 /* make_cartesian(n, ext) generated on the device (mesh.cpp:283-321). */
 int tfem_geometry_cartesian(tfem_ctx *ctx, int dim, const int *n,
                             const double *ext, tfem_geometry **out);
+/* The n_local block at cell offset `origin` of make_cartesian(n_global, ext):
+ * vertex coordinates are ext * (origin + i) / n_global, bit-identical to the
+ * global mesh (one rank's slab in an element-partitioned run). */
+int tfem_geometry_cartesian_box(tfem_ctx *ctx, int dim, const int *n_local,
+                                const int *origin, const int *n_global,
+                                const double *ext, tfem_geometry **out);
 int tfem_geometry_destroy(tfem_geometry *g);
 /* Physical coordinates of the nq^dim points of `rule` in every element,
  * E x nq^dim x dim, so the host can evaluate a Coefficient
@@ -207,6 +213,34 @@ int tfem_operator_mult_async(tfem_ctx *ctx, const tfem_operator *op,
  * driver's diag[ess] = 1 (driver.cpp:151-159). */
 int tfem_operator_diagonal(tfem_ctx *ctx, const tfem_operator *op,
                            tfem_vec *diag);
+
+/* --------------------------------------------------- distributed operator */
+/* Element-partitioned runs: each rank holds its elements plus
+ * one ghost element layer, so every owned DOF gets all its contributions
+ * locally, in global element order.  Per CG iteration the library packs
+ * p[send_idx[k]] into send_buf[k], calls exchange(), unpacks recv_buf[k]
+ * into p[recv_idx[k]]; reductions land in red[0..k) and allreduce(k) sums
+ * them over ranks in place.  Hooks run on the host in stream order and must
+ * only enqueue work on the context's stream (e.g. NCCL through
+ * torch.distributed with that stream current); buffers are device memory
+ * owned by the caller.  `not_owned` DOFs are left out of every dot. */
+#define TFEM_MAX_PEERS 8
+typedef struct {
+   void (*exchange)(void *user);
+   void (*allreduce)(int k, void *user);
+   void *user;
+} tfem_comm;
+
+typedef struct {
+   int n_peers;
+   int64_t n_send[TFEM_MAX_PEERS], n_recv[TFEM_MAX_PEERS];
+   const int32_t *send_idx[TFEM_MAX_PEERS], *recv_idx[TFEM_MAX_PEERS]; /* host */
+   double *send_buf[TFEM_MAX_PEERS], *recv_buf[TFEM_MAX_PEERS];         /* device */
+   double *red;                                                         /* device, >= 4 */
+} tfem_halo;
+
+int tfem_operator_set_comm(tfem_operator *op, const tfem_comm *comm, const tfem_halo *halo,
+                           int64_t n_not_owned, const int32_t *not_owned);
 
 /* ------------------------------------------------------------------- CG */
 typedef struct {

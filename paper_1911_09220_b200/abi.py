@@ -61,6 +61,22 @@ class CgResult(C.Structure):
 
 CG_CALLBACK = C.CFUNCTYPE(None, C.c_int, dp, i64, vp)
 
+MAX_PEERS = 8
+EXCHANGE_HOOK = C.CFUNCTYPE(None, vp)
+ALLREDUCE_HOOK = C.CFUNCTYPE(None, C.c_int, vp)
+
+
+class Comm(C.Structure):
+    _fields_ = [("exchange", EXCHANGE_HOOK), ("allreduce", ALLREDUCE_HOOK), ("user", vp)]
+
+
+class Halo(C.Structure):
+    _fields_ = [("n_peers", C.c_int),
+                ("n_send", i64 * MAX_PEERS), ("n_recv", i64 * MAX_PEERS),
+                ("send_idx", i32p * MAX_PEERS), ("recv_idx", i32p * MAX_PEERS),
+                ("send_buf", vp * MAX_PEERS), ("recv_buf", vp * MAX_PEERS),
+                ("red", vp)]
+
 _PROTOS = {
     "tfem_last_error": (C.c_char_p, []),
     "tfem_version": (C.c_char_p, []),
@@ -93,6 +109,7 @@ _PROTOS = {
     "tfem_restriction_mult_transpose": (C.c_int, [vp, vp, vp, vp]),
     "tfem_geometry_create": (C.c_int, [vp, C.c_int, C.c_int, i64, dp, C.POINTER(vp)]),
     "tfem_geometry_cartesian": (C.c_int, [vp, C.c_int, ip, dp, C.POINTER(vp)]),
+    "tfem_geometry_cartesian_box": (C.c_int, [vp, C.c_int, ip, ip, ip, dp, C.POINTER(vp)]),
     "tfem_geometry_destroy": (C.c_int, [vp]),
     "tfem_geometry_points": (C.c_int, [vp, vp, C.c_int, C.c_int, dp]),
     "tfem_pa_setup": (C.c_int, [vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, dp, C.c_double,
@@ -107,6 +124,7 @@ _PROTOS = {
     "tfem_pa_diagonal": (C.c_int, [vp, vp, vp, vp]),
     "tfem_operator_create": (C.c_int, [vp, C.c_int, C.POINTER(vp), vp, i64, i32p,
                                        C.POINTER(vp)]),
+    "tfem_operator_set_comm": (C.c_int, [vp, C.POINTER(Comm), C.POINTER(Halo), i64, i32p]),
     "tfem_operator_create_csr": (C.c_int, [vp, i64, i32p, i32p, dp, C.POINTER(vp)]),
     "tfem_operator_destroy": (C.c_int, [vp]),
     "tfem_operator_size": (i64, [vp]),

@@ -55,7 +55,8 @@ template <bool EXACT, int C>
 __device__ __forceinline__ double scatter_row(const BucketArgs &B, int b, int64_t s,
                                               const double *__restrict__ evec,
                                               const double *__restrict__ x, double *y,
-                                              int overwrite, const uint32_t *ess_out, bool want_dot)
+                                              int overwrite, const uint32_t *ess_out, bool want_dot,
+                                              const uint32_t *notown)
 {
    const int32_t d = __ldg(B.dofs[b] + s);
    uint32_t sl[C];
@@ -68,13 +69,14 @@ __device__ __forceinline__ double scatter_row(const BucketArgs &B, int b, int64_
    for (int k = 1; k < C; k++) acc = add<EXACT>(acc, v[k]);
    if (ess_out && bit_set(ess_out, d)) acc = __ldg(x + d);
    y[d] = acc;
-   return want_dot ? mul<EXACT>(__ldg(x + d), acc) : 0.0;
+   return want_dot && !(notown && bit_set(notown, d)) ? mul<EXACT>(__ldg(x + d), acc) : 0.0;
 }
 
 template <bool EXACT>
 __global__ void __launch_bounds__(kScatterThreads)
 scatter_kernel(const BucketArgs B, const double *__restrict__ evec, const double *__restrict__ x,
-               double *y, int overwrite, const uint32_t *ess_out, DotSink dot, const int *done)
+               double *y, int overwrite, const uint32_t *ess_out, DotSink dot, const int *done,
+               const uint32_t *notown)
 {
    if (done && *done) return;
    int b = 0;
@@ -84,13 +86,13 @@ scatter_kernel(const BucketArgs B, const double *__restrict__ evec, const double
    if (s < B.n[b]) {
       const bool wd = static_cast<bool>(dot);
       switch (B.c[b]) {
-      case 2: dv = scatter_row<EXACT, 2>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
-      case 3: dv = scatter_row<EXACT, 3>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
-      case 4: dv = scatter_row<EXACT, 4>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
-      case 5: dv = scatter_row<EXACT, 5>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
-      case 6: dv = scatter_row<EXACT, 6>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
-      case 7: dv = scatter_row<EXACT, 7>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
-      case 8: dv = scatter_row<EXACT, 8>(B, b, s, evec, x, y, overwrite, ess_out, wd); break;
+      case 2: dv = scatter_row<EXACT, 2>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
+      case 3: dv = scatter_row<EXACT, 3>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
+      case 4: dv = scatter_row<EXACT, 4>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
+      case 5: dv = scatter_row<EXACT, 5>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
+      case 6: dv = scatter_row<EXACT, 6>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
+      case 7: dv = scatter_row<EXACT, 7>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
+      case 8: dv = scatter_row<EXACT, 8>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
       }
    }
    if (dot) {
@@ -214,7 +216,8 @@ int64_t scatter_grid(const tfem_restriction *r) { return bucket_args(r).start[r-
 
 int64_t scatter_shared(tfem_ctx *ctx, const tfem_restriction *r, const double *evec,
                        const double *x, double *y, bool overwrite, const uint32_t *ess_out,
-                       const DotSink *dot, const int *done, bool exact)
+                       const DotSink *dot, const int *done, bool exact,
+                       const uint32_t *notown)
 {
    const BucketArgs B = bucket_args(r);
    const int64_t grid = B.start[r->n_buckets];
@@ -222,10 +225,10 @@ int64_t scatter_shared(tfem_ctx *ctx, const tfem_restriction *r, const double *e
    const DotSink sink = dot ? *dot : DotSink{};
    if (exact)
       scatter_kernel<true><<<(unsigned)grid, kScatterThreads, 0, ctx->stream>>>(
-         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done);
+         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done, notown);
    else
       scatter_kernel<false><<<(unsigned)grid, kScatterThreads, 0, ctx->stream>>>(
-         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done);
+         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done, notown);
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
    return grid;
@@ -258,6 +261,7 @@ void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const
    a.overwrite = f.overwrite ? 1 : 0;
    a.mask_in = f.mask_in;
    a.ess_out = f.ess_out;
+   a.notown = f.notown;
    a.dot = f.dot;
    a.done = f.done;
    k.launch(a, ctx->stream, elem_blocks(k, pa->ne));
@@ -265,7 +269,7 @@ void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const
    TFEM_CUDA(cudaGetLastError());
    if (r->n_shared > 0)
       scatter_shared(ctx, r, a.evec, x, y, f.overwrite, f.ess_out,
-                     f.dot_scatter ? &f.dot_scatter : nullptr, f.done, exact);
+                     f.dot_scatter ? &f.dot_scatter : nullptr, f.done, exact, f.notown);
 }
 
 void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, double *diag)

@@ -10,9 +10,6 @@
 // EXACT=false fuses multiply-adds.
 #include "kernels.cuh"
 
-#include <cstdlib>
-#include <string>
-
 namespace tfem {
 
 namespace {
@@ -149,7 +146,8 @@ __global__ void __launch_bounds__(kElemThreads2D) apply2d_kernel(const ApplyArgs
             if (!a.overwrite) r = add<EXACT>(a.y[d], r);
             if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
             a.y[d] = r;
-            if (a.dot) dot = mac<EXACT>(dot, __ldg(a.x + d), r);
+            if (a.dot && !(a.notown && bit_set(a.notown, d)))
+               dot = mac<EXACT>(dot, __ldg(a.x + d), r);
          } else {
             a.evec[i * a.ne_pad + e] = r;
          }
@@ -162,231 +160,39 @@ __global__ void __launch_bounds__(kElemThreads2D) apply2d_kernel(const ApplyArgs
 }
 
 
-// ------------------------------------------------------------- pair kernel
-// Two threads per element (lanes 2k, 2k+1), halving the register footprint
-// of the one-thread kernel so twice the warps fit per SM.  Thread h owns the
-// quadrature columns qx in [QX0(h), QX0(h)+NQX(h)) for the forward
-// contraction and the output rows a in [A0(h), A0(h)+NA(h)).  The x-sum of
-// the backward contraction S(a, qy) = sum_qx G(qx, a) w(qx, qy) must run over
-// qx in ascending order: thread 0 folds its columns, hands the 2*D1 partial
-// sums to thread 1 with a shuffle, thread 1 continues with its columns and
-// returns the finished S for thread 0's rows.  Every sum keeps the
-// reference's sequential order, so EXACT results stay bit-identical.
-template <int P, int Q, int KIND, bool EXACT>
-__global__ void __launch_bounds__(kElemThreads2D, 3) apply2d_pair_kernel(const ApplyArgs a)
-{
-   constexpr int D1 = P + 1, ND = D1 * D1, NQD = Q * Q;
-   constexpr int QA = (Q + 1) / 2, QB = Q - QA; // columns of thread 0 / 1
-   constexpr int DA = (D1 + 1) / 2, DB = D1 - DA; // rows of thread 0 / 1
-   constexpr int NQX = QA, NA = DA;           // register extents (max of both)
-   if (a.done && *a.done) return;
-   const int h = threadIdx.x & 1;
-   const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 1;
-   const bool live = e < a.ne;
-   const int qx0 = h ? QA : 0, nqx = h ? QB : QA;
-   const int a0 = h ? DA : 0, na = h ? DB : DA;
-   double dot = 0.0;
-   double R[NA][D1];
-   uint32_t dof[NA][D1];
-   {
-      double V[D1][D1];
-#pragma unroll
-      for (int i = 0; i < ND; i++) {
-         const uint32_t g = live ? __ldg(a.gmap + i * a.ne_pad + e) : 0u;
-         const uint32_t d = g & kDofMask;
-         double v = live ? __ldg(a.x + d) : 0.0;
-         if (a.mask_in && live && bit_set(a.mask_in, d)) v = 0.0;
-         V[i % D1][i / D1] = v;
-#pragma unroll
-         for (int r = 0; r < NA; r++)
-            if (i % D1 == a0 + r) dof[r][i / D1] = g;
-      }
-      const double *qd = a.qdata + (live ? e : 0);
-      const int64_t pl = a.ne_pad;
-      double T1[NQX][D1], T2[NQX][D1];
-#pragma unroll
-      for (int j = 0; j < NQX; j++) {
-         const int qx = qx0 + (j < nqx ? j : 0);
-#pragma unroll
-         for (int b = 0; b < D1; b++) {
-            double s1 = mul<EXACT>(a.t.G[qx][0], V[0][b]);
-            double s2 = mul<EXACT>(a.t.B[qx][0], V[0][b]);
-#pragma unroll
-            for (int k = 1; k < D1; k++) {
-               if (KIND == TFEM_DIFFUSION) s1 = mac<EXACT>(s1, a.t.G[qx][k], V[k][b]);
-               s2 = mac<EXACT>(s2, a.t.B[qx][k], V[k][b]);
-            }
-            T1[j][b] = s1;
-            T2[j][b] = s2;
-         }
-      }
-      double vx[NA][D1], vy[NA][D1];
-#pragma unroll
-      for (int qy = 0; qy < Q; qy++) {
-         double wx[NQX], wy[NQX];
-#pragma unroll
-         for (int j = 0; j < NQX; j++) {
-            const int qx = qx0 + (j < nqx ? j : 0);
-            const int q = qy * Q + qx;
-            if (KIND == TFEM_DIFFUSION) {
-               double dx = mul<EXACT>(T1[j][0], a.t.B[qy][0]);
-               double dy = mul<EXACT>(T2[j][0], a.t.G[qy][0]);
-#pragma unroll
-               for (int b = 1; b < D1; b++) {
-                  dx = mac<EXACT>(dx, T1[j][b], a.t.B[qy][b]);
-                  dy = mac<EXACT>(dy, T2[j][b], a.t.G[qy][b]);
-               }
-               const double d0 = live ? __ldg(qd + (0 * NQD + q) * pl) : 0.0;
-               const double d1 = live ? __ldg(qd + (1 * NQD + q) * pl) : 0.0;
-               const double d2 = live ? __ldg(qd + (2 * NQD + q) * pl) : 0.0;
-               wx[j] = add<EXACT>(mul<EXACT>(d0, dx), mul<EXACT>(d1, dy));
-               wy[j] = add<EXACT>(mul<EXACT>(d1, dx), mul<EXACT>(d2, dy));
-            } else {
-               double u = mul<EXACT>(T2[j][0], a.t.B[qy][0]);
-#pragma unroll
-               for (int b = 1; b < D1; b++) u = mac<EXACT>(u, T2[j][b], a.t.B[qy][b]);
-               wy[j] = mul<EXACT>(u, live ? __ldg(qd + (qy * Q + qx) * pl) : 0.0);
-               wx[j] = 0.0;
-            }
-         }
-         // S over qx: thread 0 starts, thread 1 continues (ascending qx)
-         double sx[D1], sy[D1];
-#pragma unroll
-         for (int i = 0; i < D1; i++) {
-            double px = 0.0, py = 0.0;
-            if (h == 0) {
-               if (KIND == TFEM_DIFFUSION) px = mul<EXACT>(a.t.G[0][i], wx[0]);
-               py = mul<EXACT>(a.t.B[0][i], wy[0]);
-#pragma unroll
-               for (int j = 1; j < QA; j++) {
-                  if (KIND == TFEM_DIFFUSION) px = mac<EXACT>(px, a.t.G[j][i], wx[j]);
-                  py = mac<EXACT>(py, a.t.B[j][i], wy[j]);
-               }
-            }
-            if (KIND == TFEM_DIFFUSION) px = __shfl_up_sync(0xffffffffu, px, 1);
-            py = __shfl_up_sync(0xffffffffu, py, 1);
-            if (h == 1) {
-#pragma unroll
-               for (int j = 0; j < QB; j++) {
-                  if (KIND == TFEM_DIFFUSION) px = mac<EXACT>(px, a.t.G[QA + j][i], wx[j]);
-                  py = mac<EXACT>(py, a.t.B[QA + j][i], wy[j]);
-               }
-            }
-            sx[i] = px;
-            sy[i] = py;
-         }
-         // thread 0 receives the finished rows it owns
-#pragma unroll
-         for (int i = 0; i < DA; i++) {
-            const double tx = KIND == TFEM_DIFFUSION ? __shfl_down_sync(0xffffffffu, sx[i], 1) : 0.0;
-            const double ty = __shfl_down_sync(0xffffffffu, sy[i], 1);
-            if (h == 0) {
-               sx[i] = tx;
-               sy[i] = ty;
-            }
-         }
-#pragma unroll
-         for (int r = 0; r < NA; r++) {
-            const int i = a0 + (r < na ? r : 0);
-            const double fx = h ? sx[(DA + r) < D1 ? DA + r : 0] : sx[r];
-            const double fy = h ? sy[(DA + r) < D1 ? DA + r : 0] : sy[r];
-            (void)i;
-#pragma unroll
-            for (int b = 0; b < D1; b++) {
-               if (KIND == TFEM_DIFFUSION) {
-                  vx[r][b] = qy == 0 ? mul<EXACT>(fx, a.t.B[0][b]) : mac<EXACT>(vx[r][b], fx, a.t.B[qy][b]);
-                  vy[r][b] = qy == 0 ? mul<EXACT>(fy, a.t.G[0][b]) : mac<EXACT>(vy[r][b], fy, a.t.G[qy][b]);
-               } else {
-                  vy[r][b] = qy == 0 ? mul<EXACT>(fy, a.t.B[0][b]) : mac<EXACT>(vy[r][b], fy, a.t.B[qy][b]);
-               }
-            }
-         }
-      }
-#pragma unroll
-      for (int r = 0; r < NA; r++)
-#pragma unroll
-         for (int b = 0; b < D1; b++)
-            R[r][b] = KIND == TFEM_DIFFUSION ? add<EXACT>(vx[r][b], vy[r][b]) : vy[r][b];
-   }
-   if (live) {
-#pragma unroll
-      for (int r = 0; r < NA; r++) {
-         if (r >= na) continue;
-#pragma unroll
-         for (int b = 0; b < D1; b++) {
-            const uint32_t g = dof[r][b];
-            double val = R[r][b];
-            if (g & kExclusive) {
-               const uint32_t d = g & kDofMask;
-               if (!a.overwrite) val = add<EXACT>(a.y[d], val);
-               if (a.ess_out && bit_set(a.ess_out, d)) val = __ldg(a.x + d);
-               a.y[d] = val;
-               if (a.dot) dot = mac<EXACT>(dot, __ldg(a.x + d), val);
-            } else {
-               a.evec[(int64_t)(b * D1 + a0 + r) * a.ne_pad + e] = val;
-            }
-         }
-      }
-   }
-   if (a.dot) {
-      const double v[1] = {dot};
-      emit<kElemThreads2D, 1>(a.dot, v);
-   }
-}
-
 template <int P, int Q, int KIND, bool EXACT>
 void launch2d(const ApplyArgs &a, cudaStream_t s, unsigned blocks)
 {
    apply2d_kernel<P, Q, KIND, EXACT><<<blocks, kElemThreads2D, 0, s>>>(a);
 }
 
-template <int P, int Q, int KIND, bool EXACT>
-void launch2d_pair(const ApplyArgs &a, cudaStream_t s, unsigned blocks)
-{
-   apply2d_pair_kernel<P, Q, KIND, EXACT><<<blocks, kElemThreads2D, 0, s>>>(a);
-}
-
 template <int P, int KIND>
-Launch pick_q(int nq, bool exact, bool pair)
+Launch pick_q(int nq, bool exact)
 {
-   if (pair) {
-      if (nq == P + 2)
-         return exact ? launch2d_pair<P, P + 2, KIND, true> : launch2d_pair<P, P + 2, KIND, false>;
-      if (nq == P + 1)
-         return exact ? launch2d_pair<P, P + 1, KIND, true> : launch2d_pair<P, P + 1, KIND, false>;
-      return nullptr;
-   }
    if (nq == P + 2) return exact ? launch2d<P, P + 2, KIND, true> : launch2d<P, P + 2, KIND, false>;
    if (nq == P + 1) return exact ? launch2d<P, P + 1, KIND, true> : launch2d<P, P + 1, KIND, false>;
    return nullptr;
 }
 
 template <int KIND>
-Launch pick_p(int p, int nq, bool exact, bool pair)
+Launch pick_p(int p, int nq, bool exact)
 {
    switch (p) {
-   case 1: return pick_q<1, KIND>(nq, exact, false);
-   case 2: return pick_q<2, KIND>(nq, exact, pair);
-   case 3: return pick_q<3, KIND>(nq, exact, pair);
+   case 1: return pick_q<1, KIND>(nq, exact);
+   case 2: return pick_q<2, KIND>(nq, exact);
+   case 3: return pick_q<3, KIND>(nq, exact);
    }
    return nullptr;
 }
 
 } // namespace
 
-// TFEM_APPLY2D=pair selects the two-threads-per-element variant (A/B runs;
-// measured 2.6x slower than one thread per element at p = 3 on B200).
 KernelPick pick_apply2d_reg(int p, int nq, int kind, bool exact)
 {
-   static const bool pair = [] {
-      const char *v = std::getenv("TFEM_APPLY2D");
-      return v && std::string(v) == "pair";
-   }();
-   const bool use_pair = pair && p >= 2;
    KernelPick k;
-   k.launch = kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact, use_pair)
-                                : pick_p<TFEM_DIFFUSION>(p, nq, exact, use_pair);
-   k.elems_per_block = use_pair ? kElemThreads2D / 2 : kElemThreads2D;
+   k.launch = kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact)
+                                : pick_p<TFEM_DIFFUSION>(p, nq, exact);
+   k.elems_per_block = kElemThreads2D;
    k.threads = kElemThreads2D;
    return k;
 }

@@ -132,7 +132,7 @@ __global__ void apply2d_grp_kernel(const ApplyArgs a)
          if (!a.overwrite) r = add<EXACT>(a.y[d], r);
          if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
          a.y[d] = r;
-         if (a.dot) dot = mul<EXACT>(__ldg(a.x + d), r);
+         if (a.dot && !(a.notown && bit_set(a.notown, d))) dot = mul<EXACT>(__ldg(a.x + d), r);
       } else {
          a.evec[e * ND + t] = r;
       }
@@ -296,7 +296,7 @@ __global__ void apply3d_kernel(const ApplyArgs a)
             if (!a.overwrite) r += a.y[d];
             if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
             a.y[d] = r;
-            if (a.dot) dot = fma(__ldg(a.x + d), r, dot);
+            if (a.dot && !(a.notown && bit_set(a.notown, d))) dot = fma(__ldg(a.x + d), r, dot);
          } else {
             a.evec[e * ND + i] = r;
          }

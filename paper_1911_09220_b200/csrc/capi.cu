@@ -4,6 +4,7 @@
 #include "common.cuh"
 
 #include <cstring>
+#include <memory>
 #include <string>
 
 namespace tfem {
@@ -16,6 +17,8 @@ int64_t restriction_boundary_dofs(const tfem_restriction *r, int32_t *host);
 void restriction_mult(tfem_ctx *ctx, const tfem_restriction *r, const double *l, double *e);
 void vec_axpy(tfem_ctx *ctx, double a, const double *x, double *y, int64_t n);
 void operator_set_ess(tfem_ctx *ctx, tfem_operator *op, int64_t n_ess, const int32_t *ess);
+void operator_set_comm(tfem_ctx *ctx, tfem_operator *op, const tfem_comm &comm,
+                       const tfem_halo &halo, int64_t n_not_owned, const int32_t *not_owned);
 tfem_operator *operator_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, const int32_t *cols,
                             const double *vals);
 void operator_release(tfem_operator *op);
@@ -345,36 +348,40 @@ int tfem_geometry_create(tfem_ctx *ctx, int dim, int order, int64_t n_elem, cons
    });
 }
 
-int tfem_geometry_cartesian(tfem_ctx *ctx, int dim, const int *n, const double *ext,
-                            tfem_geometry **out)
+int tfem_geometry_cartesian_box(tfem_ctx *ctx, int dim, const int *n_local, const int *origin,
+                                const int *n_global, const double *ext, tfem_geometry **out)
 {
    return guard([&] {
       need(ctx, "tfem_geometry_cartesian");
-      need(n, "tfem_geometry_cartesian");
+      need(n_local, "tfem_geometry_cartesian");
       need(out, "tfem_geometry_cartesian");
       if (dim != 2 && dim != 3) invalid("tfem_geometry_cartesian: dim must be 2 or 3");
-      auto *g = new tfem_geometry;
+      auto g = std::make_unique<tfem_geometry>();
       g->ctx = ctx;
       g->dim = dim;
       g->order = 1;
       g->cartesian = true;
       g->ne = 1;
       for (int d = 0; d < dim; d++) {
-         if (n[d] < 1) {
-            delete g;
-            invalid("make_cartesian: need nx, ny >= 1");
-         }
+         if (n_local[d] < 1) invalid("make_cartesian: need nx, ny >= 1");
          const double e = ext ? ext[d] : 1.0;
-         if (!(e > 0.0)) {
-            delete g;
-            invalid("make_cartesian: need positive extents");
-         }
-         g->n[d] = n[d];
+         if (!(e > 0.0)) invalid("make_cartesian: need positive extents");
+         g->n[d] = n_local[d];
+         g->origin[d] = origin ? origin[d] : 0;
+         g->n_global[d] = n_global ? n_global[d] : n_local[d];
+         if (g->origin[d] < 0 || g->origin[d] + g->n[d] > g->n_global[d])
+            invalid("tfem_geometry_cartesian_box: block outside the global mesh");
          g->ext[d] = e;
-         g->ne *= n[d];
+         g->ne *= n_local[d];
       }
-      *out = g;
+      *out = g.release();
    });
+}
+
+int tfem_geometry_cartesian(tfem_ctx *ctx, int dim, const int *n, const double *ext,
+                            tfem_geometry **out)
+{
+   return tfem_geometry_cartesian_box(ctx, dim, n, nullptr, nullptr, ext, out);
 }
 
 int tfem_geometry_destroy(tfem_geometry *g)
@@ -533,6 +540,18 @@ int tfem_operator_create(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa, const tfem
          throw;
       }
       *out = op;
+   });
+}
+
+int tfem_operator_set_comm(tfem_operator *op, const tfem_comm *comm, const tfem_halo *halo,
+                           int64_t n_not_owned, const int32_t *not_owned)
+{
+   return guard([&] {
+      need(op, "tfem_operator_set_comm");
+      need(comm, "tfem_operator_set_comm");
+      need(halo, "tfem_operator_set_comm");
+      if (!comm->exchange || !comm->allreduce) invalid("tfem_operator_set_comm: null hook");
+      operator_set_comm(op->ctx, op, *comm, *halo, n_not_owned, not_owned);
    });
 }
 

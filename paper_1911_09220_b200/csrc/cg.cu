@@ -45,12 +45,14 @@ __global__ void fill_kernel(double *d, int64_t n, double v)
 }
 
 __global__ void __launch_bounds__(kVecThreads)
-dot_kernel(const double *__restrict__ a, const double *__restrict__ b, int64_t n, DotSink sink)
+dot_kernel(const double *__restrict__ a, const double *__restrict__ b, int64_t n, DotSink sink,
+           const uint32_t *notown)
 {
    double s = 0.0;
    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
         i += (int64_t)gridDim.x * blockDim.x)
-      s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
+      if (!(notown && bit_set(notown, static_cast<uint32_t>(i))))
+         s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
    const double v[1] = {s};
    emit<kVecThreads, 1>(sink, v);
 }
@@ -127,7 +129,7 @@ __device__ __forceinline__ int next_buffer(int cur, int best)
 __global__ void __launch_bounds__(kVecThreads)
 cg_init_kernel(const double *__restrict__ b, const double *__restrict__ diag, int64_t n,
                double *__restrict__ r, double *__restrict__ p, double *__restrict__ x,
-               DotSink sink)
+               DotSink sink, const uint32_t *notown)
 {
    double rr = 0.0, rz = 0.0;
    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -137,6 +139,7 @@ cg_init_kernel(const double *__restrict__ b, const double *__restrict__ diag, in
       r[i] = ri;
       p[i] = zi;
       x[i] = 0.0;
+      if (notown && bit_set(notown, static_cast<uint32_t>(i))) continue;
       rr = __dadd_rn(rr, __dmul_rn(ri, ri));
       rz = __dadd_rn(rz, __dmul_rn(ri, zi));
    }
@@ -144,28 +147,70 @@ cg_init_kernel(const double *__restrict__ b, const double *__restrict__ diag, in
    emit<kVecThreads, 2>(sink, v);
 }
 
+__device__ void init_step(CgState *st, double rr, double rz)
+{
+   st->rz = rz;
+   st->rnorm = sqrt(rr);
+   st->best_rnorm = st->rnorm;
+   st->it = 0;
+   st->done = 0;
+   st->converged = 0;
+   st->iterations = 0;
+   st->status = 0;
+   st->cur = 0;
+   st->best = 0;
+   if (st->rnorm <= st->target) { // top of iteration 1 (solvers.cpp:61-65)
+      st->done = 1;
+      st->converged = 1;
+      st->iterations = 0;
+   }
+}
+
+__device__ void alpha_step(CgState *st, double pq)
+{
+   const double alpha = st->rz / pq;
+   st->alpha = alpha;
+   if (!isfinite(alpha)) { // solvers.cpp:69-71
+      st->status = 1;
+      st->done = 1;
+   }
+}
+
+__device__ void beta_step(CgState *st, double rr, double rz_next)
+{
+   const double rnorm = sqrt(rr);
+   st->rnorm = rnorm;
+   if (!isfinite(rnorm)) { // solvers.cpp:74-77
+      st->status = 2;
+      st->done = 1;
+      return;
+   }
+   st->it += 1;
+   const int nxt = next_buffer(st->cur, st->best);
+   st->cur = nxt;
+   if (rnorm < st->best_rnorm) { // solvers.cpp:78-81
+      st->best_rnorm = rnorm;
+      st->best = nxt;
+   }
+   st->beta = rz_next / st->rz;
+   st->rz = rz_next;
+   if (rnorm <= st->target) { // checked at the top of the next iteration
+      st->done = 1;
+      st->converged = 1;
+      st->iterations = st->it;
+   } else if (st->it >= st->max_iters) {
+      st->done = 1;
+      st->converged = 0;
+      st->iterations = st->max_iters;
+   }
+}
+
 __global__ void __launch_bounds__(kVecThreads)
 cg_init_finish_kernel(const double *chunks, int64_t nch, CgState *st)
 {
    const double rr = fold(chunks, nch);
    const double rz = fold(chunks + nch, nch);
-   if (threadIdx.x == 0) {
-      st->rz = rz;
-      st->rnorm = sqrt(rr);
-      st->best_rnorm = st->rnorm;
-      st->it = 0;
-      st->done = 0;
-      st->converged = 0;
-      st->iterations = 0;
-      st->status = 0;
-      st->cur = 0;
-      st->best = 0;
-      if (st->rnorm <= st->target) { // top of iteration 1 (solvers.cpp:61-65)
-         st->done = 1;
-         st->converged = 1;
-         st->iterations = 0;
-      }
-   }
+   if (threadIdx.x == 0) init_step(st, rr, rz);
 }
 
 // pq = (element-kernel chunks) + (scatter chunks) in a fixed order.
@@ -177,14 +222,34 @@ cg_alpha_kernel(const double *ch_a, int64_t na, const double *ch_b, int64_t nb, 
    for (int64_t i = threadIdx.x; i < na + nb; i += blockDim.x)
       s += __ldcg(i < na ? ch_a + i : ch_b + (i - na));
    const double pq = block_sum<kVecThreads>(s);
-   if (threadIdx.x == 0) {
-      const double alpha = st->rz / pq;
-      st->alpha = alpha;
-      if (!isfinite(alpha)) { // solvers.cpp:69-71
-         st->status = 1;
-         st->done = 1;
-      }
+   if (threadIdx.x == 0) alpha_step(st, pq);
+}
+
+// Distributed variants: the rank-local fold lands in red[] (device), the
+// host hook sums red[] over ranks in place, then the step kernel reads it.
+__global__ void __launch_bounds__(kVecThreads)
+fold_to_kernel(const double *ch_a, int64_t na, const double *ch_b, int64_t nb, int k,
+               double *out)
+{
+   for (int j = 0; j < k; j++) {
+      double s = 0.0;
+      for (int64_t i = threadIdx.x; i < na + nb; i += blockDim.x)
+         s += __ldcg(i < na ? ch_a + j * na + i : ch_b + j * nb + (i - na));
+      const double t = block_sum<kVecThreads>(s);
+      if (threadIdx.x == 0) out[j] = t;
    }
+}
+
+__global__ void red_init_kernel(const double *red, CgState *st) { init_step(st, red[0], red[1]); }
+
+__global__ void red_alpha_kernel(const double *red, CgState *st)
+{
+   if (!st->done) alpha_step(st, red[0]);
+}
+
+__global__ void red_beta_kernel(const double *red, CgState *st)
+{
+   if (!st->done) beta_step(st, red[0], red[1]);
 }
 
 struct XBufs {
@@ -198,7 +263,8 @@ constexpr int kUnroll = 4;
 __global__ void __launch_bounds__(kVecThreads)
 cg_update_kernel(const CgState *st, XBufs xb, const double *__restrict__ p,
                  const double *__restrict__ q, double *__restrict__ r,
-                 const double *__restrict__ diag, int64_t n, DotSink sink)
+                 const double *__restrict__ diag, int64_t n, DotSink sink,
+                 const uint32_t *notown)
 {
    if (st->done) return;
    const double alpha = st->alpha, nalpha = -alpha;
@@ -225,6 +291,7 @@ cg_update_kernel(const CgState *st, XBufs xb, const double *__restrict__ p,
          const double ri = __dadd_rn(rv[u], __dmul_rn(nalpha, qv[u]));
          r[j] = ri;
          const double zi = diag ? __ddiv_rn(ri, dv[u]) : ri;
+         if (notown && bit_set(notown, static_cast<uint32_t>(j))) continue;
          rr = __dadd_rn(rr, __dmul_rn(ri, ri));
          rz = __dadd_rn(rz, __dmul_rn(ri, zi));
       }
@@ -234,6 +301,7 @@ cg_update_kernel(const CgState *st, XBufs xb, const double *__restrict__ p,
       const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, q[i]));
       r[i] = ri;
       const double zi = diag ? __ddiv_rn(ri, diag[i]) : ri;
+      if (notown && bit_set(notown, static_cast<uint32_t>(i))) continue;
       rr = __dadd_rn(rr, __dmul_rn(ri, ri));
       rz = __dadd_rn(rz, __dmul_rn(ri, zi));
    }
@@ -247,32 +315,7 @@ cg_beta_kernel(const double *chunks, int64_t nch, CgState *st)
    if (st->done) return;
    const double rr = fold(chunks, nch);
    const double rz_next = fold(chunks + nch, nch);
-   if (threadIdx.x != 0) return;
-   const double rnorm = sqrt(rr);
-   st->rnorm = rnorm;
-   if (!isfinite(rnorm)) { // solvers.cpp:74-77
-      st->status = 2;
-      st->done = 1;
-      return;
-   }
-   st->it += 1;
-   const int nxt = next_buffer(st->cur, st->best);
-   st->cur = nxt;
-   if (rnorm < st->best_rnorm) { // solvers.cpp:78-81
-      st->best_rnorm = rnorm;
-      st->best = nxt;
-   }
-   st->beta = rz_next / st->rz;
-   st->rz = rz_next;
-   if (rnorm <= st->target) { // checked at the top of the next iteration
-      st->done = 1;
-      st->converged = 1;
-      st->iterations = st->it;
-   } else if (st->it >= st->max_iters) {
-      st->done = 1;
-      st->converged = 0;
-      st->iterations = st->max_iters;
-   }
+   if (threadIdx.x == 0) beta_step(st, rr, rz_next);
 }
 
 // p = z + beta p with z = r / d (solvers.cpp:84-87)
@@ -417,12 +460,26 @@ void enqueue_iteration(tfem_ctx *ctx, const tfem_operator *op, Workspace &w, XBu
                                                        w.st);
    const unsigned vb = vec_blocks(ctx, n);
    cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.p, w.q, w.r, diag, n,
-                                                         w.s_vec.s);
+                                                         w.s_vec.s, nullptr);
    cg_beta_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, w.st);
    cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.r, diag, w.p, n);
    ctx->launched(4);
    TFEM_CUDA(cudaGetLastError());
 }
+
+__global__ void gather_idx_kernel(const double *v, const int32_t *idx, int64_t n, double *out)
+{
+   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (i < n) out[i] = v[idx[i]];
+}
+
+__global__ void scatter_idx_kernel(const double *in, const int32_t *idx, int64_t n, double *v)
+{
+   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (i < n) v[idx[i]] = in[i];
+}
+
+__global__ void copy_scalar_kernel(const double *src, double *dst) { *dst = *src; }
 
 } // namespace
 
@@ -433,8 +490,10 @@ void vec_fill(tfem_ctx *ctx, double *d, int64_t n, double v)
    TFEM_CUDA(cudaGetLastError());
 }
 
-double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n)
+double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n,
+               const tfem_operator *dist)
 {
+   const uint32_t *notown = dist ? dist->notown : nullptr;
    static thread_local std::unordered_map<int64_t, SinkStore> sinks;
    const unsigned nb = vec_blocks(ctx, n);
    auto it = sinks.find(nb);
@@ -444,10 +503,16 @@ double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n)
       it = sinks.emplace(nb, st).first;
    }
    const SinkStore &s = it->second;
-   dot_kernel<<<nb, kVecThreads, 0, ctx->stream>>>(a, b, n, s.s);
+   dot_kernel<<<nb, kVecThreads, 0, ctx->stream>>>(a, b, n, s.s, notown);
    fold_kernel<<<1, kVecThreads, 0, ctx->stream>>>(s.s.chunks, s.nch, ctx->scalars);
    ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
+   if (dist) {
+      copy_scalar_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scalars, dist->red);
+      dist->comm.allreduce(1, dist->comm.user);
+      copy_scalar_kernel<<<1, 1, 0, ctx->stream>>>(dist->red, ctx->scalars);
+      ctx->launched(2);
+   }
    TFEM_CUDA(cudaMemcpyAsync(ctx->host_scalars, ctx->scalars, sizeof(double),
                              cudaMemcpyDeviceToHost, ctx->stream));
    TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -482,6 +547,71 @@ void operator_set_ess(tfem_ctx *ctx, tfem_operator *op, int64_t n_ess, const int
    TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+void operator_set_comm(tfem_ctx *ctx, tfem_operator *op, const tfem_comm &comm,
+                       const tfem_halo &halo, int64_t n_not_owned, const int32_t *not_owned)
+{
+   if (op->csr) invalid("tfem_operator_set_comm: needs a PA operator");
+   if (halo.n_peers < 0 || halo.n_peers > TFEM_MAX_PEERS)
+      invalid("tfem_operator_set_comm: bad peer count");
+   if (!halo.red) invalid("tfem_operator_set_comm: null reduction buffer");
+   auto upload = [&](const int32_t *idx, int64_t n) -> int32_t * {
+      for (int64_t i = 0; i < n; i++)
+         if (idx[i] < 0 || idx[i] >= op->n) invalid("tfem_operator_set_comm: DOF out of range");
+      int32_t *d = dalloc<int32_t>(n);
+      if (n) TFEM_CUDA(cudaMemcpy(d, idx, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+      return d;
+   };
+   for (int k = 0; k < op->n_peers; k++) {
+      cudaFree(op->send_idx[k]);
+      cudaFree(op->recv_idx[k]);
+   }
+   op->n_peers = halo.n_peers;
+   for (int k = 0; k < halo.n_peers; k++) {
+      op->n_send[k] = halo.n_send[k];
+      op->n_recv[k] = halo.n_recv[k];
+      op->send_idx[k] = upload(halo.send_idx[k], halo.n_send[k]);
+      op->recv_idx[k] = upload(halo.recv_idx[k], halo.n_recv[k]);
+      op->send_buf[k] = halo.send_buf[k];
+      op->recv_buf[k] = halo.recv_buf[k];
+   }
+   op->red = halo.red;
+   cudaFree(op->notown);
+   op->notown = nullptr;
+   if (n_not_owned > 0) {
+      int32_t *d = upload(not_owned, n_not_owned);
+      const int64_t words = (op->n + 31) / 32;
+      op->notown = dalloc<uint32_t>(words);
+      TFEM_CUDA(cudaMemsetAsync(op->notown, 0, sizeof(uint32_t) * words, ctx->stream));
+      set_bits_kernel<<<blocks_for(n_not_owned, 256), 256, 0, ctx->stream>>>(d, n_not_owned,
+                                                                              op->notown);
+      ctx->launched();
+      TFEM_CUDA(cudaGetLastError());
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(d);
+   }
+   op->comm = comm;
+   op->has_comm = true;
+}
+
+// Halo update of a device vector: pack, hook, unpack (all on the stream).
+void halo_exchange(tfem_ctx *ctx, const tfem_operator *op, double *v)
+{
+   for (int k = 0; k < op->n_peers; k++)
+      if (op->n_send[k] > 0) {
+         gather_idx_kernel<<<blocks_for(op->n_send[k], 256), 256, 0, ctx->stream>>>(
+            v, op->send_idx[k], op->n_send[k], op->send_buf[k]);
+         ctx->launched();
+      }
+   op->comm.exchange(op->comm.user);
+   for (int k = 0; k < op->n_peers; k++)
+      if (op->n_recv[k] > 0) {
+         scatter_idx_kernel<<<blocks_for(op->n_recv[k], 256), 256, 0, ctx->stream>>>(
+            op->recv_buf[k], op->recv_idx[k], op->n_recv[k], v);
+         ctx->launched();
+      }
+   TFEM_CUDA(cudaGetLastError());
+}
+
 tfem_operator *operator_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, const int32_t *cols,
                             const double *vals)
 {
@@ -505,6 +635,7 @@ void operator_release(tfem_operator *op)
    workspaces().erase(op);
    cudaFree(op->ess);
    cudaFree(op->ess_mask);
+   cudaFree(op->notown);
    cudaFree(op->rowptr);
    cudaFree(op->cols);
    cudaFree(op->vals);
@@ -531,6 +662,7 @@ void operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, doub
       f.mask_in = op->ess_mask;
       const bool last = (k + 1 == op->pa.size());
       f.ess_out = last ? op->ess_mask : nullptr;
+      f.notown = op->notown;
       if (last && dot_elem) f.dot = *dot_elem;
       if (last && dot_scatter) f.dot_scatter = *dot_scatter;
       f.done = done;
@@ -586,7 +718,8 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
       if (hb) invalid("cg_solve: Jacobi diagonal must be strictly positive");
    }
    Workspace &w = workspace_for(ctx, op);
-   const double bnorm = std::sqrt(vec_dot(ctx, b, b, n));
+   const tfem_comm *comm = op->has_comm ? &op->comm : nullptr;
+   const double bnorm = std::sqrt(vec_dot(ctx, b, b, n, comm ? op : nullptr));
    res->initial_norm = bnorm;
    if (!std::isfinite(bnorm)) runtime("cg_solve: right-hand side is not finite");
    if (bnorm == 0.0) { // solvers.cpp:37-41
@@ -600,11 +733,42 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
    init.max_iters = max_iters;
    TFEM_CUDA(cudaMemcpyAsync(w.st, &init, sizeof(CgState), cudaMemcpyHostToDevice, ctx->stream));
    const unsigned vb = vec_blocks(ctx, n);
-   cg_init_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(b, diag, n, w.r, w.p, x, w.s_vec.s);
-   cg_init_finish_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, w.st);
-   ctx->launched(2);
+   cg_init_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(b, diag, n, w.r, w.p, x, w.s_vec.s,
+                                                       op->notown);
+   if (comm) {
+      fold_to_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, nullptr,
+                                                         0, 2, op->red);
+      comm->allreduce(2, comm->user);
+      red_init_kernel<<<1, 1, 0, ctx->stream>>>(op->red, w.st);
+   } else {
+      cg_init_finish_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch,
+                                                                w.st);
+   }
+   ctx->launched(comm ? 3 : 2);
    TFEM_CUDA(cudaGetLastError());
    const XBufs xb{{x, w.xa, w.xb}};
+
+   // Distributed iteration: halo update of p, then the same kernels with the
+   // rank-local folds summed over ranks by the allreduce hook.
+   auto dist_iteration = [&]() {
+      halo_exchange(ctx, op, w.p);
+      operator_mult(ctx, op, w.p, w.q, &w.s_elem.s, w.s_scatter.grid ? &w.s_scatter.s : nullptr,
+                    &w.st->done);
+      fold_to_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_elem.s.chunks, w.s_elem.nch,
+                                                         w.s_scatter.s.chunks, w.s_scatter.nch,
+                                                         1, op->red);
+      comm->allreduce(1, comm->user);
+      red_alpha_kernel<<<1, 1, 0, ctx->stream>>>(op->red, w.st);
+      cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.p, w.q, w.r, diag, n,
+                                                            w.s_vec.s, op->notown);
+      fold_to_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, nullptr,
+                                                         0, 2, op->red);
+      comm->allreduce(2, comm->user);
+      red_beta_kernel<<<1, 1, 0, ctx->stream>>>(op->red, w.st);
+      cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.r, diag, w.p, n);
+      ctx->launched(6);
+      TFEM_CUDA(cudaGetLastError());
+   };
 
    auto read_state = [&]() {
       TFEM_CUDA(cudaMemcpyAsync(w.host_st, w.st, sizeof(CgState), cudaMemcpyDeviceToHost,
@@ -623,13 +787,21 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
    if (cb) {
       std::vector<double> hx(n);
       while (!hs.done) {
-         enqueue_iteration(ctx, op, w, xb, diag);
+         if (comm) dist_iteration();
+         else enqueue_iteration(ctx, op, w, xb, diag);
          hs = read_state();
          if (hs.status == 0 && hs.it > 0) {
             TFEM_CUDA(cudaMemcpy(hx.data(), xb.x[hs.cur], sizeof(double) * n,
                                  cudaMemcpyDeviceToHost));
             cb(hs.it, hx.data(), n, user);
          }
+      }
+   } else if (comm) {
+      // Eager: the hooks enqueue communication on the stream.  All ranks see
+      // the same scalars, hence the same stop decision at the same batch.
+      while (!hs.done) {
+         for (int k = 0; k < 8; k++) dist_iteration();
+         hs = read_state();
       }
    } else {
       // Batches of iterations as one graph; the batch length keeps the

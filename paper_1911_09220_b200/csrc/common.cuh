@@ -111,7 +111,9 @@ struct tfem_geometry {
    int64_t ne = 0;
    double *ctrl = nullptr; // [e][l][dim] (null for Cartesian)
    bool cartesian = false;
-   int n[3] = {0, 0, 0};
+   int n[3] = {0, 0, 0};        // local cells per axis
+   int origin[3] = {0, 0, 0};   // cell offset inside the global mesh
+   int n_global[3] = {0, 0, 0}; // global cells per axis
    double ext[3] = {1.0, 1.0, 1.0};
 };
 
@@ -135,6 +137,14 @@ struct tfem_operator {
    int64_t n_ess = 0;
    int32_t *ess = nullptr;      // sorted list
    uint32_t *ess_mask = nullptr; // bitmap over DOFs
+   uint32_t *notown = nullptr;   // bitmap: DOFs owned by another rank (dist)
+   bool has_comm = false;        // distributed: CG calls the hooks below
+   tfem_comm comm{};
+   int n_peers = 0;
+   int64_t n_send[TFEM_MAX_PEERS] = {}, n_recv[TFEM_MAX_PEERS] = {};
+   int32_t *send_idx[TFEM_MAX_PEERS] = {}, *recv_idx[TFEM_MAX_PEERS] = {}; // device
+   double *send_buf[TFEM_MAX_PEERS] = {}, *recv_buf[TFEM_MAX_PEERS] = {}; // caller's
+   double *red = nullptr;                                                // caller's
    int32_t *rowptr = nullptr, *cols = nullptr;
    double *vals = nullptr;
 };
@@ -161,7 +171,9 @@ void eval_matrices(int p, int node_kind, int nq, int rule, double *B, double *G)
 
 // Launch helpers implemented per translation unit.
 void vec_fill(tfem_ctx *ctx, double *d, int64_t n, double v);
-double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n);
+// Optional: skip DOFs in `notown`, then sum over ranks with the comm hook.
+double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n,
+               const tfem_operator *dist = nullptr);
 
 // Restriction / layout (restriction.cu)
 tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne, int64_t ndofs,
@@ -174,7 +186,8 @@ void restriction_mult_transpose(tfem_ctx *ctx, const tfem_restriction *r, const 
 // x . y partials.  Returns the grid size (for the dot sink).
 int64_t scatter_shared(tfem_ctx *ctx, const tfem_restriction *r, const double *evec,
                        const double *x, double *y, bool overwrite, const uint32_t *ess_out,
-                       const DotSink *dot, const int *done, bool exact);
+                       const DotSink *dot, const int *done, bool exact,
+                       const uint32_t *notown = nullptr);
 int64_t scatter_grid(const tfem_restriction *r);
 
 // PA kernels (apply.cu)
@@ -182,6 +195,7 @@ struct ApplyFlags {
    bool overwrite = false;   // y = (else y +=)
    const uint32_t *mask_in = nullptr;  // zero gathered essential DOFs
    const uint32_t *ess_out = nullptr;  // y[ess] = x[ess]
+   const uint32_t *notown = nullptr;   // excluded from the dot (other rank's DOFs)
    DotSink dot;                        // element-kernel x . y partials
    DotSink dot_scatter;                // scatter-kernel x . y partials
    const int *done = nullptr;          // device flag: skip when set (CG)

@@ -23,6 +23,7 @@ struct ApplyArgs {
    int overwrite;
    const uint32_t *mask_in;
    const uint32_t *ess_out;
+   const uint32_t *notown; // DOFs owned by another rank: left out of the dot
    DotSink dot;     // fused x . y partials (CG's p . q)
    const int *done; // CG stop flag: skip the work once the solve has ended
 };

@@ -27,7 +27,9 @@ struct GeoSource {
    int dim;
    int64_t ne;
    const double *ctrl; // [e][l][dim] or null (Cartesian)
-   int n[3];
+   int n[3];           // local cells per axis
+   int origin[3];      // cell offset in the global mesh
+   int ng[3];          // global cells per axis
    double ext[3];
 };
 
@@ -39,12 +41,13 @@ __device__ __forceinline__ double S(double a, double b) { return __dsub_rn(a, b)
 __device__ __forceinline__ double ctrl_at(const GeoSource &g, int64_t e, int l, int r, int n1)
 {
    if (g.ctrl) return g.ctrl[(e * (g.dim == 2 ? n1 * n1 : n1 * n1 * n1) + l) * g.dim + r];
-   // make_cartesian vertex coordinate width * i / nx (mesh.cpp:296)
+   // make_cartesian vertex coordinate width * i / nx (mesh.cpp:296), i global
    int64_t idx;
    if (r == 0) idx = e % g.n[0] + (l & 1);
    else if (r == 1) idx = (e / g.n[0]) % g.n[1] + ((l >> 1) & 1);
    else idx = e / ((int64_t)g.n[0] * g.n[1]) + ((l >> 2) & 1);
-   return __ddiv_rn(M(g.ext[r], static_cast<double>(idx)), static_cast<double>(g.n[r]));
+   idx += g.origin[r];
+   return __ddiv_rn(M(g.ext[r], static_cast<double>(idx)), static_cast<double>(g.ng[r]));
 }
 
 // J[r][s] = d x_r / d xh_s at the lattice point (px, py, pz) of the tables
@@ -225,6 +228,8 @@ GeoSource source_of(const tfem_geometry *g)
    s.ctrl = g->ctrl;
    for (int d = 0; d < 3; d++) {
       s.n[d] = g->n[d];
+      s.origin[d] = g->origin[d];
+      s.ng[d] = g->n_global[d];
       s.ext[d] = g->ext[d];
    }
    return s;

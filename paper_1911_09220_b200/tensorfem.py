@@ -224,6 +224,25 @@ class FeSpace:
         return cls(dev, dim, order, r, g, tuple(n))
 
     @classmethod
+    def cartesian_box(cls, dev: Device, n_local: Sequence[int], origin: Sequence[int],
+                      n_global: Sequence[int], order: int,
+                      extents: Optional[Sequence[float]] = None) -> "FeSpace":
+        """The n_local block at cell offset `origin` of make_cartesian(n_global)
+        (one rank's slab): local DOF numbering, global vertex coordinates."""
+        dim = len(n_local)
+        pad = lambda v: (C.c_int * 3)(*(list(v) + [0] * (3 - dim)))
+        r = abi.vp()
+        check(lib().tfem_restriction_cartesian(dev.h, dim, pad(n_local), order, C.byref(r)))
+        g = abi.vp()
+        ext = (C.c_double * 3)(*(list(extents or [1.0] * dim) + [0.0] * (3 - dim)))
+        rc = lib().tfem_geometry_cartesian_box(dev.h, dim, pad(n_local), pad(origin),
+                                               pad(n_global), ext, C.byref(g))
+        if rc:
+            lib().tfem_restriction_destroy(r)
+            check(rc)
+        return cls(dev, dim, order, r, g, tuple(n_local))
+
+    @classmethod
     def from_mesh(cls, dev: Device, dim: int, order: int, elem_dofs: np.ndarray, n_dofs: int,
                   ctrl: np.ndarray, geom_order: int = 1) -> "FeSpace":
         """A space from a host element -> DOF table (FeSpace::element_dofs,

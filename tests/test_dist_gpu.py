@@ -1,0 +1,138 @@
+"""GPU: the library's distributed CG loop (tfem_operator_set_comm hooks,
+owned-DOF dots, halo pack/unpack, rank-local folds + allreduce).
+
+* 1 rank over NCCL: bit-identical iterates to the single-device solver.
+* 2 ranks sharing the one GPU over gloo (host-staged hooks; no kernel waits
+  on another process): same iteration count as the single-device solve of
+  the global problem, same solution on owned DOFs.
+"""
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+pytestmark = pytest.mark.gpu
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def single_device_solution(dev, n_global, p, tol, its, seed):
+    import paper_1911_09220_b200 as tf
+    from paper_1911_09220_b200.dist import lattice
+    sp = tf.FeSpace.cartesian(dev, n_global, p)
+    a = tf.BilinearForm(sp)
+    a.add_diffusion(1.0)
+    a.assemble()
+    ess = sp.essential_true_dofs()
+    op = tf.ConstrainedOperator(a, ess)
+    L = lattice(sp.element_dofs(), n_global, p, sp.n_dofs)
+    return sp, op, ess, L
+
+
+def test_one_rank_nccl_matches_single_device(dev):
+    import torch
+    import torch.distributed as tdist
+    import paper_1911_09220_b200 as tf
+    from paper_1911_09220_b200.dist import DistOperator, partition
+    tdist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{free_port()}", rank=0,
+                             world_size=1)
+    try:
+        n, p = (40, 30), 3
+        d = DistOperator(dev, partition(2, n, p, 0, 1))
+        sp, op, ess, _ = single_device_solution(dev, n, p, 1e-10, 2000, 0)
+        assert (d.plan.ess == ess).all() and len(d.plan.not_owned) == 0
+        b = np.random.default_rng(4).uniform(-1, 1, sp.n_dofs)
+        b[ess] = 0.0
+        r1 = tf.cg_solve(d.op, b, 1e-10, 2000, d.diag)
+        r2 = tf.cg_solve(op, b, 1e-10, 2000, op.diagonal())
+        assert r1.iterations == r2.iterations and r1.converged and r2.converged
+        assert (r1.x.numpy() == r2.x.numpy()).all()
+        r3 = tf.cg_solve(d.op, b, 0.0, 37, d.diag)       # exhaustion path
+        r4 = tf.cg_solve(op, b, 0.0, 37, op.diagonal())
+        assert r3.iterations == r4.iterations == 37
+        assert (r3.x.numpy() == r4.x.numpy()).all()
+    finally:
+        tdist.destroy_process_group()
+
+
+def _rank(rank, world, port, n, p, q):
+    sys.path.insert(0, str(ROOT))
+    try:
+        import torch
+        import torch.distributed as tdist
+        import paper_1911_09220_b200 as tf
+        from paper_1911_09220_b200.dist import DistOperator, lattice, partition
+        torch.cuda.set_device(0)
+        tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                 world_size=world)
+        dev = tf.Device(0)
+        d = DistOperator(dev, partition(len(n), n, p, rank, world))
+        sp, op, ess, Lg = single_device_solution(dev, n, p, 1e-10, 3000, 0)
+        dims = tuple(k * p + 1 for k in n)
+        table = np.full(int(np.prod(dims)), -1, dtype=np.int64)
+        table[np.ravel_multi_index(tuple(Lg.T), dims, order="F")] = np.arange(len(Lg))
+        L = d.lattice.copy()
+        L[:, -1] += d.slab.lo * p
+        l2g = table[np.ravel_multi_index(tuple(L.T), dims, order="F")]
+        # smooth right-hand side: random ones amplify round-off over hundreds
+        # of iterations (the reference's CG fixtures are smooth, too)
+        bg = np.prod([np.sin(np.pi * Lg[:, k] / (n[k] * p)) for k in range(len(n))], axis=0)
+        bg[ess] = 0.0
+        # operator on owned DOFs: bit-identical to the global device operator
+        xg = np.random.default_rng(9).uniform(-1, 1, sp.n_dofs)
+        y = tf.Vector(dev, d.space.n_dofs)
+        plain = tf.BilinearForm(d.space)
+        plain.add_diffusion(1.0)
+        plain.assemble()
+        plain.mult_true(xg[l2g], y)
+        yg = tf.Vector(dev, sp.n_dofs)
+        a = tf.BilinearForm(sp)
+        a.add_diffusion(1.0)
+        a.assemble()
+        a.mult_true(xg, yg)
+        own = d.plan.owned
+        assert (y.numpy()[own] == yg.numpy()[l2g[own]]).all()
+        rd = tf.cg_solve(d.op, bg[l2g], 1e-9, 3000, d.diag)
+        rg = tf.cg_solve(op, bg, 1e-9, 3000, op.diagonal())
+        assert rd.converged and rg.converged and rd.iterations == rg.iterations, \
+            (rd.iterations, rg.iterations)
+        err = np.abs(rd.x.numpy()[own] - rg.x.numpy()[l2g[own]]).max()
+        assert err <= 1e-9 * np.abs(rg.x.numpy()).max(), err
+        q.put((rank, "ok", rd.iterations))
+    except Exception:
+        import traceback
+        q.put((rank, "fail", traceback.format_exc()))
+    finally:
+        try:
+            import torch.distributed as tdist
+            if tdist.is_initialized():
+                tdist.destroy_process_group()
+        except Exception:
+            pass
+
+
+@pytest.mark.parametrize("n,p", [((24, 18), 3), ((6, 5, 8), 2)])
+def test_two_ranks_share_one_gpu_gloo(dev, n, p):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, n, p, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for pr in procs:
+        pr.join(timeout=60)
+        if pr.is_alive():
+            pr.kill()
+    bad = [r for r in res if r[1] != "ok"]
+    assert not bad, bad[0][2]
