@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--order", type=int, default=3)
     ap.add_argument("--cells", type=int, default=0, help="cells per axis (0: ~10M DOFs)")
     ap.add_argument("--iters", type=int, default=200)
-    ap.add_argument("--numerics", default="reference", choices=["reference", "fma"])
+    ap.add_argument("--numerics", default="fma", choices=["reference", "fma"])
     ap.add_argument("--cpu-iters", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -292,6 +292,24 @@ def run_tfem(args):
     clocks = clk.summary()
     value = N * args.iters * args.steps / t_value / 1e9
 
+    # ---- the bit-exact numerics (reference operation order), same workload
+    exact = None
+    if args.numerics == "fma" and args.dim == 2:
+        dev.set_numerics("reference")
+        for _ in range(2):
+            step()
+        dev.sync()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ev1.synchronize()
+        t_exact = ev0.elapsed_time(ev1) / 1e3
+        exact = {"value": N * args.iters * args.steps / t_exact / 1e9, "unit": "GDOF/s",
+                 "ms_per_step": 1e3 * t_exact / args.steps,
+                 "note": "TFEM_NUMERICS_REFERENCE: bit-identical to the CPU reference"}
+        dev.set_numerics(args.numerics)
+
     # ---- roofline of the dominant kernel: the operator application
     nc = 3 if args.dim == 2 else 6
     nq = p + 2
@@ -363,7 +381,7 @@ def run_tfem(args):
         "cg_roofline": {"achieved": cg_achieved, "frac": cg_achieved / peak, "unit": "GB/s",
                         "bytes_per_dof_iteration": b_it / N},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
-        "setup_s": setup_s,
+        "bit_exact_numerics": exact, "setup_s": setup_s,
     }
     print(json.dumps(line))
 

@@ -43,7 +43,13 @@ inline void check(int rc)
 
 class Device {
 public:
-   explicit Device(int device = 0) { check(tfem_ctx_create(device, &ctx_)); }
+   /// numerics: TFEM_NUMERICS_FMA (default) or TFEM_NUMERICS_REFERENCE
+   /// (the reference's operation order, bit-identical results).
+   explicit Device(int device = 0, int numerics = TFEM_NUMERICS_FMA)
+   {
+      check(tfem_ctx_create(device, &ctx_));
+      check(tfem_ctx_set_numerics(ctx_, numerics));
+   }
    ~Device() { tfem_ctx_destroy(ctx_); }
    Device(const Device &) = delete;
    Device &operator=(const Device &) = delete;

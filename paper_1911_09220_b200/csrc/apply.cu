@@ -7,6 +7,10 @@
 // (forms.cpp:289-295) -- deterministic, no atomics.
 #include "kernels.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
 namespace tfem {
 
 namespace {
@@ -201,14 +205,28 @@ Tables tables_of(const tfem_pa *pa)
 
 KernelPick pick(const tfem_ctx *ctx, const tfem_pa *pa)
 {
+   // TFEM_APPLY2D=reg selects the plain one-thread-per-element kernel (A/B).
+   static const bool use_tma = [] {
+      const char *v = std::getenv("TFEM_APPLY2D");
+      return !(v && std::string(v) == "reg");
+   }();
    const bool exact = pa->dim == 2 && ctx->numerics == TFEM_NUMERICS_REFERENCE;
-   KernelPick k = (pa->dim == 2 && pa->p <= 3) ? pick_apply2d_reg(pa->p, pa->nq, pa->kind, exact)
-                                               : pick_apply_grp(pa->dim, pa->p, pa->nq, pa->kind, exact);
+   KernelPick k;
+   if (pa->dim == 2 && pa->p <= 3)
+      k = use_tma ? pick_apply2d_tma(pa->p, pa->nq, pa->kind, exact, ctx->sm_count)
+                  : pick_apply2d_reg(pa->p, pa->nq, pa->kind, exact);
+   else
+      k = pick_apply_grp(pa->dim, pa->p, pa->nq, pa->kind, exact);
    if (!k.launch) invalid("pa_apply: unsupported (order, points) pair on the device");
    return k;
 }
 
-unsigned elem_blocks(const KernelPick &k, int64_t ne) { return blocks_for(ne, k.elems_per_block); }
+unsigned elem_blocks(const KernelPick &k, int64_t ne)
+{
+   const int64_t b = blocks_for(ne, k.elems_per_block);
+   return static_cast<unsigned>(k.persistent_blocks > 0 ? std::min<int64_t>(b, k.persistent_blocks)
+                                                        : b);
+}
 
 } // namespace
 

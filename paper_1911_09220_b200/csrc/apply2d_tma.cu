@@ -1,0 +1,363 @@
+// K2, 2D p <= 3: the thread-per-element sum factorisation of apply2d_reg.cu
+// fed by an asynchronous bulk-copy pipeline (sm_90+ cp.async.bulk + mbarrier;
+// SASS UBLKCP).
+//
+// Persistent blocks of 128 threads walk tiles of 128 consecutive elements.
+// For every tile the qdata is streamed as Q "slices" (one per qy: the nc*Q
+// planes (c, qy, qx), each a contiguous 1 KB run of the [(c*nqd+q)][ne_pad]
+// layout) through a ring of kStages shared-memory stages, and the element
+// map (D1^2 planes of 512 B) through a double buffer one tile ahead.  One
+// elected thread issues the copies; consumers wait on the stage's mbarrier,
+// read their element's factors with conflict-free ld.shared, and a block
+// barrier after each slice frees the stage for the copy kSt slices ahead.
+// The DRAM stream therefore no longer depends on how many loads the
+// 254-register compute threads can keep in flight (the one-thread kernel's
+// limiter: long-scoreboard stalls on each slice's first use).
+//
+// Arithmetic is the same code path as apply2d_reg.cu (EXACT = reference
+// operation order, bit-identical).
+#include "kernels.cuh"
+
+namespace tfem {
+
+namespace {
+
+constexpr int kTile = 128;  // elements per tile = threads per block
+constexpr int kStages = 4;  // qdata slice ring depth
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                "r"(bytes)
+                : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+   asm volatile("{\n"
+                ".reg .pred p;\n"
+                "WAIT_%=:\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                "@!p bra WAIT_%=;\n"
+                "}\n" ::"r"(smem_u32(bar)),
+                "r"(parity)
+                : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+                "[%3];" ::"r"(smem_u32(dst)),
+                "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                : "memory");
+}
+
+template <int P, int Q, int KIND>
+struct TmaSmem {
+   static constexpr int D1 = P + 1, ND = D1 * D1;
+   static constexpr int NC = KIND == TFEM_MASS ? 1 : 3;
+   static constexpr int SLICE = NC * Q; // planes per qy slice
+   double q[kStages][SLICE][kTile];
+   uint32_t gmap[2][ND][kTile];
+   uint64_t full[kStages]; // slice landed (tx count)
+   uint64_t gfull[2];
+};
+
+// Issue qdata slice `k` of this block (tile lt = k / Q, qy = k % Q).
+template <int P, int Q, int KIND>
+__device__ __forceinline__ void issue_slice(TmaSmem<P, Q, KIND> &sm, const ApplyArgs &a,
+                                            int64_t ntiles, int64_t k)
+{
+   constexpr int NQD = Q * Q, SLICE = TmaSmem<P, Q, KIND>::SLICE;
+   const int64_t lt = k / Q;
+   const int qy = static_cast<int>(k % Q);
+   const int64_t t = blockIdx.x + lt * gridDim.x;
+   if (t >= ntiles) return;
+   const int64_t e0 = t * kTile;
+   const unsigned bytes = static_cast<unsigned>(a.ne_pad - e0 < kTile ? a.ne_pad - e0 : kTile) * 8u;
+   const int s = static_cast<int>(k % kStages);
+   mbar_expect_tx(&sm.full[s], bytes * SLICE);
+#pragma unroll
+   for (int j = 0; j < SLICE; j++) {
+      const int c = j / Q, qx = j % Q;
+      const int64_t plane = c * NQD + qy * Q + qx;
+      bulk_g2s(&sm.q[s][j][0], a.qdata + plane * a.ne_pad + e0, bytes, &sm.full[s]);
+   }
+}
+
+template <int P, int Q, int KIND>
+__device__ __forceinline__ void issue_gmap(TmaSmem<P, Q, KIND> &sm, const ApplyArgs &a,
+                                           int64_t ntiles, int64_t lt)
+{
+   constexpr int ND = (P + 1) * (P + 1);
+   const int64_t t = blockIdx.x + lt * gridDim.x;
+   if (t >= ntiles) return;
+   const int64_t e0 = t * kTile;
+   const unsigned bytes = static_cast<unsigned>(a.ne_pad - e0 < kTile ? a.ne_pad - e0 : kTile) * 4u;
+   const int b = static_cast<int>(lt & 1);
+   mbar_expect_tx(&sm.gfull[b], bytes * ND);
+#pragma unroll
+   for (int i = 0; i < ND; i++) bulk_g2s(&sm.gmap[b][i][0], a.gmap + i * a.ne_pad + e0, bytes, &sm.gfull[b]);
+}
+
+// One qy slice of the diffusion chain for the calling thread's element:
+// d = T B^t / T G^t at (qx, qy), w = D d, then S = G^t w / B^t w over qx and
+// v += S B / S G (reference order; FIRST starts the v sums with a product).
+template <int P, int Q, bool EXACT, bool FIRST>
+__device__ __forceinline__ void diffusion_slice(const ApplyArgs &a, int qy, const double (&T1)[Q][P + 1],
+                                                const double (&T2)[Q][P + 1],
+                                                const double (*qs)[kTile], int tid,
+                                                double (&vx)[P + 1][P + 1],
+                                                double (&vy)[P + 1][P + 1])
+{
+   constexpr int D1 = P + 1;
+   double wx[Q], wy[Q];
+#pragma unroll
+   for (int qx = 0; qx < Q; qx++) {
+      double dx = mul<EXACT>(T1[qx][0], a.t.B[qy][0]);
+      double dy = mul<EXACT>(T2[qx][0], a.t.G[qy][0]);
+#pragma unroll
+      for (int b = 1; b < D1; b++) {
+         dx = mac<EXACT>(dx, T1[qx][b], a.t.B[qy][b]);
+         dy = mac<EXACT>(dy, T2[qx][b], a.t.G[qy][b]);
+      }
+      const double d0 = qs[0 * Q + qx][tid], d1 = qs[1 * Q + qx][tid], d2 = qs[2 * Q + qx][tid];
+      wx[qx] = add<EXACT>(mul<EXACT>(d0, dx), mul<EXACT>(d1, dy));
+      wy[qx] = add<EXACT>(mul<EXACT>(d1, dx), mul<EXACT>(d2, dy));
+   }
+#pragma unroll
+   for (int i = 0; i < D1; i++) {
+      double sx = mul<EXACT>(a.t.G[0][i], wx[0]);
+      double sy = mul<EXACT>(a.t.B[0][i], wy[0]);
+#pragma unroll
+      for (int qx = 1; qx < Q; qx++) {
+         sx = mac<EXACT>(sx, a.t.G[qx][i], wx[qx]);
+         sy = mac<EXACT>(sy, a.t.B[qx][i], wy[qx]);
+      }
+#pragma unroll
+      for (int b = 0; b < D1; b++) {
+         if (FIRST) {
+            vx[i][b] = mul<EXACT>(sx, a.t.B[qy][b]);
+            vy[i][b] = mul<EXACT>(sy, a.t.G[qy][b]);
+         } else {
+            vx[i][b] = mac<EXACT>(vx[i][b], sx, a.t.B[qy][b]);
+            vy[i][b] = mac<EXACT>(vy[i][b], sy, a.t.G[qy][b]);
+         }
+      }
+   }
+}
+
+template <int P, int Q, bool EXACT, bool FIRST>
+__device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const double (&T)[Q][P + 1],
+                                           const double (*qs)[kTile], int tid,
+                                           double (&R)[P + 1][P + 1])
+{
+   constexpr int D1 = P + 1;
+   double w[Q];
+#pragma unroll
+   for (int qx = 0; qx < Q; qx++) {
+      double u = mul<EXACT>(T[qx][0], a.t.B[qy][0]);
+#pragma unroll
+      for (int b = 1; b < D1; b++) u = mac<EXACT>(u, T[qx][b], a.t.B[qy][b]);
+      w[qx] = mul<EXACT>(u, qs[qx][tid]);
+   }
+#pragma unroll
+   for (int i = 0; i < D1; i++) {
+      double s = mul<EXACT>(a.t.B[0][i], w[0]);
+#pragma unroll
+      for (int qx = 1; qx < Q; qx++) s = mac<EXACT>(s, a.t.B[qx][i], w[qx]);
+#pragma unroll
+      for (int b = 0; b < D1; b++)
+         R[i][b] = FIRST ? mul<EXACT>(s, a.t.B[qy][b]) : mac<EXACT>(R[i][b], s, a.t.B[qy][b]);
+   }
+}
+
+template <int P, int Q, int KIND, bool EXACT>
+__global__ void __launch_bounds__(kTile) apply2d_tma_kernel(const ApplyArgs a)
+{
+   constexpr int D1 = P + 1, ND = D1 * D1;
+   if (a.done && *a.done) return;
+   extern __shared__ __align__(128) unsigned char smem_raw[];
+   auto &sm = *reinterpret_cast<TmaSmem<P, Q, KIND> *>(smem_raw);
+   const int tid = threadIdx.x;
+   const int64_t ntiles = (a.ne + kTile - 1) / kTile;
+   const int64_t my_tiles =
+      blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+   const int64_t n_slices = my_tiles * Q;
+   if (tid == 0) {
+      for (int s = 0; s < kStages; s++) mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.gfull[0], 1);
+      mbar_init(&sm.gfull[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+   }
+   __syncthreads();
+   if (tid == 0) {
+      issue_gmap<P, Q, KIND>(sm, a, ntiles, 0);
+      for (int64_t k = 0; k < kStages && k < n_slices; k++) issue_slice<P, Q, KIND>(sm, a, ntiles, k);
+   }
+   double dot = 0.0;
+   int64_t k = 0; // slice counter
+   // Wait for slice k; after use a block barrier frees its stage and thread 0
+   // refills it with slice k + kStages.  (Per-warp mbarrier releases were
+   // measured slower: the producer warp then trails the slowest warp.)
+   auto acquire = [&]() -> const double(*)[kTile] {
+      const int s = static_cast<int>(k % kStages);
+      mbar_wait(&sm.full[s], static_cast<unsigned>((k / kStages) & 1));
+      return sm.q[s];
+   };
+   auto release = [&]() {
+      __syncthreads();
+      if (tid == 0 && k + kStages < n_slices) issue_slice<P, Q, KIND>(sm, a, ntiles, k + kStages);
+      k++;
+   };
+   for (int64_t lt = 0; lt < my_tiles; lt++) {
+      const int64_t e = (blockIdx.x + lt * gridDim.x) * kTile + tid;
+      const bool live = e < a.ne;
+      const int gb = static_cast<int>(lt & 1);
+      mbar_wait(&sm.gfull[gb], static_cast<unsigned>((lt >> 1) & 1));
+      // the other map buffer was last read at the start of tile lt-1, before
+      // that tile's slice barriers: prefetch the next tile's map into it
+      if (tid == 0) issue_gmap<P, Q, KIND>(sm, a, ntiles, lt + 1);
+      uint32_t dof[ND];
+      double V[D1][D1];
+#pragma unroll
+      for (int i = 0; i < ND; i++) {
+         dof[i] = sm.gmap[gb][i][tid];
+         const uint32_t d = dof[i] & kDofMask;
+         double v = live ? __ldg(a.x + d) : 0.0;
+         if (a.mask_in && live && bit_set(a.mask_in, d)) v = 0.0;
+         V[i % D1][i / D1] = v;
+      }
+      double R[D1][D1];
+      if (KIND == TFEM_DIFFUSION) {
+         double T1[Q][D1], T2[Q][D1];
+#pragma unroll
+         for (int qx = 0; qx < Q; qx++)
+#pragma unroll
+            for (int b = 0; b < D1; b++) {
+               double s1 = mul<EXACT>(a.t.G[qx][0], V[0][b]);
+               double s2 = mul<EXACT>(a.t.B[qx][0], V[0][b]);
+#pragma unroll
+               for (int kk = 1; kk < D1; kk++) {
+                  s1 = mac<EXACT>(s1, a.t.G[qx][kk], V[kk][b]);
+                  s2 = mac<EXACT>(s2, a.t.B[qx][kk], V[kk][b]);
+               }
+               T1[qx][b] = s1;
+               T2[qx][b] = s2;
+            }
+         double vx[D1][D1], vy[D1][D1];
+#pragma unroll
+         for (int qy = 0; qy < Q; qy++) { // unrolled: table indices stay immediates
+            if (qy == 0) diffusion_slice<P, Q, EXACT, true>(a, qy, T1, T2, acquire(), tid, vx, vy);
+            else diffusion_slice<P, Q, EXACT, false>(a, qy, T1, T2, acquire(), tid, vx, vy);
+            release();
+         }
+#pragma unroll
+         for (int i = 0; i < D1; i++)
+#pragma unroll
+            for (int b = 0; b < D1; b++) R[i][b] = add<EXACT>(vx[i][b], vy[i][b]);
+      } else {
+         double T[Q][D1];
+#pragma unroll
+         for (int qx = 0; qx < Q; qx++)
+#pragma unroll
+            for (int b = 0; b < D1; b++) {
+               double s = mul<EXACT>(a.t.B[qx][0], V[0][b]);
+#pragma unroll
+               for (int kk = 1; kk < D1; kk++) s = mac<EXACT>(s, a.t.B[qx][kk], V[kk][b]);
+               T[qx][b] = s;
+            }
+#pragma unroll
+         for (int qy = 0; qy < Q; qy++) {
+            if (qy == 0) mass_slice<P, Q, EXACT, true>(a, qy, T, acquire(), tid, R);
+            else mass_slice<P, Q, EXACT, false>(a, qy, T, acquire(), tid, R);
+            release();
+         }
+      }
+      if (live) {
+#pragma unroll
+         for (int i = 0; i < ND; i++) {
+            const uint32_t g = dof[i];
+            double r = R[i % D1][i / D1];
+            if (g & kExclusive) {
+               const uint32_t d = g & kDofMask;
+               if (!a.overwrite) r = add<EXACT>(a.y[d], r);
+               if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
+               a.y[d] = r;
+               if (a.dot && !(a.notown && bit_set(a.notown, d)))
+                  dot = mac<EXACT>(dot, __ldg(a.x + d), r);
+            } else {
+               a.evec[i * a.ne_pad + e] = r;
+            }
+         }
+      }
+   }
+   if (a.dot) {
+      const double v[1] = {dot};
+      emit<kTile, 1>(a.dot, v);
+   }
+}
+
+int g_sm_count = 0;
+
+template <int P, int Q, int KIND, bool EXACT>
+void launch(const ApplyArgs &a, cudaStream_t s, unsigned /*blocks*/)
+{
+   const size_t smem = sizeof(TmaSmem<P, Q, KIND>);
+   static const bool once = [&] {
+      cudaFuncSetAttribute(apply2d_tma_kernel<P, Q, KIND, EXACT>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      return true;
+   }();
+   (void)once;
+   const int64_t ntiles = (a.ne + kTile - 1) / kTile;
+   const unsigned grid = static_cast<unsigned>(ntiles < 2 * (int64_t)g_sm_count ? ntiles : 2 * (int64_t)g_sm_count);
+   apply2d_tma_kernel<P, Q, KIND, EXACT><<<grid, kTile, smem, s>>>(a);
+}
+
+template <int P, int KIND>
+Launch pick_q(int nq, bool exact)
+{
+   if (nq == P + 2) return exact ? launch<P, P + 2, KIND, true> : launch<P, P + 2, KIND, false>;
+   if (nq == P + 1) return exact ? launch<P, P + 1, KIND, true> : launch<P, P + 1, KIND, false>;
+   return nullptr;
+}
+
+template <int KIND>
+Launch pick_p(int p, int nq, bool exact)
+{
+   switch (p) {
+   case 1: return pick_q<1, KIND>(nq, exact);
+   case 2: return pick_q<2, KIND>(nq, exact);
+   case 3: return pick_q<3, KIND>(nq, exact);
+   }
+   return nullptr;
+}
+
+} // namespace
+
+// Grid: min(tiles, 2 per SM) persistent blocks; the dot sink is sized by
+// elem_blocks_tma().
+KernelPick pick_apply2d_tma(int p, int nq, int kind, bool exact, int sm_count)
+{
+   g_sm_count = sm_count;
+   KernelPick k;
+   k.launch = kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact)
+                                : pick_p<TFEM_DIFFUSION>(p, nq, exact);
+   k.elems_per_block = kTile;
+   k.threads = kTile;
+   k.persistent_blocks = 2 * sm_count;
+   return k;
+}
+
+} // namespace tfem

@@ -343,7 +343,7 @@ int tfem_geometry_create(tfem_ctx *ctx, int dim, int order, int64_t n_elem, cons
       for (int d = 0; d < dim; d++) nc *= order + 1;
       const size_t bytes = sizeof(double) * static_cast<size_t>(n_elem * nc * dim);
       TFEM_CUDA(cudaMalloc(&g->ctrl, bytes));
-      TFEM_CUDA(cudaMemcpy(g->ctrl, ctrl, bytes, cudaMemcpyHostToDevice));
+      h2d(ctx->stream, g->ctrl, ctrl, bytes);
       *out = g;
    });
 }
@@ -464,7 +464,7 @@ int tfem_pa_qdata(const tfem_pa *pa, double *host)
       need(host, "PaData::d");
       const size_t n = static_cast<size_t>(pa->ncomp) * pa->nqd * pa->ne_pad;
       std::vector<double> dev(n);
-      TFEM_CUDA(cudaMemcpy(dev.data(), pa->qdata, sizeof(double) * n, cudaMemcpyDeviceToHost));
+      d2h(pa->ctx->stream, dev.data(), pa->qdata, sizeof(double) * n);
       for (int64_t e = 0; e < pa->ne; e++)
          for (int q = 0; q < pa->nqd; q++)
             for (int c = 0; c < pa->ncomp; c++) {

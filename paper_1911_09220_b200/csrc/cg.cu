@@ -367,14 +367,14 @@ T *dalloc(int64_t n)
 struct SinkStore {
    DotSink s;
    int64_t grid = 0, nch = 0;
-   void alloc(int64_t g, int nv)
+   void alloc(cudaStream_t stream, int64_t g, int nv)
    {
       grid = g;
       nch = n_chunks(g);
       s.partials = dalloc<double>(nv * g);
       s.chunks = dalloc<double>(nv * nch);
       s.tickets = dalloc<unsigned>(nch);
-      TFEM_CUDA(cudaMemset(s.tickets, 0, sizeof(unsigned) * nch));
+      TFEM_CUDA(cudaMemsetAsync(s.tickets, 0, sizeof(unsigned) * nch, stream));
    }
    void release()
    {
@@ -394,7 +394,7 @@ struct Workspace {
    CgState *host_st = nullptr; // pinned
    cudaGraphExec_t graph = nullptr;
    const double *g_diag = nullptr, *g_x = nullptr;
-   int g_batch = 0;
+   int g_batch = 0, g_numerics = -1;
    int64_t g_launches = 0;
    ~Workspace()
    {
@@ -431,16 +431,16 @@ Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
    w->xa = dalloc<double>(op->n);
    w->xb = dalloc<double>(op->n);
    if (op->csr) {
-      w->s_elem.alloc(blocks_for(op->n, kVecThreads), 1);
+      w->s_elem.alloc(ctx->stream, blocks_for(op->n, kVecThreads), 1);
    } else {
       // everything the iteration touches must exist before graph capture
       if (op->r->n_shared > 0) const_cast<tfem_restriction *>(op->r)->ensure_evec();
       int64_t ge = 0, gs = 0;
       pa_apply_grids(op->pa.back(), op->r, &ge, &gs);
-      w->s_elem.alloc(ge, 1);
-      if (gs > 0) w->s_scatter.alloc(gs, 1);
+      w->s_elem.alloc(ctx->stream, ge, 1);
+      if (gs > 0) w->s_scatter.alloc(ctx->stream, gs, 1);
    }
-   w->s_vec.alloc(vec_blocks(ctx, op->n), 2);
+   w->s_vec.alloc(ctx->stream, vec_blocks(ctx, op->n), 2);
    w->st = dalloc<CgState>(1);
    TFEM_CUDA(cudaMallocHost(&w->host_st, sizeof(CgState)));
    auto &ref = *w;
@@ -499,7 +499,7 @@ double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n,
    auto it = sinks.find(nb);
    if (it == sinks.end()) {
       SinkStore st;
-      st.alloc(nb, 1);
+      st.alloc(ctx->stream, nb, 1);
       it = sinks.emplace(nb, st).first;
    }
    const SinkStore &s = it->second;
@@ -538,7 +538,7 @@ void operator_set_ess(tfem_ctx *ctx, tfem_operator *op, int64_t n_ess, const int
    op->ess = dalloc<int32_t>(n_ess);
    const int64_t words = (op->n + 31) / 32;
    op->ess_mask = dalloc<uint32_t>(words);
-   TFEM_CUDA(cudaMemcpy(op->ess, ess, sizeof(int32_t) * n_ess, cudaMemcpyHostToDevice));
+   h2d(ctx->stream, op->ess, ess, sizeof(int32_t) * n_ess);
    TFEM_CUDA(cudaMemsetAsync(op->ess_mask, 0, sizeof(uint32_t) * words, ctx->stream));
    set_bits_kernel<<<blocks_for(n_ess, 256), 256, 0, ctx->stream>>>(op->ess, n_ess,
                                                                    op->ess_mask);
@@ -558,7 +558,7 @@ void operator_set_comm(tfem_ctx *ctx, tfem_operator *op, const tfem_comm &comm,
       for (int64_t i = 0; i < n; i++)
          if (idx[i] < 0 || idx[i] >= op->n) invalid("tfem_operator_set_comm: DOF out of range");
       int32_t *d = dalloc<int32_t>(n);
-      if (n) TFEM_CUDA(cudaMemcpy(d, idx, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+      h2d(ctx->stream, d, idx, sizeof(int32_t) * n);
       return d;
    };
    for (int k = 0; k < op->n_peers; k++) {
@@ -624,9 +624,9 @@ tfem_operator *operator_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, con
    op->rowptr = dalloc<int32_t>(n + 1);
    op->cols = dalloc<int32_t>(nnz);
    op->vals = dalloc<double>(nnz);
-   TFEM_CUDA(cudaMemcpy(op->rowptr, rowptr, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice));
-   TFEM_CUDA(cudaMemcpy(op->cols, cols, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
-   TFEM_CUDA(cudaMemcpy(op->vals, vals, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+   h2d(ctx->stream, op->rowptr, rowptr, sizeof(int32_t) * (n + 1));
+   h2d(ctx->stream, op->cols, cols, sizeof(int32_t) * nnz);
+   h2d(ctx->stream, op->vals, vals, sizeof(double) * nnz);
    return op;
 }
 
@@ -791,8 +791,7 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
          else enqueue_iteration(ctx, op, w, xb, diag);
          hs = read_state();
          if (hs.status == 0 && hs.it > 0) {
-            TFEM_CUDA(cudaMemcpy(hx.data(), xb.x[hs.cur], sizeof(double) * n,
-                                 cudaMemcpyDeviceToHost));
+            d2h(ctx->stream, hx.data(), xb.x[hs.cur], sizeof(double) * n);
             cb(hs.it, hx.data(), n, user);
          }
       }
@@ -807,7 +806,8 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
       // Batches of iterations as one graph; the batch length keeps the
       // per-batch host round trip small against the work it covers.
       const int batch = n >= (1 << 22) ? 4 : 16;
-      if (!w.graph || w.g_diag != diag || w.g_x != x || w.g_batch != batch) {
+      if (!w.graph || w.g_diag != diag || w.g_x != x || w.g_batch != batch ||
+          w.g_numerics != ctx->numerics) {
          if (w.graph) {
             cudaGraphExecDestroy(w.graph);
             w.graph = nullptr;
@@ -824,6 +824,7 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
          w.g_diag = diag;
          w.g_x = x;
          w.g_batch = batch;
+         w.g_numerics = ctx->numerics;
       }
       while (!hs.done) {
          TFEM_CUDA(cudaGraphLaunch(w.graph, ctx->stream));

@@ -31,6 +31,22 @@ inline void cuda_check(cudaError_t e, const char *what)
 }
 #define TFEM_CUDA(call) ::tfem::cuda_check((call), #call)
 
+// Copies / fills ordered on a context's (non-blocking) stream.  Never use the
+// legacy-stream cudaMemcpy / cudaMemset next to kernels on ctx->stream: the
+// non-blocking stream does not wait for the legacy one.
+inline void h2d(cudaStream_t s, void *dst, const void *src, size_t bytes)
+{
+   if (!bytes) return;
+   TFEM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+   TFEM_CUDA(cudaStreamSynchronize(s));
+}
+inline void d2h(cudaStream_t s, void *dst, const void *src, size_t bytes)
+{
+   if (!bytes) return;
+   TFEM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+   TFEM_CUDA(cudaStreamSynchronize(s));
+}
+
 // Flag bit on an element-map entry: the DOF has exactly one element slot, so
 // the element kernel owns it and writes it directly (no E-vector round trip).
 constexpr uint32_t kExclusive = 0x80000000u;
@@ -61,7 +77,7 @@ struct Reducer {
 struct tfem_ctx {
    int device = 0;
    cudaStream_t stream = nullptr;
-   int numerics = TFEM_NUMERICS_REFERENCE;
+   int numerics = TFEM_NUMERICS_FMA;
    int sm_count = 148;
    int64_t launches = 0;
    tfem::Reducer red;

@@ -34,12 +34,16 @@ struct KernelPick {
    Launch launch = nullptr;
    int elems_per_block = 1;
    int threads = 128;
+   int persistent_blocks = 0; // > 0: grid = min(ceil(ne / elems_per_block), this)
 };
 
 constexpr int kElemThreads2D = 128;
 
 // Register-resident thread-per-element kernels: 2D, p <= 3.
 KernelPick pick_apply2d_reg(int p, int nq, int kind, bool exact);
+// The same arithmetic fed by a cp.async.bulk / mbarrier qdata pipeline
+// (persistent blocks): 2D, p <= 3.
+KernelPick pick_apply2d_tma(int p, int nq, int kind, bool exact, int sm_count);
 // Thread-group-per-element kernels through shared memory: 2D p >= 4, 3D.
 KernelPick pick_apply_grp(int dim, int p, int nq, int kind, bool exact);
 

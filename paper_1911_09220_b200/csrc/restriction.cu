@@ -323,8 +323,8 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
       ctx->launched();
       exclusive_scan(ctx, flag, scan, ndofs);
       int32_t last_scan = 0, last_flag = 0;
-      TFEM_CUDA(cudaMemcpy(&last_scan, scan + ndofs - 1, 4, cudaMemcpyDeviceToHost));
-      TFEM_CUDA(cudaMemcpy(&last_flag, flag + ndofs - 1, 4, cudaMemcpyDeviceToHost));
+      d2h(s, &last_scan, scan + ndofs - 1, 4);
+      d2h(s, &last_flag, flag + ndofs - 1, 4);
       const int64_t n = static_cast<int64_t>(last_scan) + last_flag;
       if (n == 0) continue;
       const int b = r->n_buckets++;
@@ -438,8 +438,8 @@ tfem_restriction *restriction_create(tfem_ctx *ctx, int dim, int p, int64_t ne, 
    const int64_t ne_pad = round_up(ne, 64);
    int32_t *emap = dalloc<int32_t>(ne * nd);
    int *bad = dalloc<int>(1);
-   TFEM_CUDA(cudaMemcpy(emap, elem_dofs, sizeof(int32_t) * ne * nd, cudaMemcpyHostToDevice));
-   TFEM_CUDA(cudaMemset(bad, 0, sizeof(int)));
+   h2d(ctx->stream, emap, elem_dofs, sizeof(int32_t) * ne * nd);
+   TFEM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
    uint32_t *gmap = dalloc<uint32_t>(nd * ne_pad);
    TFEM_CUDA(cudaMemsetAsync(gmap, 0, sizeof(uint32_t) * nd * ne_pad, ctx->stream));
    const Layout L{elem_major_layout(dim, p), nd, ne, ne_pad};
@@ -447,7 +447,7 @@ tfem_restriction *restriction_create(tfem_ctx *ctx, int dim, int p, int64_t ne, 
                                                                          bad);
    ctx->launched();
    int hbad = 0;
-   TFEM_CUDA(cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost));
+   d2h(ctx->stream, &hbad, bad, sizeof(int));
    cudaFree(emap);
    cudaFree(bad);
    if (hbad) {
@@ -472,7 +472,7 @@ void restriction_destroy(tfem_restriction *r)
 void restriction_elem_dofs(const tfem_restriction *r, int32_t *host)
 {
    std::vector<uint32_t> g(static_cast<size_t>(r->nd) * r->ne_pad);
-   TFEM_CUDA(cudaMemcpy(g.data(), r->gmap, sizeof(uint32_t) * g.size(), cudaMemcpyDeviceToHost));
+   d2h(r->ctx->stream, g.data(), r->gmap, sizeof(uint32_t) * g.size());
    const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad};
    for (int64_t e = 0; e < r->ne; e++)
       for (int i = 0; i < r->nd; i++)

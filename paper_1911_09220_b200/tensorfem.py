@@ -67,9 +67,11 @@ def _iptr(a: np.ndarray):
 
 # ----------------------------------------------------------------- device
 class Device:
-    """A CUDA device with one stream (tfem_ctx)."""
+    """A CUDA device with one stream (tfem_ctx).  numerics: "fma" (default;
+    fused multiply-adds, within 1e-15 of the reference) or "reference" (the
+    reference's exact operation order: bit-identical 2D results)."""
 
-    def __init__(self, device: int = 0, numerics: str = "reference"):
+    def __init__(self, device: int = 0, numerics: str = "fma"):
         h = abi.vp()
         check(lib().tfem_ctx_create(device, C.byref(h)))
         self.h = h

@@ -25,14 +25,27 @@ def oracle_built():
     return pyoracle
 
 
-@pytest.fixture(scope="session")
-def dev():
+def _device(numerics):
     """Device 0.  The library import is unconditional: on a GPU box a missing
     libtfem_cuda.so is an error, never a skip."""
     from paper_1911_09220_b200 import CudaError, Device, InvalidArgument
     try:
-        d = Device(0)
+        return Device(0, numerics=numerics)
     except (CudaError, InvalidArgument) as e:  # no device in this container
         pytest.skip(f"no CUDA device: {e}")
+
+
+@pytest.fixture(scope="session")
+def dev():
+    """Bit-exact numerics (the reference's operation order): `==` parity."""
+    d = _device("reference")
+    yield d
+    d.close()
+
+
+@pytest.fixture(scope="session")
+def dev_fma():
+    """The default numerics (fused multiply-adds): 1e-12 parity."""
+    d = _device("fma")
     yield d
     d.close()

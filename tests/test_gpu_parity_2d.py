@@ -285,18 +285,40 @@ def test_multiply_count_and_storage(dev):
         assert a2.stored_reals() == 4 * 3 * nq * nq
 
 
-def test_fma_mode_within_tolerance(dev):
-    """TFEM_NUMERICS_FMA: 1e-12 relative (the north-star bar)."""
-    p = 3
-    rs = RefSpace.cartesian(16, 16, p)
-    f = RefForm(rs, [("diffusion", "varying", 0.0)])
-    d2 = tf.Device(0, numerics="fma")
-    sp = tf.FeSpace.cartesian(d2, (16, 16), p)
-    pa = tf.pa_setup(sp, "diffusion", varying)
-    x = rng_vec(sp.n_dofs, 9)
-    y = tf.Vector(d2, sp.n_dofs)
-    tf.pa_apply_local(pa, sp, tf.Vector.from_numpy(d2, x), y)
+@pytest.mark.parametrize("p", ORDERS)
+@pytest.mark.parametrize("kind", ["diffusion", "mass"])
+def test_fma_numerics_within_tolerance(dev_fma, p, kind):
+    """Default numerics (TFEM_NUMERICS_FMA): operator action and diagonal
+    within the north-star 1e-12 relative of the reference."""
+    rs = RefSpace.cartesian(9, 7, p)
+    f = RefForm(rs, [(kind, "varying", 0.0)])
+    sp = tf.FeSpace.cartesian(dev_fma, (9, 7), p)
+    pa = tf.pa_setup(sp, kind, varying)
+    x = rng_vec(sp.n_dofs, 9 + p)
+    y = tf.Vector(dev_fma, sp.n_dofs)
+    tf.pa_apply_local(pa, sp, tf.Vector.from_numpy(dev_fma, x), y)
     assert rel(y.numpy(), f.mult(x)) <= 1e-12
+    assert rel(tf.pa_diagonal(pa, sp).numpy(), f.diagonal()) <= 1e-12
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("jacobi", [True, False])
+def test_fma_numerics_cg_iterations_match(dev_fma, p, jacobi):
+    """Default numerics: identical CG iteration counts to the reference at
+    tol 1e-12 on the driver's front system."""
+    n = 16
+    rs = RefSpace.cartesian(n, n, p)
+    f = RefForm(rs, [("diffusion", "const", 1.0)])
+    rsys = RefSystem(f, "front")
+    xr, itr, cr, _ = rsys.cg(1e-12, 2000, jacobi)
+    sp = tf.FeSpace.cartesian(dev_fma, (n, n), p)
+    a = tf.BilinearForm(sp)
+    a.add_diffusion(1.0)
+    a.assemble()
+    op = tf.ConstrainedOperator(a, sp.essential_true_dofs())
+    res = tf.cg_solve(op, rsys.rhs, 1e-12, 2000, op.diagonal() if jacobi else None)
+    assert res.converged == cr and res.iterations == itr
+    assert np.abs(res.x.numpy() - xr).max() <= 1e-10 * np.abs(xr).max()
 
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4])
