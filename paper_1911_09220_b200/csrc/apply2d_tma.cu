@@ -2,17 +2,16 @@
 // fed by an asynchronous bulk-copy pipeline (sm_90+ cp.async.bulk + mbarrier;
 // SASS UBLKCP).
 //
-// Persistent blocks of 128 threads walk tiles of 128 consecutive elements.
-// For every tile the qdata is streamed as Q "slices" (one per qy: the nc*Q
-// planes (c, qy, qx), each a contiguous 1 KB run of the [(c*nqd+q)][ne_pad]
-// layout) through a ring of kStages shared-memory stages, and the element
-// map (D1^2 planes of 512 B) through a double buffer one tile ahead.  One
-// elected thread issues the copies; consumers wait on the stage's mbarrier,
-// read their element's factors with conflict-free ld.shared, and a block
-// barrier after each slice frees the stage for the copy kSt slices ahead.
-// The DRAM stream therefore no longer depends on how many loads the
-// 254-register compute threads can keep in flight (the one-thread kernel's
-// limiter: long-scoreboard stalls on each slice's first use).
+// Warp-specialised persistent kernel, one block of 8 warps per SM: warps
+// 0-6 compute (one element per lane, tiles of 224 consecutive elements),
+// warp 7 is the producer.  A tile's qdata is streamed as Q "slices" (one per
+// qy: the nc*Q planes (c, qy, qx), each a contiguous 1792 B run of the
+// [(c*nqd+q)][ne_pad] layout) through a ring of kStages shared-memory
+// stages, and the element map (D1^2 planes) through a double buffer.  The
+// producer waits on a stage's "empty" mbarrier (one arrive per compute warp)
+// before refilling it with cp.async.bulk; compute warps wait on "full" and
+// never on each other (no block barriers -- the per-slice __syncthreads of a
+// single-role design was its top stall; see profiles/).
 //
 // Arithmetic is the same code path as apply2d_reg.cu (EXACT = reference
 // operation order, bit-identical).
@@ -22,8 +21,10 @@ namespace tfem {
 
 namespace {
 
-constexpr int kTile = 128;  // elements per tile = threads per block
-constexpr int kStages = 4;  // qdata slice ring depth
+constexpr int kCompute = 7;                // compute warps per block
+constexpr int kTile = 32 * kCompute;       // elements per tile
+constexpr int kBlock = 32 * (kCompute + 1); // + the producer warp
+constexpr int kStages = 5;                 // qdata slice ring depth
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -54,6 +55,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
                 : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
 {
    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
@@ -63,28 +69,31 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 }
 
 template <int P, int Q, int KIND>
-struct TmaSmem {
+struct TileSmem {
    static constexpr int D1 = P + 1, ND = D1 * D1;
    static constexpr int NC = KIND == TFEM_MASS ? 1 : 3;
    static constexpr int SLICE = NC * Q; // planes per qy slice
    double q[kStages][SLICE][kTile];
    uint32_t gmap[2][ND][kTile];
-   uint64_t full[kStages]; // slice landed (tx count)
-   uint64_t gfull[2];
+   uint64_t full[kStages];  // slice landed (tx count)
+   uint64_t empty[kStages]; // slice consumed (kCompute arrivals)
+   uint64_t gfull[2], gempty[2];
 };
 
 // Issue qdata slice `k` of this block (tile lt = k / Q, qy = k % Q).
 template <int P, int Q, int KIND>
-__device__ __forceinline__ void issue_slice(TmaSmem<P, Q, KIND> &sm, const ApplyArgs &a,
+__device__ __forceinline__ void issue_slice(TileSmem<P, Q, KIND> &sm, const ApplyArgs &a,
                                             int64_t ntiles, int64_t k)
 {
-   constexpr int NQD = Q * Q, SLICE = TmaSmem<P, Q, KIND>::SLICE;
+   constexpr int NQD = Q * Q, SLICE = TileSmem<P, Q, KIND>::SLICE;
    const int64_t lt = k / Q;
    const int qy = static_cast<int>(k % Q);
    const int64_t t = blockIdx.x + lt * gridDim.x;
    if (t >= ntiles) return;
    const int64_t e0 = t * kTile;
-   const unsigned bytes = static_cast<unsigned>(a.ne_pad - e0 < kTile ? a.ne_pad - e0 : kTile) * 8u;
+   // whole 224-element runs except the last tile (ne_pad: multiple of 64)
+   const int64_t avail = a.ne_pad - e0;
+   const unsigned bytes = static_cast<unsigned>(avail < kTile ? avail : kTile) * 8u;
    const int s = static_cast<int>(k % kStages);
    mbar_expect_tx(&sm.full[s], bytes * SLICE);
 #pragma unroll
@@ -96,14 +105,15 @@ __device__ __forceinline__ void issue_slice(TmaSmem<P, Q, KIND> &sm, const Apply
 }
 
 template <int P, int Q, int KIND>
-__device__ __forceinline__ void issue_gmap(TmaSmem<P, Q, KIND> &sm, const ApplyArgs &a,
+__device__ __forceinline__ void issue_gmap(TileSmem<P, Q, KIND> &sm, const ApplyArgs &a,
                                            int64_t ntiles, int64_t lt)
 {
    constexpr int ND = (P + 1) * (P + 1);
    const int64_t t = blockIdx.x + lt * gridDim.x;
    if (t >= ntiles) return;
    const int64_t e0 = t * kTile;
-   const unsigned bytes = static_cast<unsigned>(a.ne_pad - e0 < kTile ? a.ne_pad - e0 : kTile) * 4u;
+   const int64_t avail = a.ne_pad - e0;
+   const unsigned bytes = static_cast<unsigned>(avail < kTile ? avail : kTile) * 4u;
    const int b = static_cast<int>(lt & 1);
    mbar_expect_tx(&sm.gfull[b], bytes * ND);
 #pragma unroll
@@ -183,41 +193,59 @@ __device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const dou
 }
 
 template <int P, int Q, int KIND, bool EXACT>
-__global__ void __launch_bounds__(kTile) apply2d_tma_kernel(const ApplyArgs a)
+__global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs a)
 {
    constexpr int D1 = P + 1, ND = D1 * D1;
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
-   auto &sm = *reinterpret_cast<TmaSmem<P, Q, KIND> *>(smem_raw);
-   const int tid = threadIdx.x;
+   auto &sm = *reinterpret_cast<TileSmem<P, Q, KIND> *>(smem_raw);
+   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+   const int tid = threadIdx.x; // element slot inside the tile (compute warps)
    const int64_t ntiles = (a.ne + kTile - 1) / kTile;
    const int64_t my_tiles =
       blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
    const int64_t n_slices = my_tiles * Q;
-   if (tid == 0) {
-      for (int s = 0; s < kStages; s++) mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.gfull[0], 1);
-      mbar_init(&sm.gfull[1], 1);
+   if (threadIdx.x == 0) {
+      for (int s = 0; s < kStages; s++) {
+         mbar_init(&sm.full[s], 1);
+         mbar_init(&sm.empty[s], kCompute);
+      }
+      for (int b = 0; b < 2; b++) {
+         mbar_init(&sm.gfull[b], 1);
+         mbar_init(&sm.gempty[b], kCompute);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
    }
    __syncthreads();
-   if (tid == 0) {
-      issue_gmap<P, Q, KIND>(sm, a, ntiles, 0);
-      for (int64_t k = 0; k < kStages && k < n_slices; k++) issue_slice<P, Q, KIND>(sm, a, ntiles, k);
-   }
    double dot = 0.0;
+   if (warp == kCompute) {
+      // ---------------------------------------------------------- producer
+      if (lane == 0) {
+         int64_t k = 0;
+         for (int64_t lt = 0; lt < my_tiles; lt++) {
+            const int gb = static_cast<int>(lt & 1);
+            if (lt >= 2) mbar_wait(&sm.gempty[gb], static_cast<unsigned>(((lt >> 1) - 1) & 1));
+            issue_gmap<P, Q, KIND>(sm, a, ntiles, lt);
+            for (int qy = 0; qy < Q; qy++, k++) {
+               const int s = static_cast<int>(k % kStages);
+               if (k >= kStages)
+                  mbar_wait(&sm.empty[s], static_cast<unsigned>((k / kStages - 1) & 1));
+               issue_slice<P, Q, KIND>(sm, a, ntiles, k);
+            }
+         }
+      }
+      __syncwarp();
+   } else {
+   // ---------------------------------------------------------- consumers
    int64_t k = 0; // slice counter
-   // Wait for slice k; after use a block barrier frees its stage and thread 0
-   // refills it with slice k + kStages.  (Per-warp mbarrier releases were
-   // measured slower: the producer warp then trails the slowest warp.)
    auto acquire = [&]() -> const double(*)[kTile] {
       const int s = static_cast<int>(k % kStages);
       mbar_wait(&sm.full[s], static_cast<unsigned>((k / kStages) & 1));
       return sm.q[s];
    };
    auto release = [&]() {
-      __syncthreads();
-      if (tid == 0 && k + kStages < n_slices) issue_slice<P, Q, KIND>(sm, a, ntiles, k + kStages);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[k % kStages]);
       k++;
    };
    for (int64_t lt = 0; lt < my_tiles; lt++) {
@@ -225,9 +253,6 @@ __global__ void __launch_bounds__(kTile) apply2d_tma_kernel(const ApplyArgs a)
       const bool live = e < a.ne;
       const int gb = static_cast<int>(lt & 1);
       mbar_wait(&sm.gfull[gb], static_cast<unsigned>((lt >> 1) & 1));
-      // the other map buffer was last read at the start of tile lt-1, before
-      // that tile's slice barriers: prefetch the next tile's map into it
-      if (tid == 0) issue_gmap<P, Q, KIND>(sm, a, ntiles, lt + 1);
       uint32_t dof[ND];
       double V[D1][D1];
 #pragma unroll
@@ -238,6 +263,8 @@ __global__ void __launch_bounds__(kTile) apply2d_tma_kernel(const ApplyArgs a)
          if (a.mask_in && live && bit_set(a.mask_in, d)) v = 0.0;
          V[i % D1][i / D1] = v;
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.gempty[gb]); // map buffer free again
       double R[D1][D1];
       if (KIND == TFEM_DIFFUSION) {
          double T1[Q][D1], T2[Q][D1];
@@ -302,9 +329,10 @@ __global__ void __launch_bounds__(kTile) apply2d_tma_kernel(const ApplyArgs a)
          }
       }
    }
+   } // consumers
    if (a.dot) {
       const double v[1] = {dot};
-      emit<kTile, 1>(a.dot, v);
+      emit<kBlock, 1>(a.dot, v);
    }
 }
 
@@ -313,16 +341,16 @@ int g_sm_count = 0;
 template <int P, int Q, int KIND, bool EXACT>
 void launch(const ApplyArgs &a, cudaStream_t s, unsigned /*blocks*/)
 {
-   const size_t smem = sizeof(TmaSmem<P, Q, KIND>);
+   const size_t smem = sizeof(TileSmem<P, Q, KIND>);
    static const bool once = [&] {
       cudaFuncSetAttribute(apply2d_tma_kernel<P, Q, KIND, EXACT>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       return true;
    }();
    (void)once;
-   const int64_t ntiles = (a.ne + kTile - 1) / kTile;
-   const unsigned grid = static_cast<unsigned>(ntiles < 2 * (int64_t)g_sm_count ? ntiles : 2 * (int64_t)g_sm_count);
-   apply2d_tma_kernel<P, Q, KIND, EXACT><<<grid, kTile, smem, s>>>(a);
+   const int64_t nblk = (a.ne + kTile - 1) / kTile;
+   const unsigned grid = static_cast<unsigned>(nblk < g_sm_count ? nblk : g_sm_count);
+   apply2d_tma_kernel<P, Q, KIND, EXACT><<<grid, kBlock, smem, s>>>(a);
 }
 
 template <int P, int KIND>
@@ -355,8 +383,8 @@ KernelPick pick_apply2d_tma(int p, int nq, int kind, bool exact, int sm_count)
    k.launch = kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact)
                                 : pick_p<TFEM_DIFFUSION>(p, nq, exact);
    k.elems_per_block = kTile;
-   k.threads = kTile;
-   k.persistent_blocks = 2 * sm_count;
+   k.threads = kBlock;
+   k.persistent_blocks = sm_count;
    return k;
 }
 
