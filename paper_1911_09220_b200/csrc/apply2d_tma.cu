@@ -24,7 +24,14 @@ namespace {
 constexpr int kCompute = 7;                // compute warps per block
 constexpr int kTile = 32 * kCompute;       // elements per tile
 constexpr int kBlock = 32 * (kCompute + 1); // + the producer warp
-constexpr int kStages = 5;                 // qdata slice ring depth
+// Exact numerics prefetch the next tile's x gather into shared memory
+// (LDGSTS, +57 KB) and keep a 4-deep slice ring; FMA numerics gather directly
+// and keep a 5-deep ring (measured: each is the faster choice for its mode).
+template <bool EXACT>
+struct Mode {
+   static constexpr bool prefetch = EXACT;
+   static constexpr int stages = EXACT ? 4 : 5;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -60,6 +67,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// 8-byte asynchronous gather into shared memory (LDGSTS); a lane's pending
+// gathers arrive on an mbarrier when they land.
+__device__ __forceinline__ void gather8(void *dst, const void *src)
+{
+   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
+                : "memory");
+}
+
+__device__ __forceinline__ void gather_arrive(uint64_t *bar)
+{
+   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+                : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
 {
    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
@@ -68,24 +89,27 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                 : "memory");
 }
 
-template <int P, int Q, int KIND>
+template <int P, int Q, int KIND, bool EXACT>
 struct TileSmem {
    static constexpr int D1 = P + 1, ND = D1 * D1;
    static constexpr int NC = KIND == TFEM_MASS ? 1 : 3;
    static constexpr int SLICE = NC * Q; // planes per qy slice
+   static constexpr int kStages = Mode<EXACT>::stages;
    double q[kStages][SLICE][kTile];
    uint32_t gmap[2][ND][kTile];
+   double xg[Mode<EXACT>::prefetch ? 2 : 1][ND][Mode<EXACT>::prefetch ? kTile : 1];
    uint64_t full[kStages];  // slice landed (tx count)
    uint64_t empty[kStages]; // slice consumed (kCompute arrivals)
    uint64_t gfull[2], gempty[2];
+   uint64_t xfull[2];       // a tile's gathers landed (kTile lane arrivals)
 };
 
 // Issue qdata slice `k` of this block (tile lt = k / Q, qy = k % Q).
-template <int P, int Q, int KIND>
-__device__ __forceinline__ void issue_slice(TileSmem<P, Q, KIND> &sm, const ApplyArgs &a,
+template <int P, int Q, int KIND, bool EXACT>
+__device__ __forceinline__ void issue_slice(TileSmem<P, Q, KIND, EXACT> &sm, const ApplyArgs &a,
                                             int64_t ntiles, int64_t k)
 {
-   constexpr int NQD = Q * Q, SLICE = TileSmem<P, Q, KIND>::SLICE;
+   constexpr int NQD = Q * Q, SLICE = TileSmem<P, Q, KIND, EXACT>::SLICE;
    const int64_t lt = k / Q;
    const int qy = static_cast<int>(k % Q);
    const int64_t t = blockIdx.x + lt * gridDim.x;
@@ -94,6 +118,7 @@ __device__ __forceinline__ void issue_slice(TileSmem<P, Q, KIND> &sm, const Appl
    // whole 224-element runs except the last tile (ne_pad: multiple of 64)
    const int64_t avail = a.ne_pad - e0;
    const unsigned bytes = static_cast<unsigned>(avail < kTile ? avail : kTile) * 8u;
+   constexpr int kStages = TileSmem<P, Q, KIND, EXACT>::kStages;
    const int s = static_cast<int>(k % kStages);
    mbar_expect_tx(&sm.full[s], bytes * SLICE);
 #pragma unroll
@@ -104,8 +129,8 @@ __device__ __forceinline__ void issue_slice(TileSmem<P, Q, KIND> &sm, const Appl
    }
 }
 
-template <int P, int Q, int KIND>
-__device__ __forceinline__ void issue_gmap(TileSmem<P, Q, KIND> &sm, const ApplyArgs &a,
+template <int P, int Q, int KIND, bool EXACT>
+__device__ __forceinline__ void issue_gmap(TileSmem<P, Q, KIND, EXACT> &sm, const ApplyArgs &a,
                                            int64_t ntiles, int64_t lt)
 {
    constexpr int ND = (P + 1) * (P + 1);
@@ -196,9 +221,11 @@ template <int P, int Q, int KIND, bool EXACT>
 __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs a)
 {
    constexpr int D1 = P + 1, ND = D1 * D1;
+   constexpr int kStages = TileSmem<P, Q, KIND, EXACT>::kStages;
+   constexpr bool kPrefetch = Mode<EXACT>::prefetch;
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
-   auto &sm = *reinterpret_cast<TileSmem<P, Q, KIND> *>(smem_raw);
+   auto &sm = *reinterpret_cast<TileSmem<P, Q, KIND, EXACT> *>(smem_raw);
    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
    const int tid = threadIdx.x; // element slot inside the tile (compute warps)
    const int64_t ntiles = (a.ne + kTile - 1) / kTile;
@@ -213,6 +240,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       for (int b = 0; b < 2; b++) {
          mbar_init(&sm.gfull[b], 1);
          mbar_init(&sm.gempty[b], kCompute);
+         mbar_init(&sm.xfull[b], kTile);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
    }
@@ -220,17 +248,23 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
    double dot = 0.0;
    if (warp == kCompute) {
       // ---------------------------------------------------------- producer
+      // map(lt + 1) goes out before tile lt's slices: consumers prefetch the
+      // next tile's x gather at the start of tile lt and need it landed
       if (lane == 0) {
          int64_t k = 0;
+         if (my_tiles > 0) issue_gmap<P, Q, KIND, EXACT>(sm, a, ntiles, 0);
          for (int64_t lt = 0; lt < my_tiles; lt++) {
-            const int gb = static_cast<int>(lt & 1);
-            if (lt >= 2) mbar_wait(&sm.gempty[gb], static_cast<unsigned>(((lt >> 1) - 1) & 1));
-            issue_gmap<P, Q, KIND>(sm, a, ntiles, lt);
+            const int64_t nt = lt + 1;
+            if (nt < my_tiles) {
+               if (nt >= 2)
+                  mbar_wait(&sm.gempty[nt & 1], static_cast<unsigned>(((nt >> 1) - 1) & 1));
+               issue_gmap<P, Q, KIND, EXACT>(sm, a, ntiles, nt);
+            }
             for (int qy = 0; qy < Q; qy++, k++) {
                const int s = static_cast<int>(k % kStages);
                if (k >= kStages)
                   mbar_wait(&sm.empty[s], static_cast<unsigned>((k / kStages - 1) & 1));
-               issue_slice<P, Q, KIND>(sm, a, ntiles, k);
+               issue_slice<P, Q, KIND, EXACT>(sm, a, ntiles, k);
             }
          }
       }
@@ -248,23 +282,49 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       if (lane == 0) mbar_arrive(&sm.empty[k % kStages]);
       k++;
    };
+   if (kPrefetch && my_tiles > 0) { // gather of the first tile
+      mbar_wait(&sm.gfull[0], 0u);
+      if (blockIdx.x * (int64_t)kTile + tid < a.ne) {
+#pragma unroll
+         for (int i = 0; i < ND; i++)
+            gather8(&sm.xg[0][i][kPrefetch ? tid : 0], a.x + (sm.gmap[0][i][tid] & kDofMask));
+      }
+      gather_arrive(&sm.xfull[0]);
+   }
    for (int64_t lt = 0; lt < my_tiles; lt++) {
       const int64_t e = (blockIdx.x + lt * gridDim.x) * kTile + tid;
       const bool live = e < a.ne;
       const int gb = static_cast<int>(lt & 1);
-      mbar_wait(&sm.gfull[gb], static_cast<unsigned>((lt >> 1) & 1));
+      // prefetch mode: this tile's gather was issued one tile ahead (or in
+      // the prologue); otherwise gather straight from global memory
+      if (kPrefetch) mbar_wait(&sm.xfull[gb], static_cast<unsigned>((lt >> 1) & 1));
+      else mbar_wait(&sm.gfull[gb], static_cast<unsigned>((lt >> 1) & 1));
       uint32_t dof[ND];
       double V[D1][D1];
 #pragma unroll
       for (int i = 0; i < ND; i++) {
          dof[i] = sm.gmap[gb][i][tid];
          const uint32_t d = dof[i] & kDofMask;
-         double v = live ? __ldg(a.x + d) : 0.0;
+         double v = live ? (kPrefetch ? sm.xg[gb][i][tid] : __ldg(a.x + d)) : 0.0;
          if (a.mask_in && live && bit_set(a.mask_in, d)) v = 0.0;
          V[i % D1][i / D1] = v;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.gempty[gb]); // map buffer free again
+      // Prefetch of the next tile's gather (issued after the x contraction,
+      // when V is dead, to keep register pressure down).
+      auto prefetch_next = [&]() {
+         if (!kPrefetch || lt + 1 >= my_tiles) return;
+         const int nb = gb ^ 1;
+         mbar_wait(&sm.gfull[nb], static_cast<unsigned>(((lt + 1) >> 1) & 1));
+         if ((blockIdx.x + (lt + 1) * gridDim.x) * kTile + tid < a.ne) {
+#pragma unroll 4
+            for (int i = 0; i < ND; i++)
+               gather8(&sm.xg[kPrefetch ? nb : 0][i][kPrefetch ? tid : 0],
+                       a.x + (sm.gmap[nb][i][tid] & kDofMask));
+         }
+         gather_arrive(&sm.xfull[nb]);
+      };
       double R[D1][D1];
       if (KIND == TFEM_DIFFUSION) {
          double T1[Q][D1], T2[Q][D1];
@@ -282,6 +342,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
                T1[qx][b] = s1;
                T2[qx][b] = s2;
             }
+         prefetch_next();
          double vx[D1][D1], vy[D1][D1];
 #pragma unroll
          for (int qy = 0; qy < Q; qy++) { // unrolled: table indices stay immediates
@@ -304,6 +365,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
                for (int kk = 1; kk < D1; kk++) s = mac<EXACT>(s, a.t.B[qx][kk], V[kk][b]);
                T[qx][b] = s;
             }
+         prefetch_next();
 #pragma unroll
          for (int qy = 0; qy < Q; qy++) {
             if (qy == 0) mass_slice<P, Q, EXACT, true>(a, qy, T, acquire(), tid, R);
@@ -341,7 +403,7 @@ int g_sm_count = 0;
 template <int P, int Q, int KIND, bool EXACT>
 void launch(const ApplyArgs &a, cudaStream_t s, unsigned /*blocks*/)
 {
-   const size_t smem = sizeof(TileSmem<P, Q, KIND>);
+   const size_t smem = sizeof(TileSmem<P, Q, KIND, EXACT>);
    static const bool once = [&] {
       cudaFuncSetAttribute(apply2d_tma_kernel<P, Q, KIND, EXACT>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
