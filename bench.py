@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-bitexact", action="store_true", help="skip the reference-numerics line")
     return ap.parse_args()
 
 
@@ -294,7 +295,7 @@ def run_tfem(args):
 
     # ---- the bit-exact numerics (reference operation order), same workload
     exact = None
-    if args.numerics == "fma" and args.dim == 2:
+    if args.numerics == "fma" and args.dim == 2 and not args.no_bitexact:
         dev.set_numerics("reference")
         for _ in range(2):
             step()

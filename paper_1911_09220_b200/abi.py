@@ -9,10 +9,12 @@ fallback: if the shared library is missing, importing fails.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
-SO_PATH = HERE / "libtfem_cuda.so"
+# TFEM_LIB: an out-of-tree variant build (tools/variants.sh), for A/B timing
+SO_PATH = Path(os.environ.get("TFEM_LIB") or HERE / "libtfem_cuda.so")
 
 
 class TfemError(Exception):

@@ -21,16 +21,41 @@ namespace tfem {
 
 namespace {
 
-constexpr int kCompute = 7;                // compute warps per block
+#ifndef TFEM_TMA_WARPS
+#define TFEM_TMA_WARPS 7
+#endif
+constexpr int kCompute = TFEM_TMA_WARPS;   // compute warps per block
 constexpr int kTile = 32 * kCompute;       // elements per tile
 constexpr int kBlock = 32 * (kCompute + 1); // + the producer warp
-// Exact numerics prefetch the next tile's x gather into shared memory
-// (LDGSTS, +57 KB) and keep a 4-deep slice ring; FMA numerics gather directly
-// and keep a 5-deep ring (measured: each is the faster choice for its mode).
+// How a tile's x values reach the compute lanes:
+//   kXSmem   the next tile's gather is issued one tile ahead into shared
+//            memory (LDGSTS, +57 KB); the element map lives in registers
+//   kXReg    the next tile's gather is issued one tile ahead into registers;
+//            the map stays in shared memory until the outputs are written
+//            (triple-buffered so the producer never waits on the open tile)
+//   kXDirect gathered from global memory at the start of the tile
+// Exact numerics keep the reference's two-term order (vx, vy, then R =
+// vx + vy); FMA numerics can accumulate both into R (32 fewer registers).
+// The FMA knobs are build-time defines so variants can be A/B timed
+// (tools/variants.sh); the defaults are the measured best.
+#ifndef TFEM_TMA_FMA_X
+#define TFEM_TMA_FMA_X 0 // 0 kXDirect, 1 kXReg
+#endif
+#ifndef TFEM_TMA_FMA_FUSED
+#define TFEM_TMA_FMA_FUSED 1
+#endif
+#ifndef TFEM_TMA_FMA_STAGES
+#define TFEM_TMA_FMA_STAGES 5
+#endif
+enum XGather { kXDirect, kXReg, kXSmem };
 template <bool EXACT>
 struct Mode {
-   static constexpr bool prefetch = EXACT;
-   static constexpr int stages = EXACT ? 4 : 5;
+   static constexpr int xg = EXACT ? kXSmem : (TFEM_TMA_FMA_X ? kXReg : kXDirect);
+   static constexpr bool prefetch = xg == kXSmem;
+   static constexpr bool map_in_regs = xg != kXReg;
+   static constexpr bool fused = !EXACT && TFEM_TMA_FMA_FUSED;
+   static constexpr int stages = EXACT ? 4 : TFEM_TMA_FMA_STAGES; // qdata slice ring
+   static constexpr int maps = map_in_regs ? 2 : 3;               // element-map buffers
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -96,11 +121,12 @@ struct TileSmem {
    static constexpr int SLICE = NC * Q; // planes per qy slice
    static constexpr int kStages = Mode<EXACT>::stages;
    double q[kStages][SLICE][kTile];
-   uint32_t gmap[2][ND][kTile];
+   static constexpr int kMaps = Mode<EXACT>::maps;
+   uint32_t gmap[kMaps][ND][kTile];
    double xg[Mode<EXACT>::prefetch ? 2 : 1][ND][Mode<EXACT>::prefetch ? kTile : 1];
    uint64_t full[kStages];  // slice landed (tx count)
    uint64_t empty[kStages]; // slice consumed (kCompute arrivals)
-   uint64_t gfull[2], gempty[2];
+   uint64_t gfull[kMaps], gempty[kMaps];
    uint64_t xfull[2];       // a tile's gathers landed (kTile lane arrivals)
 };
 
@@ -139,7 +165,7 @@ __device__ __forceinline__ void issue_gmap(TileSmem<P, Q, KIND, EXACT> &sm, cons
    const int64_t e0 = t * kTile;
    const int64_t avail = a.ne_pad - e0;
    const unsigned bytes = static_cast<unsigned>(avail < kTile ? avail : kTile) * 4u;
-   const int b = static_cast<int>(lt & 1);
+   const int b = static_cast<int>(lt % TileSmem<P, Q, KIND, EXACT>::kMaps);
    mbar_expect_tx(&sm.gfull[b], bytes * ND);
 #pragma unroll
    for (int i = 0; i < ND; i++) bulk_g2s(&sm.gmap[b][i][0], a.gmap + i * a.ne_pad + e0, bytes, &sm.gfull[b]);
@@ -192,6 +218,45 @@ __device__ __forceinline__ void diffusion_slice(const ApplyArgs &a, int qy, cons
    }
 }
 
+// FMA numerics: both terms go straight into R (R += S_x B + S_y G).
+template <int P, int Q, bool FIRST>
+__device__ __forceinline__ void diffusion_slice_fused(const ApplyArgs &a, int qy,
+                                                      const double (&T1)[Q][P + 1],
+                                                      const double (&T2)[Q][P + 1],
+                                                      const double (*qs)[kTile], int tid,
+                                                      double (&R)[P + 1][P + 1])
+{
+   constexpr int D1 = P + 1;
+   double wx[Q], wy[Q];
+#pragma unroll
+   for (int qx = 0; qx < Q; qx++) {
+      double dx = T1[qx][0] * a.t.B[qy][0];
+      double dy = T2[qx][0] * a.t.G[qy][0];
+#pragma unroll
+      for (int b = 1; b < D1; b++) {
+         dx = fma(T1[qx][b], a.t.B[qy][b], dx);
+         dy = fma(T2[qx][b], a.t.G[qy][b], dy);
+      }
+      const double d0 = qs[0 * Q + qx][tid], d1 = qs[1 * Q + qx][tid], d2 = qs[2 * Q + qx][tid];
+      wx[qx] = fma(d0, dx, d1 * dy);
+      wy[qx] = fma(d1, dx, d2 * dy);
+   }
+#pragma unroll
+   for (int i = 0; i < D1; i++) {
+      double sx = a.t.G[0][i] * wx[0];
+      double sy = a.t.B[0][i] * wy[0];
+#pragma unroll
+      for (int qx = 1; qx < Q; qx++) {
+         sx = fma(a.t.G[qx][i], wx[qx], sx);
+         sy = fma(a.t.B[qx][i], wy[qx], sy);
+      }
+#pragma unroll
+      for (int b = 0; b < D1; b++)
+         R[i][b] = FIRST ? fma(sx, a.t.B[qy][b], sy * a.t.G[qy][b])
+                         : fma(sx, a.t.B[qy][b], fma(sy, a.t.G[qy][b], R[i][b]));
+   }
+}
+
 template <int P, int Q, bool EXACT, bool FIRST>
 __device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const double (&T)[Q][P + 1],
                                            const double (*qs)[kTile], int tid,
@@ -217,12 +282,30 @@ __device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const dou
    }
 }
 
+// Gather of the calling lane's element values from the map in `map`
+// (masked essential DOFs read as zero; dead lanes give zeros).
+template <int ND>
+__device__ __forceinline__ void gather_x(const ApplyArgs &a, const uint32_t (*map)[kTile], int tid,
+                                         bool live, double (&X)[ND])
+{
+#pragma unroll
+   for (int i = 0; i < ND; i++) {
+      const uint32_t d = map[i][tid] & kDofMask;
+      double v = live ? __ldg(a.x + d) : 0.0;
+      if (a.mask_in && live && bit_set(a.mask_in, d)) v = 0.0;
+      X[i] = v;
+   }
+}
+
 template <int P, int Q, int KIND, bool EXACT>
 __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs a)
 {
    constexpr int D1 = P + 1, ND = D1 * D1;
    constexpr int kStages = TileSmem<P, Q, KIND, EXACT>::kStages;
+   constexpr int kMaps = TileSmem<P, Q, KIND, EXACT>::kMaps;
    constexpr bool kPrefetch = Mode<EXACT>::prefetch;
+   constexpr bool kRegX = Mode<EXACT>::xg == kXReg;
+   constexpr bool kMapRegs = Mode<EXACT>::map_in_regs;
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
    auto &sm = *reinterpret_cast<TileSmem<P, Q, KIND, EXACT> *>(smem_raw);
@@ -231,33 +314,35 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
    const int64_t ntiles = (a.ne + kTile - 1) / kTile;
    const int64_t my_tiles =
       blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-   const int64_t n_slices = my_tiles * Q;
    if (threadIdx.x == 0) {
       for (int s = 0; s < kStages; s++) {
          mbar_init(&sm.full[s], 1);
          mbar_init(&sm.empty[s], kCompute);
       }
-      for (int b = 0; b < 2; b++) {
+      for (int b = 0; b < kMaps; b++) {
          mbar_init(&sm.gfull[b], 1);
          mbar_init(&sm.gempty[b], kCompute);
-         mbar_init(&sm.xfull[b], kTile);
       }
+      for (int b = 0; b < 2; b++) mbar_init(&sm.xfull[b], kTile);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
    }
    __syncthreads();
+   // map buffer of local tile lt and the parity of its n-th fill
+   auto map_buf = [](int64_t lt) { return static_cast<int>(lt % kMaps); };
+   auto map_par = [](int64_t lt) { return static_cast<unsigned>((lt / kMaps) & 1); };
+   auto tile_elem = [&](int64_t lt) { return (blockIdx.x + lt * gridDim.x) * kTile + tid; };
    double dot = 0.0;
    if (warp == kCompute) {
       // ---------------------------------------------------------- producer
-      // map(lt + 1) goes out before tile lt's slices: consumers prefetch the
-      // next tile's x gather at the start of tile lt and need it landed
+      // map(lt + 1) goes out before tile lt's slices: consumers gather the
+      // next tile's x during tile lt and need it landed
       if (lane == 0) {
          int64_t k = 0;
          if (my_tiles > 0) issue_gmap<P, Q, KIND, EXACT>(sm, a, ntiles, 0);
          for (int64_t lt = 0; lt < my_tiles; lt++) {
             const int64_t nt = lt + 1;
             if (nt < my_tiles) {
-               if (nt >= 2)
-                  mbar_wait(&sm.gempty[nt & 1], static_cast<unsigned>(((nt >> 1) - 1) & 1));
+               if (nt >= kMaps) mbar_wait(&sm.gempty[map_buf(nt)], map_par(nt - kMaps));
                issue_gmap<P, Q, KIND, EXACT>(sm, a, ntiles, nt);
             }
             for (int qy = 0; qy < Q; qy++, k++) {
@@ -282,48 +367,67 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       if (lane == 0) mbar_arrive(&sm.empty[k % kStages]);
       k++;
    };
-   if (kPrefetch && my_tiles > 0) { // gather of the first tile
+   double Xn[ND]; // FMA mode: the next tile's x, gathered one tile ahead
+   if ((kPrefetch || kRegX) && my_tiles > 0) { // gather of the first tile
       mbar_wait(&sm.gfull[0], 0u);
-      if (blockIdx.x * (int64_t)kTile + tid < a.ne) {
+      if constexpr (kPrefetch) {
+         if (tile_elem(0) < a.ne) {
 #pragma unroll
-         for (int i = 0; i < ND; i++)
-            gather8(&sm.xg[0][i][kPrefetch ? tid : 0], a.x + (sm.gmap[0][i][tid] & kDofMask));
+            for (int i = 0; i < ND; i++)
+               gather8(&sm.xg[0][i][kPrefetch ? tid : 0], a.x + (sm.gmap[0][i][tid] & kDofMask));
+         }
+         gather_arrive(&sm.xfull[0]);
+      } else if constexpr (kRegX) {
+         gather_x<ND>(a, sm.gmap[0], tid, tile_elem(0) < a.ne, Xn);
       }
-      gather_arrive(&sm.xfull[0]);
    }
    for (int64_t lt = 0; lt < my_tiles; lt++) {
-      const int64_t e = (blockIdx.x + lt * gridDim.x) * kTile + tid;
+      const int64_t e = tile_elem(lt);
       const bool live = e < a.ne;
-      const int gb = static_cast<int>(lt & 1);
-      // prefetch mode: this tile's gather was issued one tile ahead (or in
-      // the prologue); otherwise gather straight from global memory
-      if (kPrefetch) mbar_wait(&sm.xfull[gb], static_cast<unsigned>((lt >> 1) & 1));
-      else mbar_wait(&sm.gfull[gb], static_cast<unsigned>((lt >> 1) & 1));
-      uint32_t dof[ND];
+      const int gb = map_buf(lt);
+      const int xb = static_cast<int>(lt & 1);
+      uint32_t dof[kMapRegs ? ND : 1];
       double V[D1][D1];
+      if constexpr (kMapRegs) {
+         // kXSmem: this tile's gather was issued one tile ahead (or in the
+         // prologue); kXDirect: gather straight from global memory
+         if (kPrefetch) mbar_wait(&sm.xfull[xb], static_cast<unsigned>((lt >> 1) & 1));
+         else mbar_wait(&sm.gfull[gb], map_par(lt));
 #pragma unroll
-      for (int i = 0; i < ND; i++) {
-         dof[i] = sm.gmap[gb][i][tid];
-         const uint32_t d = dof[i] & kDofMask;
-         double v = live ? (kPrefetch ? sm.xg[gb][i][tid] : __ldg(a.x + d)) : 0.0;
-         if (a.mask_in && live && bit_set(a.mask_in, d)) v = 0.0;
-         V[i % D1][i / D1] = v;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.gempty[gb]); // map buffer free again
-      // Prefetch of the next tile's gather (issued after the x contraction,
-      // when V is dead, to keep register pressure down).
-      auto prefetch_next = [&]() {
-         if (!kPrefetch || lt + 1 >= my_tiles) return;
-         const int nb = gb ^ 1;
-         mbar_wait(&sm.gfull[nb], static_cast<unsigned>(((lt + 1) >> 1) & 1));
-         if ((blockIdx.x + (lt + 1) * gridDim.x) * kTile + tid < a.ne) {
-#pragma unroll 4
-            for (int i = 0; i < ND; i++)
-               gather8(&sm.xg[kPrefetch ? nb : 0][i][kPrefetch ? tid : 0],
-                       a.x + (sm.gmap[nb][i][tid] & kDofMask));
+         for (int i = 0; i < ND; i++) {
+            dof[i] = sm.gmap[gb][i][tid];
+            const uint32_t d = dof[i] & kDofMask;
+            double v = live ? (kPrefetch ? sm.xg[kPrefetch ? xb : 0][i][kPrefetch ? tid : 0]
+                                         : __ldg(a.x + d))
+                            : 0.0;
+            if (a.mask_in && live && bit_set(a.mask_in, d)) v = 0.0;
+            V[i % D1][i / D1] = v;
          }
-         gather_arrive(&sm.xfull[nb]);
+         __syncwarp();
+         if (lane == 0) mbar_arrive(&sm.gempty[gb]); // map buffer free again
+      } else {
+#pragma unroll
+         for (int i = 0; i < ND; i++) V[i % D1][i / D1] = Xn[i];
+      }
+      // Gather of the next tile (issued after the x contraction, when V is
+      // dead, to keep register pressure down).
+      auto prefetch_next = [&]() {
+         if (!kPrefetch && !kRegX) return;
+         if (lt + 1 >= my_tiles) return;
+         const int nb = map_buf(lt + 1);
+         mbar_wait(&sm.gfull[nb], map_par(lt + 1));
+         const bool nlive = tile_elem(lt + 1) < a.ne;
+         if constexpr (kPrefetch) {
+            if (nlive) {
+#pragma unroll 4
+               for (int i = 0; i < ND; i++)
+                  gather8(&sm.xg[xb ^ 1][i][kPrefetch ? tid : 0],
+                          a.x + (sm.gmap[nb][i][tid] & kDofMask));
+            }
+            gather_arrive(&sm.xfull[xb ^ 1]);
+         } else if constexpr (kRegX) {
+            gather_x<ND>(a, sm.gmap[nb], tid, nlive, Xn);
+         }
       };
       double R[D1][D1];
       if (KIND == TFEM_DIFFUSION) {
@@ -343,17 +447,26 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
                T2[qx][b] = s2;
             }
          prefetch_next();
-         double vx[D1][D1], vy[D1][D1];
+         if constexpr (!Mode<EXACT>::fused) {
+            double vx[D1][D1], vy[D1][D1];
 #pragma unroll
-         for (int qy = 0; qy < Q; qy++) { // unrolled: table indices stay immediates
-            if (qy == 0) diffusion_slice<P, Q, EXACT, true>(a, qy, T1, T2, acquire(), tid, vx, vy);
-            else diffusion_slice<P, Q, EXACT, false>(a, qy, T1, T2, acquire(), tid, vx, vy);
-            release();
+            for (int qy = 0; qy < Q; qy++) { // unrolled: table indices stay immediates
+               if (qy == 0) diffusion_slice<P, Q, EXACT, true>(a, qy, T1, T2, acquire(), tid, vx, vy);
+               else diffusion_slice<P, Q, EXACT, false>(a, qy, T1, T2, acquire(), tid, vx, vy);
+               release();
+            }
+#pragma unroll
+            for (int i = 0; i < D1; i++)
+#pragma unroll
+               for (int b = 0; b < D1; b++) R[i][b] = add<EXACT>(vx[i][b], vy[i][b]);
+         } else {
+#pragma unroll
+            for (int qy = 0; qy < Q; qy++) {
+               if (qy == 0) diffusion_slice_fused<P, Q, true>(a, qy, T1, T2, acquire(), tid, R);
+               else diffusion_slice_fused<P, Q, false>(a, qy, T1, T2, acquire(), tid, R);
+               release();
+            }
          }
-#pragma unroll
-         for (int i = 0; i < D1; i++)
-#pragma unroll
-            for (int b = 0; b < D1; b++) R[i][b] = add<EXACT>(vx[i][b], vy[i][b]);
       } else {
          double T[Q][D1];
 #pragma unroll
@@ -376,7 +489,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       if (live) {
 #pragma unroll
          for (int i = 0; i < ND; i++) {
-            const uint32_t g = dof[i];
+            const uint32_t g = kMapRegs ? dof[kMapRegs ? i : 0] : sm.gmap[gb][i][tid];
             double r = R[i % D1][i / D1];
             if (g & kExclusive) {
                const uint32_t d = g & kDofMask;
@@ -389,6 +502,10 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
                a.evec[i * a.ne_pad + e] = r;
             }
          }
+      }
+      if constexpr (!kMapRegs) {
+         __syncwarp();
+         if (lane == 0) mbar_arrive(&sm.gempty[gb]); // map buffer free again
       }
    }
    } // consumers

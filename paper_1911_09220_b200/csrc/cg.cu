@@ -1,14 +1,15 @@
 // K5 / K6: operators and the device-resident Jacobi-PCG of cg_solve
 // (solvers.cpp:11-97).
 //
-// Per iteration (all on the device, batches of iterations replayed as one
-// CUDA graph, only a 4-byte stop flag read back per batch):
-//   1. q = A p            element kernel + shared-DOF scatter, fused p.q partials
-//   2. alpha kernel       1 block: pq = sum(partials), alpha = rz / pq
-//   3. update kernel      x' = x + alpha p, r -= alpha q, z = r / d,
-//                         partials of r.r and r.z
-//   4. beta kernel        1 block: ||r||, best-iterate bookkeeping, beta, stop test
-//   5. direction kernel   p = r / d + beta p
+// Per iteration (all on the device, batches of 16 iterations replayed as one
+// CUDA graph, only the CG state read back per batch), four launches:
+//   1-2. q = A p          element kernel + shared-DOF scatter, fused p.q
+//                         partials; the last block to finish folds them and
+//                         takes alpha = rz / pq (emit, common.cuh)
+//   3.   update kernel    x' = x + alpha p, r -= alpha q, z = r / d, partials
+//                         of r.r and r.z; its last block takes ||r||, the
+//                         best-iterate bookkeeping, beta and the stop test
+//   4.   direction kernel p = r / d + beta p
 // Vector updates use unfused multiply + add in the reference's order
 // (vector.cpp:20-23, solvers.cpp:84-87), so only the dot products differ from
 // the CPU (tree vs sequential sum).  The best iterate (solvers.cpp:78-81) costs
@@ -112,19 +113,6 @@ csr_kernel(const int32_t *rowptr, const int32_t *cols, const double *vals, int64
 }
 
 // ----------------------------------------------------------------- CG
-struct CgState {
-   double rz, alpha, beta, rnorm, best_rnorm, target;
-   int it, max_iters, done, converged, iterations, status;
-   int cur, best;
-};
-
-__device__ __forceinline__ int next_buffer(int cur, int best)
-{
-   for (int k = 0; k < 3; k++)
-      if (k != cur && k != best) return k;
-   return 0;
-}
-
 // r = b, z = M r, p = z, x0 = 0; partials of r.r and r.z (solvers.cpp:43-58)
 __global__ void __launch_bounds__(kVecThreads)
 cg_init_kernel(const double *__restrict__ b, const double *__restrict__ diag, int64_t n,
@@ -166,63 +154,12 @@ __device__ void init_step(CgState *st, double rr, double rz)
    }
 }
 
-__device__ void alpha_step(CgState *st, double pq)
-{
-   const double alpha = st->rz / pq;
-   st->alpha = alpha;
-   if (!isfinite(alpha)) { // solvers.cpp:69-71
-      st->status = 1;
-      st->done = 1;
-   }
-}
-
-__device__ void beta_step(CgState *st, double rr, double rz_next)
-{
-   const double rnorm = sqrt(rr);
-   st->rnorm = rnorm;
-   if (!isfinite(rnorm)) { // solvers.cpp:74-77
-      st->status = 2;
-      st->done = 1;
-      return;
-   }
-   st->it += 1;
-   const int nxt = next_buffer(st->cur, st->best);
-   st->cur = nxt;
-   if (rnorm < st->best_rnorm) { // solvers.cpp:78-81
-      st->best_rnorm = rnorm;
-      st->best = nxt;
-   }
-   st->beta = rz_next / st->rz;
-   st->rz = rz_next;
-   if (rnorm <= st->target) { // checked at the top of the next iteration
-      st->done = 1;
-      st->converged = 1;
-      st->iterations = st->it;
-   } else if (st->it >= st->max_iters) {
-      st->done = 1;
-      st->converged = 0;
-      st->iterations = st->max_iters;
-   }
-}
-
 __global__ void __launch_bounds__(kVecThreads)
 cg_init_finish_kernel(const double *chunks, int64_t nch, CgState *st)
 {
    const double rr = fold(chunks, nch);
    const double rz = fold(chunks + nch, nch);
    if (threadIdx.x == 0) init_step(st, rr, rz);
-}
-
-// pq = (element-kernel chunks) + (scatter chunks) in a fixed order.
-__global__ void __launch_bounds__(kVecThreads)
-cg_alpha_kernel(const double *ch_a, int64_t na, const double *ch_b, int64_t nb, CgState *st)
-{
-   if (st->done) return;
-   double s = 0.0;
-   for (int64_t i = threadIdx.x; i < na + nb; i += blockDim.x)
-      s += __ldcg(i < na ? ch_a + i : ch_b + (i - na));
-   const double pq = block_sum<kVecThreads>(s);
-   if (threadIdx.x == 0) alpha_step(st, pq);
 }
 
 // Distributed variants: the rank-local fold lands in red[] (device), the
@@ -309,15 +246,6 @@ cg_update_kernel(const CgState *st, XBufs xb, const double *__restrict__ p,
    emit<kVecThreads, 2>(sink, v);
 }
 
-__global__ void __launch_bounds__(kVecThreads)
-cg_beta_kernel(const double *chunks, int64_t nch, CgState *st)
-{
-   if (st->done) return;
-   const double rr = fold(chunks, nch);
-   const double rz_next = fold(chunks + nch, nch);
-   if (threadIdx.x == 0) beta_step(st, rr, rz_next);
-}
-
 // p = z + beta p with z = r / d (solvers.cpp:84-87)
 __global__ void __launch_bounds__(kVecThreads)
 cg_direction_kernel(const CgState *st, const double *__restrict__ r,
@@ -373,8 +301,8 @@ struct SinkStore {
       nch = n_chunks(g);
       s.partials = dalloc<double>(nv * g);
       s.chunks = dalloc<double>(nv * nch);
-      s.tickets = dalloc<unsigned>(nch);
-      TFEM_CUDA(cudaMemsetAsync(s.tickets, 0, sizeof(unsigned) * nch, stream));
+      s.tickets = dalloc<unsigned>(nch + 1);
+      TFEM_CUDA(cudaMemsetAsync(s.tickets, 0, sizeof(unsigned) * (nch + 1), stream));
    }
    void release()
    {
@@ -453,17 +381,24 @@ void enqueue_iteration(tfem_ctx *ctx, const tfem_operator *op, Workspace &w, XBu
                        const double *diag)
 {
    const int64_t n = op->n;
-   operator_mult(ctx, op, w.p, w.q, &w.s_elem.s, w.s_scatter.grid ? &w.s_scatter.s : nullptr,
-                 &w.st->done);
-   cg_alpha_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_elem.s.chunks, w.s_elem.nch,
-                                                       w.s_scatter.s.chunks, w.s_scatter.nch,
-                                                       w.st);
+   // alpha is taken by the last block of the operator's final launch, beta by
+   // the last block of the update: four launches per iteration.
+   DotSink se = w.s_elem.s, ss = w.s_scatter.s, sv = w.s_vec.s;
+   DotSink &fin = w.s_scatter.grid ? ss : se;
+   if (w.s_scatter.grid) {
+      ss.pre = w.s_elem.s.chunks;
+      ss.n_pre = w.s_elem.nch;
+   }
+   fin.state = w.st;
+   fin.finish = kFinishAlpha;
+   sv.state = w.st;
+   sv.finish = kFinishBeta;
+   operator_mult(ctx, op, w.p, w.q, &se, w.s_scatter.grid ? &ss : nullptr, &w.st->done);
    const unsigned vb = vec_blocks(ctx, n);
-   cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.p, w.q, w.r, diag, n,
-                                                         w.s_vec.s, nullptr);
-   cg_beta_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, w.st);
+   cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.p, w.q, w.r, diag, n, sv,
+                                                         nullptr);
    cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.r, diag, w.p, n);
-   ctx->launched(4);
+   ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
 }
 
@@ -805,7 +740,7 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
    } else {
       // Batches of iterations as one graph; the batch length keeps the
       // per-batch host round trip small against the work it covers.
-      const int batch = n >= (1 << 22) ? 4 : 16;
+      const int batch = 16;
       if (!w.graph || w.g_diag != diag || w.g_x != x || w.g_batch != batch ||
           w.g_numerics != ctx->numerics) {
          if (w.graph) {

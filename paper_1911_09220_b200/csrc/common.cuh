@@ -169,10 +169,27 @@ namespace tfem {
 
 constexpr int kChunk = 32;
 
+// Device-resident CG scalars (solvers.cpp:43-96), advanced by the last block
+// of the kernels whose dot products they need (see emit).
+struct CgState {
+   double rz, alpha, beta, rnorm, best_rnorm, target;
+   int it, max_iters, done, converged, iterations, status;
+   int cur, best;
+};
+
+enum SinkFinish : int { kFinishNone = 0, kFinishAlpha = 1, kFinishBeta = 2 };
+
 struct DotSink {
    double *partials = nullptr;   // [nv][grid]
    double *chunks = nullptr;     // [nv][n_chunks]
-   unsigned *tickets = nullptr;  // [n_chunks], zero between launches
+   unsigned *tickets = nullptr;  // [n_chunks + 1], zero between launches
+   // Optional finish: the last chunk to complete folds `pre` (chunk sums of
+   // an earlier kernel, e.g. the element kernel's share of p.q) and this
+   // launch's chunks in a fixed order and advances the CG state.
+   const double *pre = nullptr;  // [nv][n_pre]
+   int64_t n_pre = 0;
+   CgState *state = nullptr;
+   int finish = kFinishNone;
    __host__ __device__ explicit operator bool() const { return partials != nullptr; }
 };
 
@@ -269,6 +286,52 @@ __device__ __forceinline__ double block_sum(double v)
    return s;
 }
 
+__device__ __forceinline__ int next_buffer(int cur, int best)
+{
+   for (int k = 0; k < 3; k++)
+      if (k != cur && k != best) return k;
+   return 0;
+}
+
+__device__ inline void alpha_step(CgState *st, double pq)
+{
+   const double alpha = st->rz / pq;
+   st->alpha = alpha;
+   if (!isfinite(alpha)) { // solvers.cpp:69-71
+      st->status = 1;
+      st->done = 1;
+   }
+}
+
+__device__ inline void beta_step(CgState *st, double rr, double rz_next)
+{
+   const double rnorm = sqrt(rr);
+   st->rnorm = rnorm;
+   if (!isfinite(rnorm)) { // solvers.cpp:74-77
+      st->status = 2;
+      st->done = 1;
+      return;
+   }
+   st->it += 1;
+   const int nxt = next_buffer(st->cur, st->best);
+   st->cur = nxt;
+   if (rnorm < st->best_rnorm) { // solvers.cpp:78-81
+      st->best_rnorm = rnorm;
+      st->best = nxt;
+   }
+   st->beta = rz_next / st->rz;
+   st->rz = rz_next;
+   if (rnorm <= st->target) { // checked at the top of the next iteration
+      st->done = 1;
+      st->converged = 1;
+      st->iterations = st->it;
+   } else if (st->it >= st->max_iters) {
+      st->done = 1;
+      st->converged = 0;
+      st->iterations = st->max_iters;
+   }
+}
+
 // Deterministic two-level reduction of per-block values.  Every block writes
 // its block sums to partials[k][blockIdx]; the last block to finish in each
 // chunk of kChunk consecutive blocks (atomic ticket) folds the chunk's
@@ -291,10 +354,12 @@ __device__ __forceinline__ void emit(const DotSink &s, const double (&v)[NV])
       is_last = atomicAdd(s.tickets + chunk, 1u) == nb - 1;
    }
    __syncthreads();
-   if (is_last && threadIdx.x == 0) {
+   if (!is_last) return; // block-uniform
+   __shared__ int is_final;
+   const int64_t nch = n_chunks(G);
+   if (threadIdx.x == 0) {
       __threadfence();
       const unsigned nb = min((unsigned)kChunk, G - chunk * kChunk);
-      const int64_t nch = n_chunks(G);
 #pragma unroll
       for (int k = 0; k < NV; k++) {
          double a = 0.0;
@@ -302,6 +367,27 @@ __device__ __forceinline__ void emit(const DotSink &s, const double (&v)[NV])
          s.chunks[k * nch + chunk] = a;
       }
       s.tickets[chunk] = 0u;
+      is_final = 0;
+      if (s.finish != kFinishNone) {
+         __threadfence();
+         is_final = atomicAdd(s.tickets + nch, 1u) == nch - 1;
+      }
+   }
+   __syncthreads();
+   if (!is_final) return;
+   __threadfence();
+   double f[NV];
+#pragma unroll
+   for (int k = 0; k < NV; k++) {
+      double a = 0.0;
+      for (int64_t i = threadIdx.x; i < s.n_pre + nch; i += NT)
+         a += __ldcg(i < s.n_pre ? s.pre + k * s.n_pre + i : s.chunks + k * nch + (i - s.n_pre));
+      f[k] = block_sum<NT>(a);
+   }
+   if (threadIdx.x == 0) {
+      s.tickets[nch] = 0u;
+      if (s.finish == kFinishAlpha) alpha_step(s.state, f[0]);
+      else beta_step(s.state, f[0], f[NV - 1]);
    }
 }
 
