@@ -60,7 +60,7 @@ __device__ __forceinline__ double scatter_row(const BucketArgs &B, int b, int64_
                                               const double *__restrict__ evec,
                                               const double *__restrict__ x, double *y,
                                               int overwrite, const uint32_t *ess_out, bool want_dot,
-                                              const uint32_t *notown)
+                                              const uint32_t *notown, bool ess_only)
 {
    const int32_t d = __ldg(B.dofs[b] + s);
    uint32_t sl[C];
@@ -71,8 +71,12 @@ __device__ __forceinline__ double scatter_row(const BucketArgs &B, int b, int64_
    double acc = overwrite ? v[0] : add<EXACT>(y[d], v[0]);
 #pragma unroll
    for (int k = 1; k < C; k++) acc = add<EXACT>(acc, v[k]);
-   if (ess_out && bit_set(ess_out, d)) acc = __ldg(x + d);
+   const bool es = ess_out && bit_set(ess_out, d);
+   if (es) acc = __ldg(x + d);
    y[d] = acc;
+   // ess_only: the element kernel took x . y as element energies; only the
+   // essential DOFs' x_d^2 is missing
+   if (ess_only) return want_dot && es ? mul<EXACT>(acc, acc) : 0.0;
    return want_dot && !(notown && bit_set(notown, d)) ? mul<EXACT>(__ldg(x + d), acc) : 0.0;
 }
 
@@ -80,7 +84,7 @@ template <bool EXACT>
 __global__ void __launch_bounds__(kScatterThreads)
 scatter_kernel(const BucketArgs B, const double *__restrict__ evec, const double *__restrict__ x,
                double *y, int overwrite, const uint32_t *ess_out, DotSink dot, const int *done,
-               const uint32_t *notown)
+               const uint32_t *notown, int ess_only)
 {
    if (done && *done) return;
    int b = 0;
@@ -88,15 +92,15 @@ scatter_kernel(const BucketArgs B, const double *__restrict__ evec, const double
    const int64_t s = ((int64_t)blockIdx.x - B.start[b]) * kScatterThreads + threadIdx.x;
    double dv = 0.0;
    if (s < B.n[b]) {
-      const bool wd = static_cast<bool>(dot);
+      const bool wd = static_cast<bool>(dot), eo = ess_only != 0;
       switch (B.c[b]) {
-      case 2: dv = scatter_row<EXACT, 2>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
-      case 3: dv = scatter_row<EXACT, 3>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
-      case 4: dv = scatter_row<EXACT, 4>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
-      case 5: dv = scatter_row<EXACT, 5>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
-      case 6: dv = scatter_row<EXACT, 6>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
-      case 7: dv = scatter_row<EXACT, 7>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
-      case 8: dv = scatter_row<EXACT, 8>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown); break;
+      case 2: dv = scatter_row<EXACT, 2>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 3: dv = scatter_row<EXACT, 3>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 4: dv = scatter_row<EXACT, 4>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 5: dv = scatter_row<EXACT, 5>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 6: dv = scatter_row<EXACT, 6>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 7: dv = scatter_row<EXACT, 7>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 8: dv = scatter_row<EXACT, 8>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
       }
    }
    if (dot) {
@@ -105,20 +109,22 @@ scatter_kernel(const BucketArgs B, const double *__restrict__ evec, const double
    }
 }
 
-BucketArgs bucket_args(const tfem_restriction *r)
+BucketArgs bucket_args(const tfem_restriction *r, bool global_only)
 {
+   const int nb = global_only ? r->n_gbuckets : r->n_buckets;
+   const tfem_restriction::Bucket *bk = global_only ? r->gbuckets : r->buckets;
    BucketArgs B{};
-   B.nb = r->n_buckets;
+   B.nb = nb;
    int64_t blk = 0;
-   for (int b = 0; b < r->n_buckets; b++) {
-      B.c[b] = r->buckets[b].c;
-      B.n[b] = r->buckets[b].n;
-      B.dofs[b] = r->buckets[b].dofs;
-      B.slots[b] = r->buckets[b].slots;
+   for (int b = 0; b < nb; b++) {
+      B.c[b] = bk[b].c;
+      B.n[b] = bk[b].n;
+      B.dofs[b] = bk[b].dofs;
+      B.slots[b] = bk[b].slots;
       B.start[b] = blk;
-      blk += blocks_for(r->buckets[b].n, kScatterThreads);
+      blk += blocks_for(bk[b].n, kScatterThreads);
    }
-   B.start[r->n_buckets] = blk;
+   B.start[nb] = blk;
    return B;
 }
 
@@ -132,7 +138,7 @@ __global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne,
                             const double *__restrict__ qdata, const uint32_t *gmap,
                             int elem_major, double *evec, double *y)
 {
-   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; // position
    const int i = blockIdx.y;
    if (e >= ne) return;
    const int D1 = p + 1;
@@ -183,7 +189,7 @@ __global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne,
    }
    const int64_t slot = elem_major ? e * nd + i : (int64_t)i * ne_pad + e;
    const uint32_t g = gmap[slot];
-   if (g & kExclusive) {
+   if (is_exclusive(g)) {
       const uint32_t d = g & kDofMask;
       y[d] = __dadd_rn(y[d], s);
    } else {
@@ -230,80 +236,111 @@ unsigned elem_blocks(const KernelPick &k, int64_t ne)
 
 } // namespace
 
-int64_t scatter_grid(const tfem_restriction *r) { return bucket_args(r).start[r->n_buckets]; }
+int64_t scatter_grid(const tfem_restriction *r, bool global_only)
+{
+   const BucketArgs B = bucket_args(r, global_only);
+   return B.start[B.nb];
+}
 
 int64_t scatter_shared(tfem_ctx *ctx, const tfem_restriction *r, const double *evec,
                        const double *x, double *y, bool overwrite, const uint32_t *ess_out,
                        const DotSink *dot, const int *done, bool exact,
-                       const uint32_t *notown)
+                       const uint32_t *notown, bool global_only, bool ess_only)
 {
-   const BucketArgs B = bucket_args(r);
-   const int64_t grid = B.start[r->n_buckets];
+   const BucketArgs B = bucket_args(r, global_only);
+   const int64_t grid = B.start[B.nb];
    if (grid == 0) return 0;
    const DotSink sink = dot ? *dot : DotSink{};
    if (exact)
       scatter_kernel<true><<<(unsigned)grid, kScatterThreads, 0, ctx->stream>>>(
-         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done, notown);
+         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done, notown, ess_only ? 1 : 0);
    else
       scatter_kernel<false><<<(unsigned)grid, kScatterThreads, 0, ctx->stream>>>(
-         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done, notown);
+         B, evec, x, y, overwrite ? 1 : 0, ess_out, sink, done, notown, ess_only ? 1 : 0);
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
    return grid;
 }
 
+// The tile kernel sums tile-local DOFs itself when the space has records.
+// A/B switches (TFEM_WARP_LOCAL, TFEM_EDOT = 0 disables; default on).
+bool env_on(const char *name)
+{
+   const char *v = std::getenv(name);
+   return !(v && std::string(v) == "0");
+}
+bool tiled(const KernelPick &k, const tfem_restriction *r)
+{
+   static const bool on = env_on("TFEM_WARP_LOCAL");
+   return on && k.warp_reduce && r->warp_local;
+}
+
+void check_pair(const tfem_pa *pa, const tfem_restriction *r)
+{
+   if (pa->dim != r->dim || pa->p != r->p || pa->ne != r->ne)
+      invalid("forms: point factors were built for a different space");
+   if (!(pa->order == r->order))
+      invalid("forms: point factors and restriction use different element orders (a Cartesian "
+              "restriction needs a Cartesian geometry and vice versa)");
+}
+
 void pa_apply_grids(const tfem_pa *pa, const tfem_restriction *r, int64_t *g_elem,
                     int64_t *g_scatter)
 {
-   *g_elem = elem_blocks(pick(pa->ctx, pa), pa->ne);
-   *g_scatter = scatter_grid(r);
+   const KernelPick k = pick(pa->ctx, pa);
+   *g_elem = elem_blocks(k, pa->npos);
+   *g_scatter = scatter_grid(r, tiled(k, r));
 }
 
 void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const double *x,
               double *y, const ApplyFlags &f)
 {
-   if (pa->dim != r->dim || pa->p != r->p || pa->ne != r->ne)
-      invalid("forms: point factors were built for a different space");
+   check_pair(pa, r);
    const bool exact = pa->dim == 2 && ctx->numerics == TFEM_NUMERICS_REFERENCE;
    const KernelPick k = pick(ctx, pa);
+   const bool tl = tiled(k, r);
    ApplyArgs a{};
    a.t = tables_of(pa);
-   a.ne = pa->ne;
+   a.ne = pa->npos; // element kernels run over positions (padding included)
    a.ne_pad = pa->ne_pad;
    a.nd = r->nd;
    a.gmap = r->gmap;
    a.qdata = pa->qdata;
    a.x = x;
    a.y = y;
-   a.evec = r->n_shared > 0 ? const_cast<tfem_restriction *>(r)->ensure_evec() : nullptr;
+   a.evec = r->needs_evec() ? const_cast<tfem_restriction *>(r)->ensure_evec() : nullptr;
    a.overwrite = f.overwrite ? 1 : 0;
    a.mask_in = f.mask_in;
    a.ess_out = f.ess_out;
    a.notown = f.notown;
+   a.warp_local = tl ? 1 : 0;
+   static const bool edot_on = env_on("TFEM_EDOT");
+   const bool edot = edot_on && k.energy_dot && static_cast<bool>(f.dot) && f.overwrite &&
+                     f.mask_in == f.ess_out && !f.notown;
+   a.energy_dot = edot ? 1 : 0;
    a.dot = f.dot;
    a.done = f.done;
-   k.launch(a, ctx->stream, elem_blocks(k, pa->ne));
+   k.launch(a, ctx->stream, elem_blocks(k, pa->npos));
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
    if (r->n_shared > 0)
       scatter_shared(ctx, r, a.evec, x, y, f.overwrite, f.ess_out,
-                     f.dot_scatter ? &f.dot_scatter : nullptr, f.done, exact, f.notown);
+                     f.dot_scatter ? &f.dot_scatter : nullptr, f.done, exact, f.notown, tl, edot);
 }
 
 void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, double *diag)
 {
-   if (pa->dim != r->dim || pa->p != r->p || pa->ne != r->ne)
-      invalid("forms: point factors were built for a different space");
+   check_pair(pa, r);
    const Tables t = tables_of(pa);
-   double *evec = r->n_shared > 0 ? const_cast<tfem_restriction *>(r)->ensure_evec() : nullptr;
+   double *evec = r->needs_evec() ? const_cast<tfem_restriction *>(r)->ensure_evec() : nullptr;
    const int T = 128;
-   dim3 grid(blocks_for(pa->ne, T), r->nd);
+   dim3 grid(blocks_for(pa->npos, T), r->nd);
    const int elem_major = pa->elem_major() ? 1 : 0;
    if (pa->dim == 2)
-      diag_kernel<2><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->ne, pa->ne_pad,
+      diag_kernel<2><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->npos, pa->ne_pad,
                                                  pa->qdata, r->gmap, elem_major, evec, diag);
    else
-      diag_kernel<3><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->ne, pa->ne_pad,
+      diag_kernel<3><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->npos, pa->ne_pad,
                                                  pa->qdata, r->gmap, elem_major, evec, diag);
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());

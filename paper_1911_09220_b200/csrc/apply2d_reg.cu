@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kElemThreads2D) apply2d_kernel(const ApplyArgs
       for (int i = 0; i < ND; i++) {
          const uint32_t g = dof[i];
          double r = R[i % D1][i / D1];
-         if (g & kExclusive) {
+         if (is_exclusive(g)) {
             const uint32_t d = g & kDofMask;
             if (!a.overwrite) r = add<EXACT>(a.y[d], r);
             if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);

@@ -26,36 +26,35 @@ namespace {
 #endif
 constexpr int kCompute = TFEM_TMA_WARPS;   // compute warps per block
 constexpr int kTile = 32 * kCompute;       // elements per tile
+static_assert(kTile == kTmaTile, "tile records are built for kTmaTile-element tiles");
 constexpr int kBlock = 32 * (kCompute + 1); // + the producer warp
-// How a tile's x values reach the compute lanes:
-//   kXSmem   the next tile's gather is issued one tile ahead into shared
-//            memory (LDGSTS, +57 KB); the element map lives in registers
-//   kXReg    the next tile's gather is issued one tile ahead into registers;
-//            the map stays in shared memory until the outputs are written
-//            (triple-buffered so the producer never waits on the open tile)
-//   kXDirect gathered from global memory at the start of the tile
-// Exact numerics keep the reference's two-term order (vx, vy, then R =
-// vx + vy); FMA numerics can accumulate both into R (32 fewer registers).
-// The FMA knobs are build-time defines so variants can be A/B timed
-// (tools/variants.sh); the defaults are the measured best.
-#ifndef TFEM_TMA_FMA_X
-#define TFEM_TMA_FMA_X 0 // 0 kXDirect, 1 kXReg
-#endif
+// x of a tile: exact numerics gather it one tile ahead into shared memory
+// (LDGSTS) and keep a 4-deep slice ring; FMA numerics gather straight from
+// global memory at the start of the tile (stashing the values in shared
+// memory for the epilogue), accumulate both gradient terms into one register
+// block (32 fewer registers) and keep a 5-deep ring -- each the measured best
+// for its mode.  The FMA knobs are build-time defines so variants can be A/B
+// timed (tools/variants.sh).
 #ifndef TFEM_TMA_FMA_FUSED
 #define TFEM_TMA_FMA_FUSED 1
 #endif
 #ifndef TFEM_TMA_FMA_STAGES
 #define TFEM_TMA_FMA_STAGES 5
 #endif
-enum XGather { kXDirect, kXReg, kXSmem };
+#ifndef TFEM_TMA_GATHER1
+#define TFEM_TMA_GATHER1 1
+#endif
+#ifndef TFEM_TMA_SHFL_GUARD
+#define TFEM_TMA_SHFL_GUARD 0
+#endif
+#ifndef TFEM_TMA_FMA_PREFETCH
+#define TFEM_TMA_FMA_PREFETCH 1
+#endif
 template <bool EXACT>
 struct Mode {
-   static constexpr int xg = EXACT ? kXSmem : (TFEM_TMA_FMA_X ? kXReg : kXDirect);
-   static constexpr bool prefetch = xg == kXSmem;
-   static constexpr bool map_in_regs = xg != kXReg;
+   static constexpr bool prefetch = EXACT || TFEM_TMA_FMA_PREFETCH;
    static constexpr bool fused = !EXACT && TFEM_TMA_FMA_FUSED;
-   static constexpr int stages = EXACT ? 4 : TFEM_TMA_FMA_STAGES; // qdata slice ring
-   static constexpr int maps = map_in_regs ? 2 : 3;               // element-map buffers
+   static constexpr int stages = prefetch ? 4 : TFEM_TMA_FMA_STAGES; // qdata slice ring
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -120,10 +119,13 @@ struct TileSmem {
    static constexpr int NC = KIND == TFEM_MASS ? 1 : 3;
    static constexpr int SLICE = NC * Q; // planes per qy slice
    static constexpr int kStages = Mode<EXACT>::stages;
+   static constexpr int kMaps = 3; // the open tile's map stays until its epilogue
+   static constexpr int kXBufs = Mode<EXACT>::prefetch ? 2 : 1;
+   static constexpr int kXND = Mode<EXACT>::prefetch ? ND : 1, kXT = Mode<EXACT>::prefetch ? kTile : 1;
    double q[kStages][SLICE][kTile];
-   static constexpr int kMaps = Mode<EXACT>::maps;
    uint32_t gmap[kMaps][ND][kTile];
-   double xg[Mode<EXACT>::prefetch ? 2 : 1][ND][Mode<EXACT>::prefetch ? kTile : 1];
+   double xs[kXBufs][kXND][kXT]; // exact: x gathered one tile ahead [i][lane]
+   uint32_t essm[kTile];         // per lane: slots whose DOF is essential (ess_out)
    uint64_t full[kStages];  // slice landed (tx count)
    uint64_t empty[kStages]; // slice consumed (kCompute arrivals)
    uint64_t gfull[kMaps], gempty[kMaps];
@@ -174,12 +176,12 @@ __device__ __forceinline__ void issue_gmap(TileSmem<P, Q, KIND, EXACT> &sm, cons
 // One qy slice of the diffusion chain for the calling thread's element:
 // d = T B^t / T G^t at (qx, qy), w = D d, then S = G^t w / B^t w over qx and
 // v += S B / S G (reference order; FIRST starts the v sums with a product).
-template <int P, int Q, bool EXACT, bool FIRST>
+template <int P, int Q, bool EXACT, bool FIRST, bool EN>
 __device__ __forceinline__ void diffusion_slice(const ApplyArgs &a, int qy, const double (&T1)[Q][P + 1],
                                                 const double (&T2)[Q][P + 1],
                                                 const double (*qs)[kTile], int tid,
                                                 double (&vx)[P + 1][P + 1],
-                                                double (&vy)[P + 1][P + 1])
+                                                double (&vy)[P + 1][P + 1], double &en, bool live)
 {
    constexpr int D1 = P + 1;
    double wx[Q], wy[Q];
@@ -195,6 +197,7 @@ __device__ __forceinline__ void diffusion_slice(const ApplyArgs &a, int qy, cons
       const double d0 = qs[0 * Q + qx][tid], d1 = qs[1 * Q + qx][tid], d2 = qs[2 * Q + qx][tid];
       wx[qx] = add<EXACT>(mul<EXACT>(d0, dx), mul<EXACT>(d1, dy));
       wy[qx] = add<EXACT>(mul<EXACT>(d1, dx), mul<EXACT>(d2, dy));
+      if (EN && live) en = mac<EXACT>(mac<EXACT>(en, dx, wx[qx]), dy, wy[qx]); // grad u . D grad u
    }
 #pragma unroll
    for (int i = 0; i < D1; i++) {
@@ -219,12 +222,12 @@ __device__ __forceinline__ void diffusion_slice(const ApplyArgs &a, int qy, cons
 }
 
 // FMA numerics: both terms go straight into R (R += S_x B + S_y G).
-template <int P, int Q, bool FIRST>
+template <int P, int Q, bool FIRST, bool EN>
 __device__ __forceinline__ void diffusion_slice_fused(const ApplyArgs &a, int qy,
                                                       const double (&T1)[Q][P + 1],
                                                       const double (&T2)[Q][P + 1],
                                                       const double (*qs)[kTile], int tid,
-                                                      double (&R)[P + 1][P + 1])
+                                                      double (&R)[P + 1][P + 1], double &en, bool live)
 {
    constexpr int D1 = P + 1;
    double wx[Q], wy[Q];
@@ -240,6 +243,7 @@ __device__ __forceinline__ void diffusion_slice_fused(const ApplyArgs &a, int qy
       const double d0 = qs[0 * Q + qx][tid], d1 = qs[1 * Q + qx][tid], d2 = qs[2 * Q + qx][tid];
       wx[qx] = fma(d0, dx, d1 * dy);
       wy[qx] = fma(d1, dx, d2 * dy);
+      if (EN && live) en = fma(dy, wy[qx], fma(dx, wx[qx], en));
    }
 #pragma unroll
    for (int i = 0; i < D1; i++) {
@@ -257,10 +261,10 @@ __device__ __forceinline__ void diffusion_slice_fused(const ApplyArgs &a, int qy
    }
 }
 
-template <int P, int Q, bool EXACT, bool FIRST>
+template <int P, int Q, bool EXACT, bool FIRST, bool EN>
 __device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const double (&T)[Q][P + 1],
                                            const double (*qs)[kTile], int tid,
-                                           double (&R)[P + 1][P + 1])
+                                           double (&R)[P + 1][P + 1], double &en, bool live)
 {
    constexpr int D1 = P + 1;
    double w[Q];
@@ -270,6 +274,7 @@ __device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const dou
 #pragma unroll
       for (int b = 1; b < D1; b++) u = mac<EXACT>(u, T[qx][b], a.t.B[qy][b]);
       w[qx] = mul<EXACT>(u, qs[qx][tid]);
+      if (EN && live) en = mac<EXACT>(en, u, w[qx]);
    }
 #pragma unroll
    for (int i = 0; i < D1; i++) {
@@ -282,33 +287,17 @@ __device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const dou
    }
 }
 
-// Gather of the calling lane's element values from the map in `map`
-// (masked essential DOFs read as zero; dead lanes give zeros).
-template <int ND>
-__device__ __forceinline__ void gather_x(const ApplyArgs &a, const uint32_t (*map)[kTile], int tid,
-                                         bool live, double (&X)[ND])
-{
-#pragma unroll
-   for (int i = 0; i < ND; i++) {
-      const uint32_t d = map[i][tid] & kDofMask;
-      double v = live ? __ldg(a.x + d) : 0.0;
-      if (a.mask_in && live && bit_set(a.mask_in, d)) v = 0.0;
-      X[i] = v;
-   }
-}
-
-template <int P, int Q, int KIND, bool EXACT>
+// EDOT: x . y as the sum of element energies (a.energy_dot; apply.cu).
+template <int P, int Q, int KIND, bool EXACT, bool EDOT>
 __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs a)
 {
+   using Smem = TileSmem<P, Q, KIND, EXACT>;
    constexpr int D1 = P + 1, ND = D1 * D1;
-   constexpr int kStages = TileSmem<P, Q, KIND, EXACT>::kStages;
-   constexpr int kMaps = TileSmem<P, Q, KIND, EXACT>::kMaps;
+   constexpr int kStages = Smem::kStages;
    constexpr bool kPrefetch = Mode<EXACT>::prefetch;
-   constexpr bool kRegX = Mode<EXACT>::xg == kXReg;
-   constexpr bool kMapRegs = Mode<EXACT>::map_in_regs;
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
-   auto &sm = *reinterpret_cast<TileSmem<P, Q, KIND, EXACT> *>(smem_raw);
+   auto &sm = *reinterpret_cast<Smem *>(smem_raw);
    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
    const int tid = threadIdx.x; // element slot inside the tile (compute warps)
    const int64_t ntiles = (a.ne + kTile - 1) / kTile;
@@ -319,7 +308,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
          mbar_init(&sm.full[s], 1);
          mbar_init(&sm.empty[s], kCompute);
       }
-      for (int b = 0; b < kMaps; b++) {
+      for (int b = 0; b < Smem::kMaps; b++) {
          mbar_init(&sm.gfull[b], 1);
          mbar_init(&sm.gempty[b], kCompute);
       }
@@ -327,22 +316,20 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
    }
    __syncthreads();
-   // map buffer of local tile lt and the parity of its n-th fill
-   auto map_buf = [](int64_t lt) { return static_cast<int>(lt % kMaps); };
-   auto map_par = [](int64_t lt) { return static_cast<unsigned>((lt / kMaps) & 1); };
    auto tile_elem = [&](int64_t lt) { return (blockIdx.x + lt * gridDim.x) * kTile + tid; };
    double dot = 0.0;
    if (warp == kCompute) {
       // ---------------------------------------------------------- producer
-      // map(lt + 1) goes out before tile lt's slices: consumers gather the
-      // next tile's x during tile lt and need it landed
+      // map(lt + 1) goes out before tile lt's slices (exact numerics gather
+      // the next tile's x during tile lt).
       if (lane == 0) {
          int64_t k = 0;
          if (my_tiles > 0) issue_gmap<P, Q, KIND, EXACT>(sm, a, ntiles, 0);
          for (int64_t lt = 0; lt < my_tiles; lt++) {
             const int64_t nt = lt + 1;
             if (nt < my_tiles) {
-               if (nt >= kMaps) mbar_wait(&sm.gempty[map_buf(nt)], map_par(nt - kMaps));
+               if (nt >= Smem::kMaps)
+                  mbar_wait(&sm.gempty[nt % Smem::kMaps], static_cast<unsigned>((nt / Smem::kMaps - 1) & 1));
                issue_gmap<P, Q, KIND, EXACT>(sm, a, ntiles, nt);
             }
             for (int qy = 0; qy < Q; qy++, k++) {
@@ -367,69 +354,75 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       if (lane == 0) mbar_arrive(&sm.empty[k % kStages]);
       k++;
    };
-   double Xn[ND]; // FMA mode: the next tile's x, gathered one tile ahead
-   if ((kPrefetch || kRegX) && my_tiles > 0) { // gather of the first tile
+   if (kPrefetch && my_tiles > 0) { // gather of the first tile
       mbar_wait(&sm.gfull[0], 0u);
-      if constexpr (kPrefetch) {
-         if (tile_elem(0) < a.ne) {
+      if (tile_elem(0) < a.ne) {
 #pragma unroll
-            for (int i = 0; i < ND; i++)
-               gather8(&sm.xg[0][i][kPrefetch ? tid : 0], a.x + (sm.gmap[0][i][tid] & kDofMask));
-         }
-         gather_arrive(&sm.xfull[0]);
-      } else if constexpr (kRegX) {
-         gather_x<ND>(a, sm.gmap[0], tid, tile_elem(0) < a.ne, Xn);
+         for (int i = 0; i < ND; i++)
+            gather8(&sm.xs[0][kPrefetch ? i : 0][kPrefetch ? tid : 0],
+                    a.x + (sm.gmap[0][i][tid] & kDofMask));
       }
+      gather_arrive(&sm.xfull[0]);
    }
+   const bool ess_is_mask = a.ess_out == a.mask_in;
+
    for (int64_t lt = 0; lt < my_tiles; lt++) {
       const int64_t e = tile_elem(lt);
       const bool live = e < a.ne;
-      const int gb = map_buf(lt);
-      const int xb = static_cast<int>(lt & 1);
-      uint32_t dof[kMapRegs ? ND : 1];
+      const int gb = static_cast<int>(lt % Smem::kMaps);
+      const int xb = kPrefetch ? static_cast<int>(lt & 1) : 0;
+      double *xs = &sm.xs[xb][0][0];
+      // element map and x: exact, gathered one tile ahead (or in the
+      // prologue); FMA, straight from global memory now.  The map is read
+      // again by the epilogue (no registers held across the qy loop).
+      if (kPrefetch) mbar_wait(&sm.xfull[xb], static_cast<unsigned>((lt >> 1) & 1));
+      else mbar_wait(&sm.gfull[gb], static_cast<unsigned>((lt / Smem::kMaps) & 1));
+      uint32_t essm = 0;
       double V[D1][D1];
-      if constexpr (kMapRegs) {
-         // kXSmem: this tile's gather was issued one tile ahead (or in the
-         // prologue); kXDirect: gather straight from global memory
-         if (kPrefetch) mbar_wait(&sm.xfull[xb], static_cast<unsigned>((lt >> 1) & 1));
-         else mbar_wait(&sm.gfull[gb], map_par(lt));
+#if TFEM_TMA_GATHER1
 #pragma unroll
-         for (int i = 0; i < ND; i++) {
-            dof[i] = sm.gmap[gb][i][tid];
-            const uint32_t d = dof[i] & kDofMask;
-            double v = live ? (kPrefetch ? sm.xg[kPrefetch ? xb : 0][i][kPrefetch ? tid : 0]
-                                         : __ldg(a.x + d))
-                            : 0.0;
-            if (a.mask_in && live && bit_set(a.mask_in, d)) v = 0.0;
-            V[i % D1][i / D1] = v;
-         }
-         __syncwarp();
-         if (lane == 0) mbar_arrive(&sm.gempty[gb]); // map buffer free again
-      } else {
-#pragma unroll
-         for (int i = 0; i < ND; i++) V[i % D1][i / D1] = Xn[i];
+      for (int i = 0; i < ND; i++) {
+         const uint32_t d = sm.gmap[gb][i][tid] & kDofMask;
+         double v = live ? (kPrefetch ? xs[i * kTile + tid] : __ldg(a.x + d)) : 0.0;
+         const bool m = a.mask_in && live && bit_set(a.mask_in, d);
+         const bool es = ess_is_mask ? m : live && a.ess_out && bit_set(a.ess_out, d);
+         essm |= static_cast<uint32_t>(es) << i;
+         if (m) v = 0.0;
+         V[i % D1][i / D1] = v;
       }
+#else
+      // all gathers first (one latency), then the masks
+#pragma unroll
+      for (int i = 0; i < ND; i++)
+         V[i % D1][i / D1] = !live ? 0.0 : kPrefetch ? xs[i * kTile + tid]
+                                                     : __ldg(a.x + (sm.gmap[gb][i][tid] & kDofMask));
+#pragma unroll
+      for (int i = 0; i < ND; i++) {
+         const uint32_t d = sm.gmap[gb][i][tid] & kDofMask;
+         const bool m = live && a.mask_in && bit_set(a.mask_in, d);
+         const bool es = ess_is_mask ? m : live && a.ess_out && bit_set(a.ess_out, d);
+         essm |= static_cast<uint32_t>(es) << i;
+         if (m) V[i % D1][i / D1] = 0.0;
+      }
+#endif
+      sm.essm[tid] = essm;
       // Gather of the next tile (issued after the x contraction, when V is
       // dead, to keep register pressure down).
       auto prefetch_next = [&]() {
-         if (!kPrefetch && !kRegX) return;
-         if (lt + 1 >= my_tiles) return;
-         const int nb = map_buf(lt + 1);
-         mbar_wait(&sm.gfull[nb], map_par(lt + 1));
-         const bool nlive = tile_elem(lt + 1) < a.ne;
-         if constexpr (kPrefetch) {
-            if (nlive) {
+         if (!kPrefetch || lt + 1 >= my_tiles) return;
+         const int nb = static_cast<int>((lt + 1) % Smem::kMaps);
+         mbar_wait(&sm.gfull[nb], static_cast<unsigned>(((lt + 1) / Smem::kMaps) & 1));
+         if (tile_elem(lt + 1) < a.ne) {
 #pragma unroll 4
-               for (int i = 0; i < ND; i++)
-                  gather8(&sm.xg[xb ^ 1][i][kPrefetch ? tid : 0],
-                          a.x + (sm.gmap[nb][i][tid] & kDofMask));
-            }
-            gather_arrive(&sm.xfull[xb ^ 1]);
-         } else if constexpr (kRegX) {
-            gather_x<ND>(a, sm.gmap[nb], tid, nlive, Xn);
+            for (int i = 0; i < ND; i++)
+               gather8(&sm.xs[kPrefetch ? xb ^ 1 : 0][kPrefetch ? i : 0][kPrefetch ? tid : 0],
+                       a.x + (sm.gmap[nb][i][tid] & kDofMask));
          }
+         gather_arrive(&sm.xfull[xb ^ 1]);
       };
       double R[D1][D1];
+      // EDOT: the element energies go straight into dot (live lanes)
+      double &en = dot;
       if (KIND == TFEM_DIFFUSION) {
          double T1[Q][D1], T2[Q][D1];
 #pragma unroll
@@ -451,8 +444,8 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
             double vx[D1][D1], vy[D1][D1];
 #pragma unroll
             for (int qy = 0; qy < Q; qy++) { // unrolled: table indices stay immediates
-               if (qy == 0) diffusion_slice<P, Q, EXACT, true>(a, qy, T1, T2, acquire(), tid, vx, vy);
-               else diffusion_slice<P, Q, EXACT, false>(a, qy, T1, T2, acquire(), tid, vx, vy);
+               if (qy == 0) diffusion_slice<P, Q, EXACT, true, EDOT>(a, qy, T1, T2, acquire(), tid, vx, vy, en, live);
+               else diffusion_slice<P, Q, EXACT, false, EDOT>(a, qy, T1, T2, acquire(), tid, vx, vy, en, live);
                release();
             }
 #pragma unroll
@@ -462,8 +455,8 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
          } else {
 #pragma unroll
             for (int qy = 0; qy < Q; qy++) {
-               if (qy == 0) diffusion_slice_fused<P, Q, true>(a, qy, T1, T2, acquire(), tid, R);
-               else diffusion_slice_fused<P, Q, false>(a, qy, T1, T2, acquire(), tid, R);
+               if (qy == 0) diffusion_slice_fused<P, Q, true, EDOT>(a, qy, T1, T2, acquire(), tid, R, en, live);
+               else diffusion_slice_fused<P, Q, false, EDOT>(a, qy, T1, T2, acquire(), tid, R, en, live);
                release();
             }
          }
@@ -481,32 +474,92 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
          prefetch_next();
 #pragma unroll
          for (int qy = 0; qy < Q; qy++) {
-            if (qy == 0) mass_slice<P, Q, EXACT, true>(a, qy, T, acquire(), tid, R);
-            else mass_slice<P, Q, EXACT, false>(a, qy, T, acquire(), tid, R);
+            if (qy == 0) mass_slice<P, Q, EXACT, true, EDOT>(a, qy, T, acquire(), tid, R, en, live);
+            else mass_slice<P, Q, EXACT, false, EDOT>(a, qy, T, acquire(), tid, R, en, live);
             release();
+         }
+      }
+      // Epilogue.  Warp-local DOFs: the owner lane adds its lower
+      // neighbours' slots (shuffled up 1 / 8 / 9 lanes; restriction.cu
+      // warp_partners) in ascending element order -- the scatter's sum
+      // without the E-vector.  x . y and essential values come from xs.
+      const int pc = lane & 7, pr = lane >> 3; // lane's cell in the warp patch
+      constexpr int p = P;
+      double u9 = 0.0, u8a = 0.0, u1a = 0.0, u1b = 0.0, u8b = 0.0;
+      double u1m[P > 1 ? P - 1 : 1] = {}, u8m[P > 1 ? P - 1 : 1] = {};
+#if TFEM_TMA_SHFL_GUARD
+      if (a.warp_local) // warp-uniform
+#endif
+      {
+         u9 = __shfl_up_sync(0xffffffffu, R[p][p], 9);
+         u8a = __shfl_up_sync(0xffffffffu, R[0][p], 8);
+         u1a = __shfl_up_sync(0xffffffffu, R[p][0], 1);
+         u1b = __shfl_up_sync(0xffffffffu, R[p][p], 1);
+         u8b = __shfl_up_sync(0xffffffffu, R[p][p], 8);
+#pragma unroll
+         for (int m = 1; m < P; m++) {
+            u1m[m - 1] = __shfl_up_sync(0xffffffffu, R[p][m], 1);
+            u8m[m - 1] = __shfl_up_sync(0xffffffffu, R[m][p], 8);
          }
       }
       if (live) {
 #pragma unroll
          for (int i = 0; i < ND; i++) {
-            const uint32_t g = kMapRegs ? dof[kMapRegs ? i : 0] : sm.gmap[gb][i][tid];
-            double r = R[i % D1][i / D1];
-            if (g & kExclusive) {
-               const uint32_t d = g & kDofMask;
-               if (!a.overwrite) r = add<EXACT>(a.y[d], r);
-               if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
+            const int ia = i % D1, ib = i / D1;
+            const uint32_t g = sm.gmap[gb][i][tid];
+            const uint32_t d = g & kDofMask;
+            const uint32_t fl = g & kFlagMask;
+            double r = R[ia][ib];
+            if (fl == kExclusive || (fl == kWarpOwner && a.warp_local)) {
+               // contributions in ascending element order: y = v0 (or
+               // y_old + v0), then + v1 ... (the scatter's order)
+               const double yo = a.overwrite ? 0.0 : a.y[d];
+               double acc = 0.0;
+               bool st = false;
+               auto push = [&](bool present, double x) {
+                  if (!present) return;
+                  acc = st ? add<EXACT>(acc, x) : (a.overwrite ? x : add<EXACT>(yo, x));
+                  st = true;
+               };
+               if (fl == kWarpOwner) { // present lower neighbours (warp_partners)
+                  if (ia == 0 && ib == 0) {
+                     push(pc >= 1 && pr >= 1, u9);
+                     push(pr >= 1, u8a);
+                     push(pc >= 1, u1a);
+                  } else if (ia == 0 && ib == p) {
+                     push(pc >= 1, u1b);
+                  } else if (ia == p && ib == 0) {
+                     push(pr >= 1, u8b);
+                  } else if (ia == 0) {
+                     push(pc >= 1, u1m[ib > 0 ? ib - 1 : 0]);
+                  } else if (ib == 0) {
+                     push(pr >= 1, u8m[ia > 0 ? ia - 1 : 0]);
+                  }
+               }
+               push(true, r);
+               r = acc;
+               const bool es = (sm.essm[tid] >> i) & 1u;
+               if (EDOT) {
+                  // energy of the masked x, plus x_d^2 where y_d = x_d
+                  if (es) {
+                     r = __ldg(a.x + d);
+                     dot = mac<EXACT>(dot, r, r);
+                  }
+               } else if (es || a.dot) {
+                  const double xd = __ldg(a.x + d);
+                  if (es) r = xd;
+                  if (a.dot && !(a.notown && bit_set(a.notown, d))) dot = mac<EXACT>(dot, xd, r);
+               }
                a.y[d] = r;
-               if (a.dot && !(a.notown && bit_set(a.notown, d)))
-                  dot = mac<EXACT>(dot, __ldg(a.x + d), r);
+            } else if (fl == kWarpMember && a.warp_local) {
+               // summed by the owner lane
             } else {
                a.evec[i * a.ne_pad + e] = r;
             }
          }
       }
-      if constexpr (!kMapRegs) {
-         __syncwarp();
-         if (lane == 0) mbar_arrive(&sm.gempty[gb]); // map buffer free again
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.gempty[gb]); // map buffer free again
    }
    } // consumers
    if (a.dot) {
@@ -521,15 +574,21 @@ template <int P, int Q, int KIND, bool EXACT>
 void launch(const ApplyArgs &a, cudaStream_t s, unsigned /*blocks*/)
 {
    const size_t smem = sizeof(TileSmem<P, Q, KIND, EXACT>);
+   static_assert(sizeof(TileSmem<P, Q, KIND, EXACT>) <= 227 * 1024, "shared memory budget");
    static const bool once = [&] {
-      cudaFuncSetAttribute(apply2d_tma_kernel<P, Q, KIND, EXACT>,
+      cudaFuncSetAttribute(apply2d_tma_kernel<P, Q, KIND, EXACT, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(apply2d_tma_kernel<P, Q, KIND, EXACT, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       return true;
    }();
    (void)once;
    const int64_t nblk = (a.ne + kTile - 1) / kTile;
    const unsigned grid = static_cast<unsigned>(nblk < g_sm_count ? nblk : g_sm_count);
-   apply2d_tma_kernel<P, Q, KIND, EXACT><<<grid, kBlock, smem, s>>>(a);
+   if (a.energy_dot)
+      apply2d_tma_kernel<P, Q, KIND, EXACT, true><<<grid, kBlock, smem, s>>>(a);
+   else
+      apply2d_tma_kernel<P, Q, KIND, EXACT, false><<<grid, kBlock, smem, s>>>(a);
 }
 
 template <int P, int KIND>
@@ -564,6 +623,8 @@ KernelPick pick_apply2d_tma(int p, int nq, int kind, bool exact, int sm_count)
    k.elems_per_block = kTile;
    k.threads = kBlock;
    k.persistent_blocks = sm_count;
+   k.warp_reduce = true;
+   k.energy_dot = true;
    return k;
 }
 

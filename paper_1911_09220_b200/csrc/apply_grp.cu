@@ -127,7 +127,7 @@ __global__ void apply2d_grp_kernel(const ApplyArgs a)
 #pragma unroll
          for (int qy = 1; qy < Q; qy++) r = mac<EXACT>(r, sm.S2[ia * Q + qy], sB[qy][b]);
       }
-      if (dof & kExclusive) {
+      if (is_exclusive(dof)) {
          const uint32_t d = dof & kDofMask;
          if (!a.overwrite) r = add<EXACT>(a.y[d], r);
          if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
@@ -291,7 +291,7 @@ __global__ void apply3d_kernel(const ApplyArgs a)
             }
          }
          const uint32_t gg = __ldg(gm + i);
-         if (gg & kExclusive) {
+         if (is_exclusive(gg)) {
             const uint32_t d = gg & kDofMask;
             if (!a.overwrite) r += a.y[d];
             if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);

@@ -465,14 +465,16 @@ int tfem_pa_qdata(const tfem_pa *pa, double *host)
       const size_t n = static_cast<size_t>(pa->ncomp) * pa->nqd * pa->ne_pad;
       std::vector<double> dev(n);
       d2h(pa->ctx->stream, dev.data(), pa->qdata, sizeof(double) * n);
-      for (int64_t e = 0; e < pa->ne; e++)
+      for (int64_t e = 0; e < pa->ne; e++) {
+         const int64_t pos = pa->order.pos_of(e);
          for (int q = 0; q < pa->nqd; q++)
             for (int c = 0; c < pa->ncomp; c++) {
                const double v = pa->elem_major()
-                                   ? dev[(e * pa->ncomp + c) * pa->nqd + q]
-                                   : dev[(static_cast<int64_t>(c) * pa->nqd + q) * pa->ne_pad + e];
+                                   ? dev[(pos * pa->ncomp + c) * pa->nqd + q]
+                                   : dev[(static_cast<int64_t>(c) * pa->nqd + q) * pa->ne_pad + pos];
                host[(e * pa->nqd + q) * pa->ncomp + c] = v;
             }
+      }
    });
 }
 

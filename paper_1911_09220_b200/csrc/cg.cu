@@ -17,6 +17,8 @@
 #include "common.cuh"
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <unordered_map>
 
@@ -362,7 +364,7 @@ Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
       w->s_elem.alloc(ctx->stream, blocks_for(op->n, kVecThreads), 1);
    } else {
       // everything the iteration touches must exist before graph capture
-      if (op->r->n_shared > 0) const_cast<tfem_restriction *>(op->r)->ensure_evec();
+      if (op->r->needs_evec()) const_cast<tfem_restriction *>(op->r)->ensure_evec();
       int64_t ge = 0, gs = 0;
       pa_apply_grids(op->pa.back(), op->r, &ge, &gs);
       w->s_elem.alloc(ctx->stream, ge, 1);
@@ -378,8 +380,9 @@ Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
 
 // One CG iteration's launches (used eagerly and under stream capture).
 void enqueue_iteration(tfem_ctx *ctx, const tfem_operator *op, Workspace &w, XBufs xb,
-                       const double *diag)
+                       const double *diag, cudaEvent_t *ev = nullptr)
 {
+
    const int64_t n = op->n;
    // alpha is taken by the last block of the operator's final launch, beta by
    // the last block of the update: four launches per iteration.
@@ -394,10 +397,13 @@ void enqueue_iteration(tfem_ctx *ctx, const tfem_operator *op, Workspace &w, XBu
    sv.state = w.st;
    sv.finish = kFinishBeta;
    operator_mult(ctx, op, w.p, w.q, &se, w.s_scatter.grid ? &ss : nullptr, &w.st->done);
+   if (ev) TFEM_CUDA(cudaEventRecord(ev[1], ctx->stream));
    const unsigned vb = vec_blocks(ctx, n);
    cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.p, w.q, w.r, diag, n, sv,
                                                          nullptr);
+   if (ev) TFEM_CUDA(cudaEventRecord(ev[2], ctx->stream));
    cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.r, diag, w.p, n);
+   if (ev) TFEM_CUDA(cudaEventRecord(ev[3], ctx->stream));
    ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
 }
@@ -737,6 +743,30 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
          for (int k = 0; k < 8; k++) dist_iteration();
          hs = read_state();
       }
+   } else if (std::getenv("TFEM_ITER_TIMING")) {
+      // Diagnostics: eager iterations with events between the launches;
+      // per-segment averages go to stderr (the graph path is the product).
+      cudaEvent_t ev[4];
+      for (auto &e : ev) TFEM_CUDA(cudaEventCreate(&e));
+      double acc[3] = {0, 0, 0};
+      int nit = 0;
+      while (!hs.done) {
+         for (int k = 0; k < 16; k++) {
+            TFEM_CUDA(cudaEventRecord(ev[0], ctx->stream));
+            enqueue_iteration(ctx, op, w, xb, diag, ev);
+            TFEM_CUDA(cudaEventSynchronize(ev[3]));
+            float t[3];
+            for (int j = 0; j < 3; j++) TFEM_CUDA(cudaEventElapsedTime(&t[j], ev[j], ev[j + 1]));
+            if (nit >= 4)
+               for (int j = 0; j < 3; j++) acc[j] += t[j];
+            nit++;
+         }
+         hs = read_state();
+      }
+      const int n = nit > 4 ? nit - 4 : 1;
+      std::fprintf(stderr, "[tfem] per iteration (us): operator %.1f  update %.1f  direction %.1f\n",
+                   1e3 * acc[0] / n, 1e3 * acc[1] / n, 1e3 * acc[2] / n);
+      for (auto &e : ev) cudaEventDestroy(e);
    } else {
       // Batches of iterations as one graph; the batch length keeps the
       // per-batch host round trip small against the work it covers.

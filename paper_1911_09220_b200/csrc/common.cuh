@@ -47,10 +47,73 @@ inline void d2h(cudaStream_t s, void *dst, const void *src, size_t bytes)
    TFEM_CUDA(cudaStreamSynchronize(s));
 }
 
-// Flag bit on an element-map entry: the DOF has exactly one element slot, so
-// the element kernel owns it and writes it directly (no E-vector round trip).
+// Flag bits (31:30) on an element-map entry:
+//   10 kExclusive   the DOF has exactly one element slot: the element kernel
+//                   owns it and writes it directly (no E-vector round trip)
+//   00 shared       several slots; summed from the E-vector by the scatter
+//   11 kWarpOwner / 01 kWarpMember
+//                   several slots, all in one warp patch of an ordered space
+//                   (ElemOrder): the 2D bulk-copy kernel sums them with warp
+//                   shuffles into the owner slot (the highest element); every
+//                   other kernel treats them as shared
+constexpr uint32_t kFlagMask = 0xc0000000u;
 constexpr uint32_t kExclusive = 0x80000000u;
-constexpr uint32_t kDofMask = 0x7fffffffu;
+constexpr uint32_t kWarpMember = 0x40000000u;
+constexpr uint32_t kWarpOwner = 0xc0000000u;
+constexpr uint32_t kDofMask = 0x3fffffffu;
+constexpr int kTmaTile = 224; // elements per tile of apply2d_tma.cu (7 warp patches)
+__host__ __device__ constexpr bool is_exclusive(uint32_t g) { return (g & kFlagMask) == kExclusive; }
+
+// Device element order (positions of the element map / qdata / E-vector).
+// pw == 0: position = element.  Otherwise (2D Cartesian, p <= 3) the mesh is
+// cut into pw x ph = 8 x 4 patches, one per warp (32 positions, row-major
+// inside: lane = 8 r + c), patches row-major: DOFs shared only inside a patch
+// are summed by warp shuffles, and a warp's x gathers stay coalesced along
+// its rows.  Partial patches at the mesh edge leave padding positions: zero
+// qdata, map entries DOF 0 without flags (their E-vector slots are written
+// but never read).
+struct ElemOrder {
+   int pw = 0, ph = 0;
+   int64_t nx = 0, ny = 0, px = 0, py = 0; // cells, patches per axis
+   __host__ __device__ int64_t n_pos(int64_t ne) const { return pw ? px * py * pw * ph : ne; }
+   __host__ __device__ int64_t pos_of(int64_t e) const
+   {
+      if (!pw) return e;
+      const int64_t i = e % nx, j = e / nx;
+      return ((j / ph) * px + i / pw) * (pw * ph) + (j % ph) * pw + i % pw;
+   }
+   // reference element at a position, -1 for padding
+   __host__ __device__ int64_t elem_at(int64_t pos) const
+   {
+      if (!pw) return pos;
+      const int64_t t = pos / (pw * ph), r = pos % (pw * ph);
+      const int64_t i = (t % px) * pw + r % pw, j = (t / px) * ph + r / pw;
+      return i < nx && j < ny ? j * nx + i : -1;
+   }
+   bool operator==(const ElemOrder &o) const
+   {
+      return pw == o.pw && ph == o.ph && (pw == 0 || (nx == o.nx && ny == o.ny));
+   }
+};
+
+// The order a (dim, p) space on a Cartesian mesh of n cells uses; the
+// restriction and every PaData of the space derive it independently.
+inline ElemOrder elem_order_for(int dim, int p, bool cartesian, const int *n)
+{
+   ElemOrder o;
+#ifdef TFEM_NO_ORDER
+   cartesian = false; // A/B: reference element order
+#endif
+   if (dim == 2 && p <= 3 && cartesian) {
+      o.pw = 8;
+      o.ph = 4;
+      o.nx = n[0];
+      o.ny = n[1];
+      o.px = (o.nx + o.pw - 1) / o.pw;
+      o.py = (o.ny + o.ph - 1) / o.ph;
+   }
+   return o;
+}
 
 constexpr int kMaxP = 8;
 constexpr int kMaxQ = 10;
@@ -97,7 +160,7 @@ struct tfem_vec {
 struct tfem_restriction {
    tfem_ctx *ctx = nullptr;
    int dim = 2, p = 1, nd = 4; // nd = (p+1)^dim
-   int64_t ne = 0, ne_pad = 0, ndofs = 0;
+   int64_t ne = 0, npos = 0, ne_pad = 0, ndofs = 0; // npos: positions (order.n_pos)
    // Element map with the kExclusive flag, layout elem_major_layout(dim, p):
    // slot-major [nd][ne_pad] or element-major [ne_pad][nd]; a `slot` indexes
    // both gmap and the E-vector.
@@ -115,10 +178,19 @@ struct tfem_restriction {
    int n_buckets = 0;
    Bucket buckets[kMaxBuckets];
    int64_t n_shared = 0;
+   tfem::ElemOrder order;
+   // Ordered spaces: the warp-local DOFs are flagged in gmap and the other
+   // shared DOFs form the global buckets (the bulk-copy kernel's scatter).
+   bool warp_local = false;
+   int n_gbuckets = 0;
+   Bucket gbuckets[kMaxBuckets];
+   int64_t n_gshared = 0;
    double *evec = nullptr;       // E-vector scratch, gmap layout (lazy)
    bool cartesian = false;
    int n[3] = {0, 0, 0};
    double *ensure_evec();
+   // element kernels write E-vector slots (shared DOFs; padding positions)
+   bool needs_evec() const { return n_shared > 0 || npos > ne; }
 };
 
 struct tfem_geometry {
@@ -137,9 +209,10 @@ struct tfem_pa {
    tfem_ctx *ctx = nullptr;
    int kind = TFEM_DIFFUSION, dim = 2, p = 1, nq = 3, rule = TFEM_GAUSS_LEGENDRE;
    int ncomp = 3, nqd = 9;
-   int64_t ne = 0, ne_pad = 0;
+   int64_t ne = 0, npos = 0, ne_pad = 0; // npos: element positions (order.n_pos)
    // elem_major_layout(dim, p) ? [e][c][q] : planes [(c * nqd + q)][ne_pad]
    double *qdata = nullptr;
+   tfem::ElemOrder order; // element positions of qdata (== the restriction's)
    bool elem_major() const { return tfem::elem_major_layout(dim, p); }
    std::vector<double> B, G; // nq x (p+1)
 };
@@ -210,18 +283,21 @@ double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n,
 
 // Restriction / layout (restriction.cu)
 tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne, int64_t ndofs,
-                                       bool elem_major, uint32_t *d_gmap_raw /* owned */);
+                                       bool elem_major, uint32_t *d_gmap_raw /* owned */,
+                                       ElemOrder order);
 void restriction_mult_transpose(tfem_ctx *ctx, const tfem_restriction *r, const double *e,
                                 double *l);
 
 // Shared-DOF scatter over the buckets (apply.cu): y[d] (+)= sum of the
 // E-vector slots of d in ascending element order; y[ess] = x[ess]; fused
-// x . y partials.  Returns the grid size (for the dot sink).
+// x . y partials.  `global_only`: just the DOFs that are not tile-local (the
+// tile kernel summed the others).  Returns the grid size (for the dot sink).
 int64_t scatter_shared(tfem_ctx *ctx, const tfem_restriction *r, const double *evec,
                        const double *x, double *y, bool overwrite, const uint32_t *ess_out,
                        const DotSink *dot, const int *done, bool exact,
-                       const uint32_t *notown = nullptr);
-int64_t scatter_grid(const tfem_restriction *r);
+                       const uint32_t *notown = nullptr, bool global_only = false,
+                       bool ess_only = false);
+int64_t scatter_grid(const tfem_restriction *r, bool global_only = false);
 
 // PA kernels (apply.cu)
 struct ApplyFlags {

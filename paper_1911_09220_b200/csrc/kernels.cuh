@@ -24,6 +24,10 @@ struct ApplyArgs {
    const uint32_t *mask_in;
    const uint32_t *ess_out;
    const uint32_t *notown; // DOFs owned by another rank: left out of the dot
+   int warp_local;  // sum kWarpOwner/kWarpMember DOFs in-warp (else E-vector)
+   int energy_dot;  // x . y = sum of element energies of the masked x + sum_ess x^2
+                    // (single integrator, mask_in == ess_out, no notown; the
+                    // scatter then adds only its essential DOFs' x^2)
    DotSink dot;     // fused x . y partials (CG's p . q)
    const int *done; // CG stop flag: skip the work once the solve has ended
 };
@@ -35,6 +39,8 @@ struct KernelPick {
    int elems_per_block = 1;
    int threads = 128;
    int persistent_blocks = 0; // > 0: grid = min(ceil(ne / elems_per_block), this)
+   bool warp_reduce = false;  // can sum warp-local DOFs itself (ordered spaces)
+   bool energy_dot = false;   // can take x . y as element energies
 };
 
 constexpr int kElemThreads2D = 128;

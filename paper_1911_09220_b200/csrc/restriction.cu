@@ -1,16 +1,22 @@
 // Element restriction G / G^T on the device.
 //
 // Device layout: the element map is stored slot-major,
-// gmap[i * ne_pad + e] (thread-per-element gathers are coalesced), with bit 31
-// set when DOF has a single element slot ("exclusive": written straight from
-// the element kernel).  DOFs with >= 2 slots get a transpose CSR whose slot
-// lists are sorted by element -- the reference's ascending-element
-// accumulation (forms.cpp:289-295) without atomics.
+// gmap[i * ne_pad + pos] (thread-per-element gathers are coalesced; pos is
+// the element's position in ElemOrder), with bit 31 set when DOF has a single
+// element slot ("exclusive": written straight from the element kernel).  DOFs
+// with >= 2 slots get a transpose CSR whose slot lists are sorted by element
+// -- the reference's ascending-element accumulation (forms.cpp:289-295)
+// without atomics.  Ordered spaces (ElemOrder) also flag the DOFs whose slots
+// all fall in one warp patch (kWarpOwner / kWarpMember).
 #include "common.cuh"
 
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 namespace tfem {
+
+void restriction_destroy(tfem_restriction *r);
 
 namespace {
 
@@ -26,6 +32,11 @@ struct Layout {
    bool elem_major;
    int nd;
    int64_t ne, ne_pad;
+   ElemOrder order;
+   // slot of (local i, element e) for an element in reference numbering
+   __host__ __device__ int64_t slot_e(int i, int64_t e) const { return slot(i, order.pos_of(e)); }
+   // reference element of a slot (the accumulation-order key)
+   __host__ __device__ int64_t elem_key(int64_t s) const { return order.elem_at(elem_of(s)); }
    __host__ __device__ int64_t slot(int i, int64_t e) const
    {
       return elem_major ? e * nd + i : (int64_t)i * ne_pad + e;
@@ -35,10 +46,10 @@ struct Layout {
    {
       return static_cast<int>(elem_major ? s % nd : s / ne_pad);
    }
-   // t in [0, ne*nd) enumerates every live slot
+   // t in [0, ne*nd) enumerates every live slot (padding positions excluded)
    __host__ __device__ int64_t live(int64_t t) const
    {
-      return elem_major ? t : (t / ne) * ne_pad + t % ne;
+      return elem_major ? t : slot_e(static_cast<int>(t / ne), t % ne);
    }
 };
 
@@ -82,7 +93,7 @@ __global__ void layout2d_kernel(int nx, int ny, int p, Layout L, uint32_t *gmap)
    const int64_t ib = nv + n_edges * pe;
    const int64_t v0 = i + (int64_t)(nx + 1) * j;
    auto put = [&](int a, int b, int64_t dof) {
-      gmap[L.slot(a + b * D1, e)] = static_cast<uint32_t>(dof);
+      gmap[L.slot_e(a + b * D1, e)] = static_cast<uint32_t>(dof);
    };
    put(0, 0, v0);
    put(p, 0, v0 + 1);
@@ -207,9 +218,9 @@ __global__ void sort_rows_kernel(uint32_t *slots, int64_t n, int c, Layout L)
    uint32_t *row = slots + s * c;
    for (int a = 1; a < c; a++) {
       const uint32_t v = row[a];
-      const int64_t key = L.elem_of(v);
+      const int64_t key = L.elem_key(v);
       int b = a - 1;
-      while (b >= 0 && L.elem_of(row[b]) > key) {
+      while (b >= 0 && L.elem_key(row[b]) > key) {
          row[b + 1] = row[b];
          b--;
       }
@@ -222,7 +233,7 @@ __global__ void gather_kernel(const uint32_t *gmap, Layout L, const double *l,
 {
    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    if (t >= L.ne * L.nd) return;
-   evec[t] = l[gmap[L.slot(static_cast<int>(t % L.nd), t / L.nd)] & kDofMask];
+   evec[t] = l[gmap[L.slot_e(static_cast<int>(t % L.nd), t / L.nd)] & kDofMask];
 }
 
 // Transpose of gather in element order, y += (forms.cpp:289-295).  Exclusive
@@ -232,8 +243,8 @@ __global__ void exclusive_add_kernel(const uint32_t *gmap, Layout L,
 {
    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    if (t >= L.ne * L.nd) return;
-   const uint32_t g = gmap[L.slot(static_cast<int>(t % L.nd), t / L.nd)];
-   if (g & kExclusive) l[g & kDofMask] += evec[t];
+   const uint32_t g = gmap[L.slot_e(static_cast<int>(t % L.nd), t / L.nd)];
+   if (is_exclusive(g)) l[g & kDofMask] += evec[t];
 }
 
 // API E-vector [e][i] -> internal gmap layout.
@@ -241,7 +252,7 @@ __global__ void to_internal_kernel(Layout L, const double *api, double *evec)
 {
    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    if (t >= L.ne * L.nd) return;
-   evec[L.slot(static_cast<int>(t % L.nd), t / L.nd)] = api[t];
+   evec[L.slot_e(static_cast<int>(t % L.nd), t / L.nd)] = api[t];
 }
 
 // Boundary of a Cartesian mesh: DOFs at lattice positions on the domain
@@ -264,7 +275,7 @@ __global__ void boundary_mark_kernel(const uint32_t *gmap, Layout L, int dim, in
       bool on = (i == 0 && a == 0) || (i == nx - 1 && a == p) || (j == 0 && b == 0) ||
                 (j == ny - 1 && b == p);
       if (dim == 3) on = on || (k == 0 && c == 0) || (k == nz - 1 && c == p);
-      if (on) mark[gmap[L.slot(l, e)] & kDofMask] = 1;
+      if (on) mark[gmap[L.slot_e(l, e)] & kDofMask] = 1;
    }
 }
 
@@ -287,10 +298,99 @@ void exclusive_scan(tfem_ctx *ctx, const int32_t *in, int32_t *out, int64_t n)
    ctx->launched();
 }
 
+// Warp-local DOFs of an ordered space (host side, once per space).  A
+// shared DOF is warp-local when all its slots lie in one warp patch (32
+// positions, lane = 8 r + c); its slot of the highest element is the owner
+// (kWarpOwner), the others members.  The kernel finds an owner's members by
+// position alone (warp_partners below: left / lower neighbours inside the
+// patch, in ascending element order) -- checked here against the sorted slot
+// list, so a DOF is only flagged when the rule reproduces it exactly.  All
+// other shared DOFs form the global buckets.
+struct Partner {
+   int lane_off, i; // member lane = owner lane - lane_off, local index i
+};
+int warp_partners(int p, int a, int b, int c, int r, Partner *out)
+{
+   const int D1 = p + 1;
+   int n = 0;
+   if (a == 0 && b == 0) {
+      if (c >= 1 && r >= 1) out[n++] = {9, p + p * D1};
+      if (r >= 1) out[n++] = {8, 0 + p * D1};
+      if (c >= 1) out[n++] = {1, p + 0 * D1};
+   } else if (a == 0 && b == p) {
+      if (c >= 1) out[n++] = {1, p + p * D1};
+   } else if (a == p && b == 0) {
+      if (r >= 1) out[n++] = {8, p + p * D1};
+   } else if (a == 0) {
+      if (c >= 1) out[n++] = {1, p + b * D1};
+   } else if (b == 0) {
+      if (r >= 1) out[n++] = {8, a + p * D1};
+   } else {
+      return -1; // never an owner
+   }
+   return n;
+}
+
+void build_warp_local(tfem_restriction *r, const Layout &L)
+{
+   cudaStream_t s = r->ctx->stream;
+   constexpr int W = 32;
+   const int p = r->p, D1 = p + 1;
+   std::vector<uint32_t> gmap(static_cast<size_t>(r->nd) * r->ne_pad);
+   d2h(s, gmap.data(), r->gmap, sizeof(uint32_t) * gmap.size());
+   std::vector<int32_t> gd[tfem_restriction::kMaxBuckets];
+   std::vector<uint32_t> gs[tfem_restriction::kMaxBuckets];
+   for (int b = 0; b < r->n_buckets; b++) {
+      const auto &bk = r->buckets[b];
+      const int c = bk.c;
+      std::vector<int32_t> dofs(static_cast<size_t>(bk.n));
+      std::vector<uint32_t> slots(static_cast<size_t>(bk.n) * c);
+      d2h(s, dofs.data(), bk.dofs, sizeof(int32_t) * dofs.size());
+      d2h(s, slots.data(), bk.slots, sizeof(uint32_t) * slots.size());
+      for (int64_t k = 0; k < bk.n; k++) {
+         const uint32_t *row = &slots[static_cast<size_t>(k) * c];
+         const int64_t w0 = L.elem_of(row[0]) / W;
+         bool local = true;
+         for (int j = 1; j < c && local; j++) local = L.elem_of(row[j]) / W == w0;
+         if (local) {
+            // row is sorted by element: the owner is the last slot
+            const uint32_t os = row[c - 1];
+            const int64_t opos = L.elem_of(os);
+            const int oi = L.local_of(os), lane = static_cast<int>(opos % W);
+            Partner pt[4];
+            const int n = warp_partners(p, oi % D1, oi / D1, lane % 8, lane / 8, pt);
+            local = n == c - 1;
+            for (int j = 0; j < n && local; j++)
+               local = row[j] == static_cast<uint32_t>(L.slot(pt[j].i, opos - pt[j].lane_off));
+         }
+         if (local) {
+            for (int j = 0; j + 1 < c; j++) gmap[row[j]] |= kWarpMember;
+            gmap[row[c - 1]] |= kWarpOwner;
+         } else {
+            gd[b].push_back(dofs[k]);
+            gs[b].insert(gs[b].end(), row, row + c);
+         }
+      }
+   }
+   h2d(s, r->gmap, gmap.data(), sizeof(uint32_t) * gmap.size());
+   for (int b = 0; b < r->n_buckets; b++) {
+      if (gd[b].empty()) continue;
+      auto &g = r->gbuckets[r->n_gbuckets++];
+      g.c = r->buckets[b].c;
+      g.n = static_cast<int64_t>(gd[b].size());
+      g.dofs = dalloc<int32_t>(g.n);
+      g.slots = dalloc<uint32_t>(g.n * g.c);
+      h2d(s, g.dofs, gd[b].data(), sizeof(int32_t) * gd[b].size());
+      h2d(s, g.slots, gs[b].data(), sizeof(uint32_t) * gs[b].size());
+      r->n_gshared += g.n;
+   }
+   r->warp_local = true;
+}
+
 } // namespace
 
 tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne, int64_t ndofs,
-                                       bool elem_major, uint32_t *gmap)
+                                       bool elem_major, uint32_t *gmap, ElemOrder order)
 {
    auto *r = new tfem_restriction;
    r->ctx = ctx;
@@ -298,13 +398,15 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
    r->p = p;
    r->nd = dim == 2 ? (p + 1) * (p + 1) : (p + 1) * (p + 1) * (p + 1);
    r->ne = ne;
-   r->ne_pad = round_up(ne, 64);
+   r->npos = order.n_pos(ne);
+   r->ne_pad = round_up(r->npos, 64);
    r->ndofs = ndofs;
    r->elem_major = elem_major;
    r->gmap = gmap;
+   r->order = order;
    const int64_t nslots = ne * r->nd;
    if (nslots >= (int64_t)INT32_MAX) invalid("restriction: more than 2^31-1 element slots on one device");
-   const Layout L{elem_major, r->nd, ne, r->ne_pad};
+   const Layout L{elem_major, r->nd, ne, r->ne_pad, order};
    cudaStream_t s = ctx->stream;
 
    int32_t *counts = dalloc<int32_t>(ndofs), *flag = dalloc<int32_t>(ndofs);
@@ -317,8 +419,9 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
    ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
    BucketPtrs bp{};
-   const int cmax = dim == 2 ? 4 : 8;
-   for (int c = 2; c <= cmax; c++) {
+   const int cmax = 8; // conforming quads / hexes: 4 / 8; larger valences are rejected below
+   int64_t covered = 0; // slots accounted for by exclusive DOFs and buckets
+   for (int c = 1; c <= cmax; c++) {
       flag_count_kernel<<<blocks_for(ndofs), kThreads, 0, s>>>(counts, ndofs, c, flag);
       ctx->launched();
       exclusive_scan(ctx, flag, scan, ndofs);
@@ -326,7 +429,8 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
       d2h(s, &last_scan, scan + ndofs - 1, 4);
       d2h(s, &last_flag, flag + ndofs - 1, 4);
       const int64_t n = static_cast<int64_t>(last_scan) + last_flag;
-      if (n == 0) continue;
+      covered += n * c;
+      if (n == 0 || c == 1) continue;
       const int b = r->n_buckets++;
       auto &bk = r->buckets[b];
       bk.c = c;
@@ -339,6 +443,15 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
       bp.c[b] = c;
       bp.slots[b] = bk.slots;
       r->n_shared += n;
+   }
+   if (covered != nslots) {
+      cudaFree(counts);
+      cudaFree(flag);
+      cudaFree(scan);
+      cudaFree(rank);
+      cudaFree(bucket_of);
+      restriction_destroy(r);
+      invalid("restriction: a DOF is shared by more than 8 elements");
    }
    TFEM_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * ndofs, s));
    if (r->n_buckets > 0) {
@@ -358,6 +471,7 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
    cudaFree(scan);
    cudaFree(rank);
    cudaFree(bucket_of);
+   if (order.pw == 8 && order.ph == 4 && !elem_major) build_warp_local(r, L);
    return r;
 }
 
@@ -365,7 +479,7 @@ void restriction_mult_transpose(tfem_ctx *ctx, const tfem_restriction *r, const 
                                 double *l)
 {
    const int64_t nslots = r->ne * r->nd;
-   const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad};
+   const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad, r->order};
    exclusive_add_kernel<<<blocks_for(nslots), kThreads, 0, ctx->stream>>>(r->gmap, L, e, l);
    ctx->launched();
    if (r->n_shared > 0) {
@@ -407,21 +521,22 @@ tfem_restriction *restriction_cartesian(tfem_ctx *ctx, int dim, const int *n, in
                             (int64_t)n[0] * n[1] * nvz;
       ndofs = nv + edges * pe + faces * pe * pe + ne * pe * pe * pe;
    }
-   if (ndofs >= (int64_t)kDofMask) invalid("restriction: more than 2^31-1 DOFs on one device");
+   if (ndofs >= (int64_t)kDofMask) invalid("restriction: more than 2^30-1 DOFs on one device");
    const int nd = dim == 2 ? (p + 1) * (p + 1) : (p + 1) * (p + 1) * (p + 1);
-   const int64_t ne_pad = round_up(ne, 64);
+   const ElemOrder order = elem_order_for(dim, p, true, n);
+   const int64_t ne_pad = round_up(order.n_pos(ne), 64);
    if ((int64_t)nd * ne_pad >= (int64_t)UINT32_MAX) invalid("restriction: too many element slots");
    uint32_t *gmap = dalloc<uint32_t>(nd * ne_pad);
    TFEM_CUDA(cudaMemsetAsync(gmap, 0, sizeof(uint32_t) * nd * ne_pad, ctx->stream));
    const bool em = elem_major_layout(dim, p);
    if (dim == 2)
-      layout2d_kernel<<<blocks_for(ne), kThreads, 0, ctx->stream>>>(n[0], n[1], p,
-                                                                   Layout{em, nd, ne, ne_pad}, gmap);
+      layout2d_kernel<<<blocks_for(ne), kThreads, 0, ctx->stream>>>(
+         n[0], n[1], p, Layout{em, nd, ne, ne_pad, order}, gmap);
    else
       layout3d_kernel<<<blocks_for(ne), kThreads, 0, ctx->stream>>>(n[0], n[1], n[2], p, gmap);
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
-   tfem_restriction *r = restriction_from_map(ctx, dim, p, ne, ndofs, em, gmap);
+   tfem_restriction *r = restriction_from_map(ctx, dim, p, ne, ndofs, em, gmap, order);
    r->cartesian = true;
    for (int d = 0; d < dim; d++) r->n[d] = n[d];
    return r;
@@ -433,7 +548,7 @@ tfem_restriction *restriction_create(tfem_ctx *ctx, int dim, int p, int64_t ne, 
    if (dim != 2 && dim != 3) invalid("restriction: dim must be 2 or 3");
    if (p < 1 || p > kMaxP) invalid("restriction: order must be in [1, 8]");
    if (ne < 1 || ndofs < 1) invalid("restriction: empty mesh");
-   if (ndofs >= (int64_t)kDofMask) invalid("restriction: more than 2^31-1 DOFs on one device");
+   if (ndofs >= (int64_t)kDofMask) invalid("restriction: more than 2^30-1 DOFs on one device");
    const int nd = dim == 2 ? (p + 1) * (p + 1) : (p + 1) * (p + 1) * (p + 1);
    const int64_t ne_pad = round_up(ne, 64);
    int32_t *emap = dalloc<int32_t>(ne * nd);
@@ -454,7 +569,7 @@ tfem_restriction *restriction_create(tfem_ctx *ctx, int dim, int p, int64_t ne, 
       cudaFree(gmap);
       invalid("restriction: element DOF index out of range");
    }
-   return restriction_from_map(ctx, dim, p, ne, ndofs, elem_major_layout(dim, p), gmap);
+   return restriction_from_map(ctx, dim, p, ne, ndofs, elem_major_layout(dim, p), gmap, ElemOrder{});
 }
 
 void restriction_destroy(tfem_restriction *r)
@@ -465,6 +580,10 @@ void restriction_destroy(tfem_restriction *r)
       cudaFree(r->buckets[b].dofs);
       cudaFree(r->buckets[b].slots);
    }
+   for (int b = 0; b < r->n_gbuckets; b++) {
+      cudaFree(r->gbuckets[b].dofs);
+      cudaFree(r->gbuckets[b].slots);
+   }
    cudaFree(r->evec);
    delete r;
 }
@@ -473,10 +592,10 @@ void restriction_elem_dofs(const tfem_restriction *r, int32_t *host)
 {
    std::vector<uint32_t> g(static_cast<size_t>(r->nd) * r->ne_pad);
    d2h(r->ctx->stream, g.data(), r->gmap, sizeof(uint32_t) * g.size());
-   const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad};
+   const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad, r->order};
    for (int64_t e = 0; e < r->ne; e++)
       for (int i = 0; i < r->nd; i++)
-         host[e * r->nd + i] = static_cast<int32_t>(g[L.slot(i, e)] & kDofMask);
+         host[e * r->nd + i] = static_cast<int32_t>(g[L.slot_e(i, e)] & kDofMask);
 }
 
 int64_t restriction_boundary_dofs(const tfem_restriction *r, int32_t *host)
@@ -485,7 +604,7 @@ int64_t restriction_boundary_dofs(const tfem_restriction *r, int32_t *host)
    tfem_ctx *ctx = r->ctx;
    int32_t *mark = dalloc<int32_t>(r->ndofs);
    TFEM_CUDA(cudaMemsetAsync(mark, 0, sizeof(int32_t) * r->ndofs, ctx->stream));
-   const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad};
+   const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad, r->order};
    boundary_mark_kernel<<<blocks_for(r->ne), kThreads, 0, ctx->stream>>>(
       r->gmap, L, r->dim, r->n[0], r->n[1], r->n[2], r->p, mark);
    ctx->launched();
@@ -505,7 +624,7 @@ int64_t restriction_boundary_dofs(const tfem_restriction *r, int32_t *host)
 
 void restriction_mult(tfem_ctx *ctx, const tfem_restriction *r, const double *l, double *e)
 {
-   const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad};
+   const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad, r->order};
    gather_kernel<<<blocks_for(r->ne * r->nd), kThreads, 0, ctx->stream>>>(r->gmap, L, l, e);
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());

@@ -115,21 +115,23 @@ __global__ void check_kernel(GeoSource g, GeoTables t, unsigned long long *err)
 
 template <int DIM>
 __global__ void setup_kernel(GeoSource g, GeoTables t, int kind, const double *coeff,
-                             double coeff_const, int64_t ne_pad, int emaj, double *qdata,
-                             unsigned long long *err)
+                             double coeff_const, int64_t ne_pad, int emaj, ElemOrder order,
+                             double *qdata, unsigned long long *err)
 {
    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    const int nq = t.npts, nqd = DIM == 2 ? nq * nq : nq * nq * nq;
    if (idx >= nqd * g.ne) return;
    // Planes [(c*nqd+q)][ne_pad]: element fastest; element-major [e][c][q]:
    // point fastest.  Either way the stores are coalesced.
+   // e: reference element number; pos: its position in the device order
    const int q = static_cast<int>(emaj ? idx % nqd : idx / g.ne);
    const int64_t e = emaj ? idx / nqd : idx % g.ne;
+   const int64_t pos = order.pos_of(e);
    const int qx = q % nq, qy = (q / nq) % nq, qz = q / (nq * nq);
    const int ncomp = kind == TFEM_MASS ? 1 : (DIM == 2 ? 3 : 6);
    auto out = [&](int c) -> double & {
-      return emaj ? qdata[(e * ncomp + c) * (int64_t)nqd + q]
-                  : qdata[(int64_t)(c * nqd + q) * ne_pad + e];
+      return emaj ? qdata[(pos * ncomp + c) * (int64_t)nqd + q]
+                  : qdata[(int64_t)(c * nqd + q) * ne_pad + pos];
    };
    double J[3][3];
    jacobian<DIM>(g, t, e, qx, qy, qz, J);
@@ -258,7 +260,9 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
    pa->ncomp = kind == TFEM_MASS ? 1 : (dim == 2 ? 3 : 6);
    pa->nqd = nqd;
    pa->ne = g->ne;
-   pa->ne_pad = round_up(g->ne, 64);
+   pa->order = elem_order_for(dim, p, g->cartesian, g->n);
+   pa->npos = pa->order.n_pos(g->ne);
+   pa->ne_pad = round_up(pa->npos, 64);
    pa->B.resize(static_cast<size_t>(nq) * (p + 1));
    pa->G.resize(pa->B.size());
    eval_matrices(p, TFEM_NODES_GAUSS_LOBATTO, nq, rule, pa->B.data(), pa->G.data());
@@ -291,12 +295,12 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
    if (dim == 2) {
       check_kernel<2><<<blocks_for(ncd * g->ne, T), T, 0, ctx->stream>>>(src, tc, d_err);
       setup_kernel<2><<<blocks_for(nqd * g->ne, T), T, 0, ctx->stream>>>(
-         src, tq, kind, d_coeff, coeff_const, pa->ne_pad, pa->elem_major() ? 1 : 0, pa->qdata,
-         d_err);
+         src, tq, kind, d_coeff, coeff_const, pa->ne_pad, pa->elem_major() ? 1 : 0, pa->order,
+         pa->qdata, d_err);
    } else {
       check_kernel<3><<<blocks_for(ncd * g->ne, T), T, 0, ctx->stream>>>(src, tc, d_err);
       setup_kernel<3><<<blocks_for(nqd * g->ne, T), T, 0, ctx->stream>>>(
-         src, tq, kind, d_coeff, coeff_const, pa->ne_pad, 1, pa->qdata, d_err);
+         src, tq, kind, d_coeff, coeff_const, pa->ne_pad, 1, pa->order, pa->qdata, d_err);
    }
    ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
