@@ -1,61 +1,38 @@
 // K2, 2D p <= 3: the thread-per-element sum factorisation of apply2d_reg.cu
 // fed by an asynchronous bulk-copy pipeline (sm_90+ cp.async.bulk + mbarrier;
-// SASS UBLKCP).
+// SASS UBLKCP, LDGSTS).
 //
-// Warp-specialised persistent kernel, one block of 8 warps per SM: warps
-// 0-6 compute (one element per lane, tiles of 224 consecutive elements),
-// warp 7 is the producer.  A tile's qdata is streamed as Q "slices" (one per
-// qy: the nc*Q planes (c, qy, qx), each a contiguous 1792 B run of the
-// [(c*nqd+q)][ne_pad] layout) through a ring of kStages shared-memory
-// stages, and the element map (D1^2 planes) through a double buffer.  The
-// producer waits on a stage's "empty" mbarrier (one arrive per compute warp)
-// before refilling it with cp.async.bulk; compute warps wait on "full" and
-// never on each other (no block barriers -- the per-slice __syncthreads of a
-// single-role design was its top stall; see profiles/).
+// Warp-specialised persistent kernel, one block of 8 warps per SM: warps 0-6
+// compute (one element per lane; a tile is 224 consecutive element positions,
+// seven 8 x 4 warp patches in ElemOrder), warp 7 is the producer.  A tile's
+// qdata is streamed as Q "slices" (one per qy: the nc*Q planes (c, qy, qx),
+// each a contiguous 1792 B run of the [(c*nqd+q)][ne_pad] layout) through a
+// 4-deep ring of shared-memory stages, and the element map (D1^2 planes)
+// through three buffers (the open tile's map is read again by its epilogue).
+// The producer waits on a stage's "empty" mbarrier (one arrive per compute
+// warp) before refilling it; compute warps wait on "full" and never on each
+// other (no block barriers: with warps in lockstep every latency is exposed;
+// see profiles/).  Each lane gathers the next tile's x into shared memory
+// (LDGSTS) while it computes the current one.
 //
-// Arithmetic is the same code path as apply2d_reg.cu (EXACT = reference
-// operation order, bit-identical).
+// Epilogue per slot: exclusive DOFs go straight to y; warp-local DOFs
+// (restriction.cu build_warp_local) are summed by the owner lane from its
+// lower neighbours' slots, shuffled up 1 / 8 / 9 lanes, in ascending element
+// order; the rest go to the E-vector for the scatter.  x . y (CG's p . q) is
+// taken as the sum of element energies when the operator allows (EDOT).
+//
+// EXACT: the reference operation order, bit-identical to the CPU; otherwise
+// fused multiply-adds and both gradient terms in one register block.
 #include "kernels.cuh"
 
 namespace tfem {
 
 namespace {
 
-#ifndef TFEM_TMA_WARPS
-#define TFEM_TMA_WARPS 7
-#endif
-constexpr int kCompute = TFEM_TMA_WARPS;   // compute warps per block
-constexpr int kTile = 32 * kCompute;       // elements per tile
-static_assert(kTile == kTmaTile, "tile records are built for kTmaTile-element tiles");
+constexpr int kCompute = 7;                 // compute warps per block
+constexpr int kTile = 32 * kCompute;        // elements per tile
+static_assert(kTile == kTmaTile, "kTmaTile is the tile of this kernel");
 constexpr int kBlock = 32 * (kCompute + 1); // + the producer warp
-// x of a tile: exact numerics gather it one tile ahead into shared memory
-// (LDGSTS) and keep a 4-deep slice ring; FMA numerics gather straight from
-// global memory at the start of the tile (stashing the values in shared
-// memory for the epilogue), accumulate both gradient terms into one register
-// block (32 fewer registers) and keep a 5-deep ring -- each the measured best
-// for its mode.  The FMA knobs are build-time defines so variants can be A/B
-// timed (tools/variants.sh).
-#ifndef TFEM_TMA_FMA_FUSED
-#define TFEM_TMA_FMA_FUSED 1
-#endif
-#ifndef TFEM_TMA_FMA_STAGES
-#define TFEM_TMA_FMA_STAGES 5
-#endif
-#ifndef TFEM_TMA_GATHER1
-#define TFEM_TMA_GATHER1 1
-#endif
-#ifndef TFEM_TMA_SHFL_GUARD
-#define TFEM_TMA_SHFL_GUARD 0
-#endif
-#ifndef TFEM_TMA_FMA_PREFETCH
-#define TFEM_TMA_FMA_PREFETCH 1
-#endif
-template <bool EXACT>
-struct Mode {
-   static constexpr bool prefetch = EXACT || TFEM_TMA_FMA_PREFETCH;
-   static constexpr bool fused = !EXACT && TFEM_TMA_FMA_FUSED;
-   static constexpr int stages = prefetch ? 4 : TFEM_TMA_FMA_STAGES; // qdata slice ring
-};
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -118,13 +95,11 @@ struct TileSmem {
    static constexpr int D1 = P + 1, ND = D1 * D1;
    static constexpr int NC = KIND == TFEM_MASS ? 1 : 3;
    static constexpr int SLICE = NC * Q; // planes per qy slice
-   static constexpr int kStages = Mode<EXACT>::stages;
-   static constexpr int kMaps = 3; // the open tile's map stays until its epilogue
-   static constexpr int kXBufs = Mode<EXACT>::prefetch ? 2 : 1;
-   static constexpr int kXND = Mode<EXACT>::prefetch ? ND : 1, kXT = Mode<EXACT>::prefetch ? kTile : 1;
+   static constexpr int kStages = 4; // qdata slice ring
+   static constexpr int kMaps = 3;   // the open tile's map stays until its epilogue
    double q[kStages][SLICE][kTile];
    uint32_t gmap[kMaps][ND][kTile];
-   double xs[kXBufs][kXND][kXT]; // exact: x gathered one tile ahead [i][lane]
+   double xs[2][ND][kTile];      // x of the open / next tile [i][lane]
    uint32_t essm[kTile];         // per lane: slots whose DOF is essential (ess_out)
    uint64_t full[kStages];  // slice landed (tx count)
    uint64_t empty[kStages]; // slice consumed (kCompute arrivals)
@@ -294,7 +269,6 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
    using Smem = TileSmem<P, Q, KIND, EXACT>;
    constexpr int D1 = P + 1, ND = D1 * D1;
    constexpr int kStages = Smem::kStages;
-   constexpr bool kPrefetch = Mode<EXACT>::prefetch;
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
    auto &sm = *reinterpret_cast<Smem *>(smem_raw);
@@ -354,13 +328,12 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       if (lane == 0) mbar_arrive(&sm.empty[k % kStages]);
       k++;
    };
-   if (kPrefetch && my_tiles > 0) { // gather of the first tile
+   if (my_tiles > 0) { // gather of the first tile
       mbar_wait(&sm.gfull[0], 0u);
       if (tile_elem(0) < a.ne) {
 #pragma unroll
          for (int i = 0; i < ND; i++)
-            gather8(&sm.xs[0][kPrefetch ? i : 0][kPrefetch ? tid : 0],
-                    a.x + (sm.gmap[0][i][tid] & kDofMask));
+            gather8(&sm.xs[0][i][tid], a.x + (sm.gmap[0][i][tid] & kDofMask));
       }
       gather_arrive(&sm.xfull[0]);
    }
@@ -370,53 +343,34 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       const int64_t e = tile_elem(lt);
       const bool live = e < a.ne;
       const int gb = static_cast<int>(lt % Smem::kMaps);
-      const int xb = kPrefetch ? static_cast<int>(lt & 1) : 0;
+      const int xb = static_cast<int>(lt & 1);
       double *xs = &sm.xs[xb][0][0];
-      // element map and x: exact, gathered one tile ahead (or in the
-      // prologue); FMA, straight from global memory now.  The map is read
+      // x: gathered one tile ahead (or in the prologue).  The map is read
       // again by the epilogue (no registers held across the qy loop).
-      if (kPrefetch) mbar_wait(&sm.xfull[xb], static_cast<unsigned>((lt >> 1) & 1));
-      else mbar_wait(&sm.gfull[gb], static_cast<unsigned>((lt / Smem::kMaps) & 1));
-      uint32_t essm = 0;
+      mbar_wait(&sm.xfull[xb], static_cast<unsigned>((lt >> 1) & 1));
+      uint32_t essm = 0; // slots whose DOF is essential (ess_out)
       double V[D1][D1];
-#if TFEM_TMA_GATHER1
 #pragma unroll
       for (int i = 0; i < ND; i++) {
          const uint32_t d = sm.gmap[gb][i][tid] & kDofMask;
-         double v = live ? (kPrefetch ? xs[i * kTile + tid] : __ldg(a.x + d)) : 0.0;
+         double v = live ? xs[i * kTile + tid] : 0.0;
          const bool m = a.mask_in && live && bit_set(a.mask_in, d);
          const bool es = ess_is_mask ? m : live && a.ess_out && bit_set(a.ess_out, d);
          essm |= static_cast<uint32_t>(es) << i;
          if (m) v = 0.0;
          V[i % D1][i / D1] = v;
       }
-#else
-      // all gathers first (one latency), then the masks
-#pragma unroll
-      for (int i = 0; i < ND; i++)
-         V[i % D1][i / D1] = !live ? 0.0 : kPrefetch ? xs[i * kTile + tid]
-                                                     : __ldg(a.x + (sm.gmap[gb][i][tid] & kDofMask));
-#pragma unroll
-      for (int i = 0; i < ND; i++) {
-         const uint32_t d = sm.gmap[gb][i][tid] & kDofMask;
-         const bool m = live && a.mask_in && bit_set(a.mask_in, d);
-         const bool es = ess_is_mask ? m : live && a.ess_out && bit_set(a.ess_out, d);
-         essm |= static_cast<uint32_t>(es) << i;
-         if (m) V[i % D1][i / D1] = 0.0;
-      }
-#endif
       sm.essm[tid] = essm;
       // Gather of the next tile (issued after the x contraction, when V is
       // dead, to keep register pressure down).
       auto prefetch_next = [&]() {
-         if (!kPrefetch || lt + 1 >= my_tiles) return;
+         if (lt + 1 >= my_tiles) return;
          const int nb = static_cast<int>((lt + 1) % Smem::kMaps);
          mbar_wait(&sm.gfull[nb], static_cast<unsigned>(((lt + 1) / Smem::kMaps) & 1));
          if (tile_elem(lt + 1) < a.ne) {
 #pragma unroll 4
             for (int i = 0; i < ND; i++)
-               gather8(&sm.xs[kPrefetch ? xb ^ 1 : 0][kPrefetch ? i : 0][kPrefetch ? tid : 0],
-                       a.x + (sm.gmap[nb][i][tid] & kDofMask));
+               gather8(&sm.xs[xb ^ 1][i][tid], a.x + (sm.gmap[nb][i][tid] & kDofMask));
          }
          gather_arrive(&sm.xfull[xb ^ 1]);
       };
@@ -440,7 +394,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
                T2[qx][b] = s2;
             }
          prefetch_next();
-         if constexpr (!Mode<EXACT>::fused) {
+         if constexpr (EXACT) {
             double vx[D1][D1], vy[D1][D1];
 #pragma unroll
             for (int qy = 0; qy < Q; qy++) { // unrolled: table indices stay immediates
@@ -487,10 +441,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       constexpr int p = P;
       double u9 = 0.0, u8a = 0.0, u1a = 0.0, u1b = 0.0, u8b = 0.0;
       double u1m[P > 1 ? P - 1 : 1] = {}, u8m[P > 1 ? P - 1 : 1] = {};
-#if TFEM_TMA_SHFL_GUARD
-      if (a.warp_local) // warp-uniform
-#endif
-      {
+      if (a.warp_local) { // warp-uniform
          u9 = __shfl_up_sync(0xffffffffu, R[p][p], 9);
          u8a = __shfl_up_sync(0xffffffffu, R[0][p], 8);
          u1a = __shfl_up_sync(0xffffffffu, R[p][0], 1);
