@@ -27,6 +27,7 @@ N > 1 (torchrun): the mesh is partitioned by element rows across ranks
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -327,11 +328,28 @@ def run_tfem(args):
         tf.abi.check(lib.tfem_operator_mult_async(dev.h, op.h, xin.h, yout.h))
     ev1.record(stream)
     ev1.synchronize()
-    t_op = ev0.elapsed_time(ev1) / 1e3 / M
+    t_op_alone = ev0.elapsed_time(ev1) / 1e3 / M
+    # The operator as it runs inside the solve (tfem_cg_profile: eager CG
+    # iterations with events between the launches); p arrives partly
+    # L2-resident from the direction kernel, which the standalone loop above
+    # does not see.
+    seg = (C.c_double * 3)()
+    xprof = tf.Vector(dev, N)
+    tf.abi.check(lib.tfem_cg_profile(dev.h, op.h, xin.h, min(args.iters, 100), diag.h, xprof.h, seg))
+    t_op = seg[0] * 1e-6
     peak, peak_kind = peaks()
     achieved = b_op / t_op / 1e9
     b_it = b_op + 96 * N
     cg_achieved = b_it * args.iters * args.steps / t_value / 1e9
+    cg_kernels = {
+        "operator": {"us": seg[0], "bytes_per_dof": b_op / N, "frac": achieved / peak},
+        "update": {"us": seg[1], "bytes_per_dof": 56,
+                   "frac": 56 * N / (seg[1] * 1e-6) / 1e9 / peak},
+        "direction": {"us": seg[2], "bytes_per_dof": 32,
+                      "frac": 32 * N / (seg[2] * 1e-6) / 1e9 / peak},
+        "standalone_operator_us": 1e6 * t_op_alone,
+        "source": "tfem_cg_profile (CUDA events between the launches of eager iterations)",
+    }
 
     # ---- end to end through the C ABI with host buffers
     e2e = None
@@ -380,7 +398,7 @@ def run_tfem(args):
                      "bytes_per_launch": b_op, "ms_per_launch": 1e3 * t_op,
                      "peak_source": peak_kind},
         "cg_roofline": {"achieved": cg_achieved, "frac": cg_achieved / peak, "unit": "GB/s",
-                        "bytes_per_dof_iteration": b_it / N},
+                        "bytes_per_dof_iteration": b_it / N, "kernels": cg_kernels},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
         "bit_exact_numerics": exact, "setup_s": setup_s,
     }

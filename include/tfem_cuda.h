@@ -271,6 +271,16 @@ int tfem_cg_solve_host(tfem_ctx *ctx, const tfem_operator *op,
                        const double *jacobi_diag, double *x,
                        tfem_cg_result *res);
 
+/* Diagnostics (no reference counterpart): `iters` iterations of the same
+ * Jacobi-PCG (tolerance 0) run eagerly with CUDA events on the context's
+ * stream between the launches; seg_us[0..2] = average time per iteration of
+ * the operator (element kernel + scatter), the update and the direction
+ * kernels, in microseconds -- the operator timed as it runs inside the
+ * solve (p was just written, so partly L2-resident). */
+int tfem_cg_profile(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *b,
+                    int iters, const tfem_vec *jacobi_diag, tfem_vec *x,
+                    double *seg_us);
+
 #ifdef __cplusplus
 }
 #endif

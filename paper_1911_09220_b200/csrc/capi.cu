@@ -632,6 +632,26 @@ int tfem_cg_solve(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *b, dou
    });
 }
 
+int tfem_cg_profile(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *b, int iters,
+                    const tfem_vec *jacobi_diag, tfem_vec *x, double *seg_us)
+{
+   return guard([&] {
+      need(ctx, "cg_profile");
+      need(op, "cg_profile");
+      need(seg_us, "cg_profile");
+      if (op->has_comm) invalid("cg_profile: single-device operators only");
+      if (iters < 1) invalid("cg_profile: iters must be >= 1");
+      if (!b || b->n != op->n || !x || x->n != op->n)
+         invalid("cg_profile: operator/vector size mismatch");
+      if (jacobi_diag && jacobi_diag->n != op->n)
+         invalid("cg_profile: preconditioner size mismatch");
+      if (x->d == b->d) invalid("cg_profile: x and b must not alias");
+      tfem_cg_result res{};
+      cg_solve(ctx, op, b->d, 0.0, iters, jacobi_diag ? jacobi_diag->d : nullptr, x->d, &res,
+               nullptr, nullptr, seg_us);
+   });
+}
+
 int tfem_cg_solve_host(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
                        int max_iters, const double *jacobi_diag, double *x, tfem_cg_result *res)
 {

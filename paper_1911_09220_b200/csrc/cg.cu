@@ -640,7 +640,7 @@ void operator_diagonal(tfem_ctx *ctx, const tfem_operator *op, double *diag)
 
 void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
               int max_iters, const double *diag, double *x, tfem_cg_result *res,
-              tfem_cg_callback cb, void *user)
+              tfem_cg_callback cb, void *user, double *seg_us)
 {
    const int64_t n = op->n;
    res->iterations = 0;
@@ -743,29 +743,28 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
          for (int k = 0; k < 8; k++) dist_iteration();
          hs = read_state();
       }
-   } else if (std::getenv("TFEM_ITER_TIMING")) {
-      // Diagnostics: eager iterations with events between the launches;
-      // per-segment averages go to stderr (the graph path is the product).
+   } else if (seg_us) {
+      // Diagnostics: eager iterations with events between the launches.
       cudaEvent_t ev[4];
       for (auto &e : ev) TFEM_CUDA(cudaEventCreate(&e));
       double acc[3] = {0, 0, 0};
       int nit = 0;
+      constexpr int kSkip = 4; // warm-up iterations left out of the averages
       while (!hs.done) {
-         for (int k = 0; k < 16; k++) {
+         for (int k = 0; k < 16 && nit < max_iters; k++) {
             TFEM_CUDA(cudaEventRecord(ev[0], ctx->stream));
             enqueue_iteration(ctx, op, w, xb, diag, ev);
             TFEM_CUDA(cudaEventSynchronize(ev[3]));
             float t[3];
             for (int j = 0; j < 3; j++) TFEM_CUDA(cudaEventElapsedTime(&t[j], ev[j], ev[j + 1]));
-            if (nit >= 4)
+            if (nit >= kSkip)
                for (int j = 0; j < 3; j++) acc[j] += t[j];
             nit++;
          }
          hs = read_state();
       }
-      const int n = nit > 4 ? nit - 4 : 1;
-      std::fprintf(stderr, "[tfem] per iteration (us): operator %.1f  update %.1f  direction %.1f\n",
-                   1e3 * acc[0] / n, 1e3 * acc[1] / n, 1e3 * acc[2] / n);
+      const int n = nit > kSkip ? nit - kSkip : 1;
+      for (int j = 0; j < 3; j++) seg_us[j] = 1e3 * acc[j] / n;
       for (auto &e : ev) cudaEventDestroy(e);
    } else {
       // Batches of iterations as one graph; the batch length keeps the

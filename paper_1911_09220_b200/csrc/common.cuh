@@ -328,7 +328,7 @@ void operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, doub
                    const DotSink *dot_elem, const DotSink *dot_scatter, const int *done);
 void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
               int max_iters, const double *diag, double *x, tfem_cg_result *res,
-              tfem_cg_callback cb, void *user);
+              tfem_cg_callback cb, void *user, double *seg_us = nullptr);
 
 } // namespace tfem
 

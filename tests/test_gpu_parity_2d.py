@@ -228,6 +228,27 @@ def test_cg_on_iterate_callback(dev):
     assert np.array_equal(seen[-1][1], res.x.numpy())
 
 
+def test_cg_profile_matches_solve(dev_fma):
+    """tfem_cg_profile (eager, events between launches) computes the same
+    iterates as the graph-replayed solve, and reports positive segment times."""
+    import ctypes as C
+    sp = tf.FeSpace.cartesian(dev_fma, (40, 40), 3)
+    a = tf.BilinearForm(sp)
+    a.add_diffusion(1.0)
+    a.assemble()
+    op = tf.ConstrainedOperator(a, sp.essential_true_dofs())
+    b = rng_vec(sp.n_dofs, 3)
+    b[sp.essential_true_dofs()] = 0.0
+    d = op.diagonal()
+    res = tf.cg_solve(op, b, 0.0, 37, d)
+    bv = tf.Vector.from_numpy(dev_fma, b)
+    xv = tf.Vector(dev_fma, sp.n_dofs)
+    seg = (C.c_double * 3)()
+    tf.abi.check(tf.lib().tfem_cg_profile(dev_fma.h, op.h, bv.h, 37, d.h, xv.h, seg))
+    assert np.array_equal(xv.numpy(), res.x.numpy())
+    assert all(v > 0.0 for v in seg)
+
+
 def test_setup_errors_match_reference(dev):
     sp = tf.FeSpace.cartesian(dev, (2, 2), 1)
     with pytest.raises(tf.InvalidArgument, match="coefficient must be positive"):
