@@ -68,6 +68,7 @@ typedef struct tfem_restriction tfem_restriction;
 typedef struct tfem_geometry tfem_geometry;
 typedef struct tfem_pa tfem_pa;
 typedef struct tfem_operator tfem_operator;
+typedef struct tfem_prolongation tfem_prolongation;
 
 /* ------------------------------------------------------------- errors */
 const char *tfem_last_error(void);
@@ -190,6 +191,33 @@ int tfem_pa_apply_local(tfem_ctx *ctx, const tfem_pa *pa,
 int tfem_pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa,
                      const tfem_restriction *r, tfem_vec *diag);
 
+/* --------------------------------------------------------- prolongation */
+/* FeSpace::prolongation() P (fespace.cpp:62-72, 166-203): N_L x N_T CSR with
+ * unit rows for true DOFs and constraint weights for hanging DOFs on
+ * non-conforming (forest) spaces; true_index[l] = FeSpace::true_index(l)
+ * (-1 for a constrained DOF).  Host arrays are copied. */
+int tfem_prolongation_create(tfem_ctx *ctx, int64_t n_local, int64_t n_true,
+                             const int32_t *rowptr, const int32_t *cols,
+                             const double *vals, const int32_t *true_index,
+                             tfem_prolongation **out);
+int tfem_prolongation_destroy(tfem_prolongation *P);
+/* true_to_local: y_L = P x_T (SparseMatrix::mult, sparse.cpp:75-87). */
+int tfem_prolongation_mult(tfem_ctx *ctx, const tfem_prolongation *P,
+                           const tfem_vec *x_true, tfem_vec *y_local);
+/* y_T = P^T x_L (SparseMatrix::mult_transpose, sparse.cpp:89-102: every
+ * y_T[j] sums its rows in ascending order). */
+int tfem_prolongation_mult_transpose(tfem_ctx *ctx, const tfem_prolongation *P,
+                                     const tfem_vec *x_local, tfem_vec *y_true);
+/* local_to_true: X[t] = x[true_dofs[t]] (fespace.cpp:252-262). */
+int tfem_prolongation_local_to_true(tfem_ctx *ctx, const tfem_prolongation *P,
+                                    const tfem_vec *x_local, tfem_vec *x_true);
+/* pa_diagonal on a space with P (forms.cpp:311-382): unconstrained elements
+ * add their exact local diagonal at true_index, constrained elements add the
+ * P-weighted couplings of every local pair that lands on one true DOF, all
+ * in the reference's element / pair order; diag_true += the result. */
+int tfem_pa_diagonal_p(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r,
+                       const tfem_prolongation *P, tfem_vec *diag_true);
+
 /* ------------------------------------------------------------- operator */
 /* BilinearForm::mult_true (forms.cpp:527-543) over n_pa integrators applied
  * in insertion order; with n_ess > 0 the ConstrainedOperator of
@@ -198,6 +226,13 @@ int tfem_pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa,
 int tfem_operator_create(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa,
                          const tfem_restriction *r, int64_t n_ess,
                          const int32_t *ess, tfem_operator **out);
+/* The same on a space with prolongation P (non-conforming meshes):
+ * y_T = P^T (sum_i A_i) P x_T (forms.cpp:534-542), essential DOFs and sizes
+ * on the true level.  P = NULL is tfem_operator_create. */
+int tfem_operator_create_p(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa,
+                           const tfem_restriction *r, const tfem_prolongation *P,
+                           int64_t n_ess, const int32_t *ess,
+                           tfem_operator **out);
 /* SparseOperator over a CSR matrix (solvers.hpp:26-35). */
 int tfem_operator_create_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr,
                              const int32_t *cols, const double *vals,

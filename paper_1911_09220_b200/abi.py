@@ -124,6 +124,14 @@ _PROTOS = {
     "tfem_pa_basis": (C.c_int, [vp, dp, dp]),
     "tfem_pa_apply_local": (C.c_int, [vp, vp, vp, vp, vp]),
     "tfem_pa_diagonal": (C.c_int, [vp, vp, vp, vp]),
+    "tfem_pa_diagonal_p": (C.c_int, [vp, vp, vp, vp, vp]),
+    "tfem_prolongation_create": (C.c_int, [vp, i64, i64, i32p, i32p, dp, i32p, C.POINTER(vp)]),
+    "tfem_prolongation_destroy": (C.c_int, [vp]),
+    "tfem_prolongation_mult": (C.c_int, [vp, vp, vp, vp]),
+    "tfem_prolongation_mult_transpose": (C.c_int, [vp, vp, vp, vp]),
+    "tfem_prolongation_local_to_true": (C.c_int, [vp, vp, vp, vp]),
+    "tfem_operator_create_p": (C.c_int, [vp, C.c_int, C.POINTER(vp), vp, vp, i64, i32p,
+                                         C.POINTER(vp)]),
     "tfem_operator_create": (C.c_int, [vp, C.c_int, C.POINTER(vp), vp, i64, i32p,
                                        C.POINTER(vp)]),
     "tfem_operator_set_comm": (C.c_int, [vp, C.POINTER(Comm), C.POINTER(Halo), i64, i32p]),

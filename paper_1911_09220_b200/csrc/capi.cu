@@ -22,6 +22,10 @@ void operator_set_comm(tfem_ctx *ctx, tfem_operator *op, const tfem_comm &comm,
 tfem_operator *operator_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, const int32_t *cols,
                             const double *vals);
 void operator_release(tfem_operator *op);
+tfem_prolongation *prolongation_create(tfem_ctx *ctx, int64_t n_local, int64_t n_true,
+                                       const int32_t *rowptr, const int32_t *cols,
+                                       const double *vals, const int32_t *true_index);
+void prolongation_destroy(tfem_prolongation *P);
 void operator_diagonal(tfem_ctx *ctx, const tfem_operator *op, double *diag);
 } // namespace tfem
 
@@ -519,15 +523,29 @@ int tfem_pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r
 int tfem_operator_create(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa, const tfem_restriction *r,
                          int64_t n_ess, const int32_t *ess, tfem_operator **out)
 {
+   return tfem_operator_create_p(ctx, n_pa, pa, r, nullptr, n_ess, ess, out);
+}
+
+int tfem_operator_create_p(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa,
+                           const tfem_restriction *r, const tfem_prolongation *P,
+                           int64_t n_ess, const int32_t *ess, tfem_operator **out)
+{
    return guard([&] {
       need(ctx, "tfem_operator_create");
       need(r, "tfem_operator_create");
       need(out, "tfem_operator_create");
       if (n_pa < 1) invalid("tfem_operator_create: need at least one integrator");
+      if (P && P->n_local != r->ndofs)
+         invalid("tfem_operator_create: prolongation / space size mismatch");
       auto *op = new tfem_operator;
       op->ctx = ctx;
-      op->n = r->ndofs;
+      op->n = P ? P->n_true : r->ndofs;
       op->r = r;
+      op->P = P;
+      if (P) {
+         TFEM_CUDA(cudaMalloc(&op->xl, sizeof(double) * static_cast<size_t>(r->ndofs)));
+         TFEM_CUDA(cudaMalloc(&op->yl, sizeof(double) * static_cast<size_t>(r->ndofs)));
+      }
       for (int k = 0; k < n_pa; k++) {
          if (!pa[k] || pa[k]->dim != r->dim || pa[k]->p != r->p || pa[k]->ne != r->ne) {
             delete op;
@@ -542,6 +560,79 @@ int tfem_operator_create(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa, const tfem
          throw;
       }
       *out = op;
+   });
+}
+
+// ------------------------------------------------------------ prolongation
+int tfem_prolongation_create(tfem_ctx *ctx, int64_t n_local, int64_t n_true, const int32_t *rowptr,
+                             const int32_t *cols, const double *vals, const int32_t *true_index,
+                             tfem_prolongation **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_prolongation_create");
+      need(rowptr, "tfem_prolongation_create");
+      need(true_index, "tfem_prolongation_create");
+      need(out, "tfem_prolongation_create");
+      if (rowptr[n_local] > 0 && (!cols || !vals)) invalid("tfem_prolongation_create: null CSR");
+      *out = prolongation_create(ctx, n_local, n_true, rowptr, cols, vals, true_index);
+   });
+}
+
+int tfem_prolongation_destroy(tfem_prolongation *P)
+{
+   return guard([&] { prolongation_destroy(P); });
+}
+
+int tfem_prolongation_mult(tfem_ctx *ctx, const tfem_prolongation *P, const tfem_vec *x_true,
+                           tfem_vec *y_local)
+{
+   return guard([&] {
+      need(ctx, "SparseMatrix::mult");
+      need(P, "SparseMatrix::mult");
+      if (!x_true || !y_local || x_true->n != P->n_true || y_local->n != P->n_local)
+         invalid("SparseMatrix::mult: size mismatch");
+      prolongation_mult(ctx, P, x_true->d, nullptr, y_local->d, nullptr);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+int tfem_prolongation_mult_transpose(tfem_ctx *ctx, const tfem_prolongation *P,
+                                     const tfem_vec *x_local, tfem_vec *y_true)
+{
+   return guard([&] {
+      need(ctx, "SparseMatrix::mult_transpose");
+      need(P, "SparseMatrix::mult_transpose");
+      if (!x_local || !y_true || x_local->n != P->n_local || y_true->n != P->n_true)
+         invalid("SparseMatrix::mult_transpose: size mismatch");
+      prolongation_mult_transpose(ctx, P, x_local->d, y_true->d, nullptr, nullptr, nullptr,
+                                  nullptr);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+int tfem_prolongation_local_to_true(tfem_ctx *ctx, const tfem_prolongation *P,
+                                    const tfem_vec *x_local, tfem_vec *x_true)
+{
+   return guard([&] {
+      need(ctx, "local_to_true");
+      need(P, "local_to_true");
+      if (!x_local || !x_true || x_local->n != P->n_local || x_true->n != P->n_true)
+         invalid("local_to_true: size mismatch");
+      prolongation_local_to_true(ctx, P, x_local->d, x_true->d);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+int tfem_pa_diagonal_p(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r,
+                       const tfem_prolongation *P, tfem_vec *diag_true)
+{
+   return guard([&] {
+      need(ctx, "pa_diagonal");
+      need(pa, "pa_diagonal");
+      need(r, "pa_diagonal");
+      need(P, "pa_diagonal");
+      if (!diag_true || diag_true->n != P->n_true) invalid("pa_diagonal: size mismatch");
+      pa_diagonal_p(ctx, pa, r, P, diag_true->d);
    });
 }
 

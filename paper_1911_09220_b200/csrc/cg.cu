@@ -362,6 +362,9 @@ Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
    w->xb = dalloc<double>(op->n);
    if (op->csr) {
       w->s_elem.alloc(ctx->stream, blocks_for(op->n, kVecThreads), 1);
+   } else if (op->P) {
+      if (op->r->needs_evec()) const_cast<tfem_restriction *>(op->r)->ensure_evec();
+      w->s_elem.alloc(ctx->stream, prolongation_grid(op->P), 1); // the P^T kernel's p . q
    } else {
       // everything the iteration touches must exist before graph capture
       if (op->r->needs_evec()) const_cast<tfem_restriction *>(op->r)->ensure_evec();
@@ -492,6 +495,7 @@ void operator_set_comm(tfem_ctx *ctx, tfem_operator *op, const tfem_comm &comm,
                        const tfem_halo &halo, int64_t n_not_owned, const int32_t *not_owned)
 {
    if (op->csr) invalid("tfem_operator_set_comm: needs a PA operator");
+   if (op->P) invalid("tfem_operator_set_comm: prolongated (non-conforming) operators run on one device");
    if (halo.n_peers < 0 || halo.n_peers > TFEM_MAX_PEERS)
       invalid("tfem_operator_set_comm: bad peer count");
    if (!halo.red) invalid("tfem_operator_set_comm: null reduction buffer");
@@ -580,6 +584,8 @@ void operator_release(tfem_operator *op)
    cudaFree(op->rowptr);
    cudaFree(op->cols);
    cudaFree(op->vals);
+   cudaFree(op->xl);
+   cudaFree(op->yl);
    delete op;
 }
 
@@ -595,6 +601,21 @@ void operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, doub
          op->rowptr, op->cols, op->vals, op->n, x, y, dot_elem ? *dot_elem : DotSink{}, done);
       ctx->launched();
       TFEM_CUDA(cudaGetLastError());
+      return;
+   }
+   if (op->P) {
+      // y_T = P^T (sum_i A_i) P x_T with the constraints on the true level:
+      // x_L = P (x with x[ess] = 0), y_L = the integrators' sum, then
+      // y_T = P^T y_L, y[ess] = x[ess] and the x . y partials
+      // (forms.cpp:164-190, 534-542)
+      prolongation_mult(ctx, op->P, x, op->ess_mask, op->xl, done);
+      for (size_t k = 0; k < op->pa.size(); k++) {
+         ApplyFlags f;
+         f.overwrite = (k == 0);
+         f.done = done;
+         pa_apply(ctx, op->pa[k], op->r, op->xl, op->yl, f);
+      }
+      prolongation_mult_transpose(ctx, op->P, op->yl, y, x, op->ess_mask, dot_elem, done);
       return;
    }
    for (size_t k = 0; k < op->pa.size(); k++) {
@@ -617,13 +638,17 @@ void operator_diagonal(tfem_ctx *ctx, const tfem_operator *op, double *diag)
    // diagonal_true (forms.cpp:545-557): each integrator's diagonal from zero,
    // then d.axpy(1.0, one) in insertion order.
    vec_fill(ctx, diag, op->n, 0.0);
+   auto one_diag = [&](const tfem_pa *pa, double *d) {
+      if (op->P) pa_diagonal_p(ctx, pa, op->r, op->P, d);
+      else pa_diagonal(ctx, pa, op->r, d);
+   };
    if (op->pa.size() == 1) {
-      pa_diagonal(ctx, op->pa[0], op->r, diag);
+      one_diag(op->pa[0], diag);
    } else {
       double *one = dalloc<double>(op->n);
       for (const tfem_pa *pa : op->pa) {
          vec_fill(ctx, one, op->n, 0.0);
-         pa_diagonal(ctx, pa, op->r, one);
+         one_diag(pa, one);
          vec_axpy(ctx, 1.0, one, diag, op->n);
       }
       TFEM_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -217,12 +217,25 @@ struct tfem_pa {
    std::vector<double> B, G; // nq x (p+1)
 };
 
+struct tfem_prolongation {
+   tfem_ctx *ctx = nullptr;
+   int64_t n_local = 0, n_true = 0, nnz = 0;
+   int32_t *rowptr = nullptr, *cols = nullptr; // P, N_L rows
+   double *vals = nullptr;
+   int32_t *trowptr = nullptr, *trows = nullptr; // P^T, N_T rows, ascending P rows
+   double *tvals = nullptr;
+   int32_t *true_index = nullptr; // [N_L], -1: constrained
+   int32_t *true_dofs = nullptr;  // [N_T]
+};
+
 struct tfem_operator {
    tfem_ctx *ctx = nullptr;
    bool csr = false;
    int64_t n = 0;
    std::vector<tfem_pa *> pa;
    const tfem_restriction *r = nullptr;
+   const tfem_prolongation *P = nullptr; // non-conforming: y = P^T A_L P x
+   double *xl = nullptr, *yl = nullptr;  // L-vector scratch (with P)
    int64_t n_ess = 0;
    int32_t *ess = nullptr;      // sorted list
    uint32_t *ess_mask = nullptr; // bitmap over DOFs
@@ -321,6 +334,18 @@ void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, do
 tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq, int rule,
                   const double *coeff_host, double coeff_const, int64_t *bad_elem);
 void geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq, int rule, double *host_xyz);
+
+// Prolongation (prolong.cu)
+void prolongation_mult(tfem_ctx *ctx, const tfem_prolongation *P, const double *x_true,
+                       const uint32_t *mask_true, double *y_local, const int *done);
+void prolongation_mult_transpose(tfem_ctx *ctx, const tfem_prolongation *P, const double *x_local,
+                                 double *y_true, const double *x_true_ess,
+                                 const uint32_t *ess_true, const DotSink *dot, const int *done);
+void prolongation_local_to_true(tfem_ctx *ctx, const tfem_prolongation *P, const double *x_local,
+                                double *x_true);
+void pa_diagonal_p(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r,
+                   const tfem_prolongation *P, double *diag_true);
+int64_t prolongation_grid(const tfem_prolongation *P);
 
 // Operators / CG (cg.cu)
 // With dot sinks set, the last integrator's launches emit x . y partials.

@@ -195,18 +195,26 @@ def as_vector(dev: Device, v) -> Vector:
 
 # ------------------------------------------------------------------ space
 class FeSpace:
-    """Conforming H1 space: the element restriction G (ElementRestriction)
-    plus the element geometry.  P is the identity (fespace.cpp:62-72)."""
+    """H1 space: the element restriction G (ElementRestriction), the element
+    geometry and the prolongation P -- the identity on conforming meshes
+    (fespace.cpp:62-72), [I; W] on non-conforming forests (:166-203)."""
 
-    def __init__(self, dev, dim, order, restriction, geometry, n_cells=None):
+    def __init__(self, dev, dim, order, restriction, geometry, n_cells=None, prolongation=None,
+                 n_true=None):
         self.dev = dev
         self.dim = dim
         self._order = order
         self.r = restriction
         self.g = geometry
+        self.P = prolongation
         self.n_cells = n_cells
         self.n_dofs = lib().tfem_restriction_n_dofs(restriction)
         self.n_elements = lib().tfem_restriction_n_elem(restriction)
+        self._n_true = self.n_dofs if prolongation is None else n_true
+
+    @property
+    def conforming(self) -> bool:
+        return self.P is None
 
     @classmethod
     def cartesian(cls, dev: Device, n: Sequence[int], order: int,
@@ -246,9 +254,20 @@ class FeSpace:
 
     @classmethod
     def from_mesh(cls, dev: Device, dim: int, order: int, elem_dofs: np.ndarray, n_dofs: int,
-                  ctrl: np.ndarray, geom_order: int = 1) -> "FeSpace":
+                  ctrl: np.ndarray, geom_order: int = 1, prolongation=None) -> "FeSpace":
         """A space from a host element -> DOF table (FeSpace::element_dofs,
-        [e][i]) and geometry control points ([e][lattice][dim])."""
+        [e][i]) and geometry control points ([e][lattice][dim]).
+        `prolongation` = (rowptr, cols, vals, true_index, n_true) of
+        FeSpace::prolongation() / true_index() on non-conforming meshes."""
+        P, n_true = None, None
+        if prolongation is not None:
+            rp, cols, vals, tix, n_true = prolongation
+            arrs = [np.ascontiguousarray(rp, dtype=np.int32), np.ascontiguousarray(cols, dtype=np.int32),
+                    np.ascontiguousarray(vals, dtype=np.float64), np.ascontiguousarray(tix, dtype=np.int32)]
+            P = abi.vp()
+            check(lib().tfem_prolongation_create(dev.h, n_dofs, n_true, _iptr(arrs[0]),
+                                                 _iptr(arrs[1]), _dptr(arrs[2]), _iptr(arrs[3]),
+                                                 C.byref(P)))
         ed = np.ascontiguousarray(elem_dofs, dtype=np.int32)
         r = abi.vp()
         check(lib().tfem_restriction_create(dev.h, dim, order, ed.shape[0], n_dofs, _iptr(ed),
@@ -260,14 +279,48 @@ class FeSpace:
         if rc:
             lib().tfem_restriction_destroy(r)
             check(rc)
-        return cls(dev, dim, order, r, g)
+        return cls(dev, dim, order, r, g, prolongation=P, n_true=n_true)
 
     def order(self) -> int:
         return self._order
 
     @property
     def n_true_dofs(self) -> int:
-        return self.n_dofs
+        return self._n_true
+
+    def true_to_local(self, x) -> Vector:
+        """P x (fespace.cpp:244-250)."""
+        xv = as_vector(self.dev, x)
+        if xv.n != self.n_true_dofs:
+            raise InvalidArgument("true_to_local: size mismatch")
+        y = Vector(self.dev, self.n_dofs)
+        if self.P is None:
+            y.axpy(1.0, xv)
+        else:
+            check(lib().tfem_prolongation_mult(self.dev.h, self.P, xv.h, y.h))
+        return y
+
+    def local_to_true(self, x) -> Vector:
+        """X[t] = x[true_dofs[t]] (fespace.cpp:252-262)."""
+        xv = as_vector(self.dev, x)
+        if xv.n != self.n_dofs:
+            raise InvalidArgument("local_to_true: size mismatch")
+        X = Vector(self.dev, self.n_true_dofs)
+        if self.P is None:
+            X.axpy(1.0, xv)
+        else:
+            check(lib().tfem_prolongation_local_to_true(self.dev.h, self.P, xv.h, X.h))
+        return X
+
+    def prolongation_transpose(self, y_local: Vector) -> Vector:
+        """P^T y (SparseMatrix::mult_transpose, sparse.cpp:89-102)."""
+        if self.P is None:
+            y = Vector(self.dev, self.n_dofs)
+            y.axpy(1.0, y_local)
+            return y
+        y = Vector(self.dev, self.n_true_dofs)
+        check(lib().tfem_prolongation_mult_transpose(self.dev.h, self.P, y_local.h, y.h))
+        return y
 
     def element_dofs(self) -> np.ndarray:
         nd = (self._order + 1) ** self.dim
@@ -304,6 +357,8 @@ class FeSpace:
         try:
             lib().tfem_restriction_destroy(self.r)
             lib().tfem_geometry_destroy(self.g)
+            if self.P is not None:
+                lib().tfem_prolongation_destroy(self.P)
         except Exception:
             pass
 
@@ -410,19 +465,26 @@ def pa_apply_local(pa: PaData, space: FeSpace, x: Vector, y: Vector, threads: in
 
 
 def pa_apply(pa: PaData, space: FeSpace, x) -> Vector:
-    """y = P^T G^T B^T D B G P x (forms.cpp:298-309); P = I (conforming)."""
+    """y = P^T G^T B^T D B G P x (forms.cpp:298-309)."""
     xv = as_vector(space.dev, x)
     if xv.n != space.n_true_dofs:
         raise InvalidArgument("pa_apply: size mismatch")
-    y = Vector(space.dev, space.n_dofs)
-    pa_apply_local(pa, space, xv, y)
-    return y
+    if space.P is None:
+        y = Vector(space.dev, space.n_dofs)
+        pa_apply_local(pa, space, xv, y)
+        return y
+    yl = Vector(space.dev, space.n_dofs)
+    pa_apply_local(pa, space, space.true_to_local(xv), yl)
+    return space.prolongation_transpose(yl)
 
 
 def pa_diagonal(pa: PaData, space: FeSpace) -> Vector:
-    """Exact diagonal (forms.cpp:311-382)."""
-    d = Vector(space.dev, space.n_dofs)
-    check(lib().tfem_pa_diagonal(space.dev.h, pa.h, space.r, d.h))
+    """Exact diagonal (forms.cpp:311-382), on the true DOFs."""
+    d = Vector(space.dev, space.n_true_dofs)
+    if space.P is None:
+        check(lib().tfem_pa_diagonal(space.dev.h, pa.h, space.r, d.h))
+    else:
+        check(lib().tfem_pa_diagonal_p(space.dev.h, pa.h, space.r, space.P, d.h))
     return d
 
 
@@ -478,9 +540,9 @@ class _PaOperator(LinearOperator):
             essential, dtype=np.int32)
         arr = (abi.vp * len(form._pa))(*[pa.h for pa in form._pa])
         h = abi.vp()
-        check(lib().tfem_operator_create(self.dev.h, len(form._pa), arr, form.space.r,
-                                         len(ess), _iptr(ess) if len(ess) else None,
-                                         C.byref(h)))
+        check(lib().tfem_operator_create_p(self.dev.h, len(form._pa), arr, form.space.r,
+                                           form.space.P, len(ess),
+                                           _iptr(ess) if len(ess) else None, C.byref(h)))
         self.h = h
         self.essential = ess
 
