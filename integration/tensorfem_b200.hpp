@@ -14,7 +14,8 @@
 //   pa_apply_local(pa, space, x, y)        tfem_pa_apply_local
 //   pa_diagonal(pa, space)                 tfem_pa_diagonal
 //   BilinearForm::mult_true                tfem_operator_mult
-//   ConstrainedOperator                    tfem_operator_create(..., ess)
+//   ConstrainedOperator                    tfem_operator_create_p(..., ess)
+//   FeSpace::prolongation() (NC forests)   tfem_prolongation_create
 //   cg_solve(op, b, tol, it, diag)         tfem_cg_solve (device loop)
 #pragma once
 
@@ -75,15 +76,12 @@ private:
    tfem_vec *v_ = nullptr;
 };
 
-// G and the element geometry of a conforming reference FeSpace.
+// G, the element geometry and (non-conforming forests) P of a reference
+// FeSpace.
 class DeviceSpace {
 public:
    DeviceSpace(const Device &dev, const FeSpace &space) : dev_(&dev), space_(&space)
    {
-      if (!space.conforming()) {
-         throw std::invalid_argument("b200: non-conforming spaces need the device P "
-                                     "(not built; SURVEY 8(f) rank 1)");
-      }
       const Mesh &mesh = space.mesh();
       const int ne = mesh.n_elements();
       const int p = space.collection().order();
@@ -115,11 +113,28 @@ public:
          }
       }
       check(tfem_geometry_create(dev.get(), 2, m, ne, ctrl.data(), &g_));
+      if (!space.conforming()) {
+         // P = [I; W] (fespace.cpp:166-203) and true_index
+         const SparseMatrix &P = space.prolongation();
+         std::vector<int32_t> rp(1, 0), cols, tix(space.n_dofs());
+         std::vector<double> vals;
+         for (int l = 0; l < P.rows(); l++) {
+            const auto c = P.row_cols(l);
+            const auto v = P.row_vals(l);
+            cols.insert(cols.end(), c.begin(), c.end());
+            vals.insert(vals.end(), v.begin(), v.end());
+            rp.push_back(static_cast<int32_t>(cols.size()));
+            tix[l] = space.true_index(l);
+         }
+         check(tfem_prolongation_create(dev.get(), P.rows(), P.cols(), rp.data(), cols.data(),
+                                        vals.data(), tix.data(), &p_));
+      }
    }
    ~DeviceSpace()
    {
       tfem_restriction_destroy(r_);
       tfem_geometry_destroy(g_);
+      tfem_prolongation_destroy(p_);
    }
    DeviceSpace(const DeviceSpace &) = delete;
    DeviceSpace &operator=(const DeviceSpace &) = delete;
@@ -127,12 +142,14 @@ public:
    const FeSpace &space() const { return *space_; }
    tfem_restriction *restriction() const { return r_; }
    tfem_geometry *geometry() const { return g_; }
+   tfem_prolongation *prolongation() const { return p_; } // NULL: conforming
 
 private:
    const Device *dev_;
    const FeSpace *space_;
    tfem_restriction *r_ = nullptr;
    tfem_geometry *g_ = nullptr;
+   tfem_prolongation *p_ = nullptr;
 };
 
 // PaData on the device (forms.hpp:29-58).
@@ -170,13 +187,17 @@ public:
       count_multiplies(tfem_pa_multiply_count(pa_));
    }
 
-   /// pa_diagonal (forms.cpp:311-382)
+   /// pa_diagonal (forms.cpp:311-382), on the true DOFs
    Vector diagonal() const
    {
       const Device &d = s_->device();
-      DVec dd(d, s_->space().n_dofs());
-      check(tfem_pa_diagonal(d.get(), pa_, s_->restriction(), dd.get()));
-      Vector out(s_->space().n_dofs());
+      const int n = s_->space().n_true_dofs();
+      DVec dd(d, n);
+      if (s_->prolongation())
+         check(tfem_pa_diagonal_p(d.get(), pa_, s_->restriction(), s_->prolongation(), dd.get()));
+      else
+         check(tfem_pa_diagonal(d.get(), pa_, s_->restriction(), dd.get()));
+      Vector out(n);
       dd.download(out);
       return out;
    }
@@ -196,9 +217,10 @@ public:
    {
       std::vector<tfem_pa *> h;
       for (const DevicePa *x : pa) h.push_back(x->get());
-      check(tfem_operator_create(s.device().get(), static_cast<int>(h.size()), h.data(),
-                                 s.restriction(), static_cast<int64_t>(essential.size()),
-                                 essential.empty() ? nullptr : essential.data(), &op_));
+      check(tfem_operator_create_p(s.device().get(), static_cast<int>(h.size()), h.data(),
+                                   s.restriction(), s.prolongation(),
+                                   static_cast<int64_t>(essential.size()),
+                                   essential.empty() ? nullptr : essential.data(), &op_));
    }
    ~DeviceOperator() override { tfem_operator_destroy(op_); }
    int rows() const override { return static_cast<int>(tfem_operator_size(op_)); }

@@ -27,15 +27,17 @@ def launches(path, tag):
     for d in data:
         v = float(d["Metric Value"]) * {"usecond": 1e3, "msecond": 1e6}.get(d["Metric Unit"], 1)
         k = re.sub(r"\(.*", "", d["Kernel Name"]).replace("tfem::<unnamed>::", "")
-        a = agg.setdefault(k, [0, 0.0])
-        a[0] += 1
-        a[1] += v
-    tot = sum(a[1] for a in agg.values())
+        agg.setdefault(k, []).append(v)
+    tot = sum(sum(v) for v in agg.values())
     out = [f"# {tag}: kernel launch list (ncu gpu__time_duration, cold cache, serialised)",
-           "", f"source: `{Path(path).name}`; shares are of all profiled launches", "",
-           "| kernel | launches | avg us | share |", "|---|---|---|---|"]
-    for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        out.append(f"| `{k}` | {c} | {t / c / 1e3:.1f} | {100 * t / tot:.1f}% |")
+           "", f"source: `{Path(path).name}`; shares are of all profiled launches.  CG "
+           "launches after the solve's last iteration exit at once (graph overshoot), so "
+           "the median is the per-launch cost.", "",
+           "| kernel | launches | median us | avg us | share |", "|---|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+        med = sorted(v)[len(v) // 2]
+        out.append(f"| `{k}` | {len(v)} | {med / 1e3:.1f} | {sum(v) / len(v) / 1e3:.1f} | "
+                   f"{100 * sum(v) / tot:.1f}% |")
     (HERE / f"{tag}_launches.md").write_text("\n".join(out) + "\n")
     print("\n".join(out))
 
