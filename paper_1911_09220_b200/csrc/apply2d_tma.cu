@@ -23,6 +23,7 @@
 //
 // EXACT: the reference operation order, bit-identical to the CPU; otherwise
 // fused multiply-adds and both gradient terms in one register block.
+#include "async.cuh"
 #include "kernels.cuh"
 
 namespace tfem {
@@ -33,62 +34,6 @@ constexpr int kCompute = 7;                 // compute warps per block
 constexpr int kTile = 32 * kCompute;        // elements per tile
 static_assert(kTile == kTmaTile, "kTmaTile is the tile of this kernel");
 constexpr int kBlock = 32 * (kCompute + 1); // + the producer warp
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p)
-{
-   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
-{
-   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
-{
-   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                "r"(bytes)
-                : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
-{
-   asm volatile("{\n"
-                ".reg .pred p;\n"
-                "WAIT_%=:\n"
-                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-                "@!p bra WAIT_%=;\n"
-                "}\n" ::"r"(smem_u32(bar)),
-                "r"(parity)
-                : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
-{
-   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// 8-byte asynchronous gather into shared memory (LDGSTS); a lane's pending
-// gathers arrive on an mbarrier when they land.
-__device__ __forceinline__ void gather8(void *dst, const void *src)
-{
-   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
-                : "memory");
-}
-
-__device__ __forceinline__ void gather_arrive(uint64_t *bar)
-{
-   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
-                : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
-{
-   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-                "[%3];" ::"r"(smem_u32(dst)),
-                "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                : "memory");
-}
 
 template <int P, int Q, int KIND, bool EXACT>
 struct TileSmem {
