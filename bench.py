@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--impl", default="tfem", choices=["tfem", "reference"])
     ap.add_argument("--dim", type=int, default=2)
     ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--bp", type=int, default=3, choices=[1, 3, 5],
+                    help="CEED problem: 1 mass (q=p+2 GL, plain CG), 3 diffusion (q=p+2 GL, "
+                         "Jacobi), 5 diffusion (q=p+1 GLL, Jacobi)")
     ap.add_argument("--cells", type=int, default=0, help="cells per axis (0: ~10M DOFs)")
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--numerics", default="fma", choices=["reference", "fma"])
@@ -229,8 +232,11 @@ def config_of(args, n, p, ndofs, per_step_iters=None, world=1):
     it = per_step_iters if per_step_iters is not None else args.iters
     dim = args.dim
     return {
-        "workload": f"BP3 {dim}D p={p} n={n}^{dim} ({ndofs:,} DOFs/rank), PA diffusion "
-                    f"q=p+2 Gauss-Legendre, Jacobi-PCG {it} iterations per step",
+        "workload": f"BP{args.bp} {dim}D p={p} n={n}^{dim} ({ndofs:,} DOFs/rank), "
+                    + {1: "PA mass q=p+2 Gauss-Legendre, CG",
+                       3: "PA diffusion q=p+2 Gauss-Legendre, Jacobi-PCG",
+                       5: "PA diffusion q=p+1 Gauss-Lobatto, Jacobi-PCG"}[args.bp]
+                    + f" {it} iterations per step",
         "dim": dim, "order": p, "cells_per_axis": n, "dofs_per_rank": ndofs,
         "dofs_total": ndofs * world, "iterations_per_step": it, "numerics": args.numerics,
         "l2": "inputs larger than L2 (qdata alone > 126 MB); no flush needed",
@@ -259,13 +265,19 @@ def run_tfem(args):
     t0 = time.perf_counter()
     sp = tf.FeSpace.cartesian(dev, cells, p)
     a = tf.BilinearForm(sp)
-    a.add_diffusion(1.0)
+    if args.bp == 1:
+        a.add_mass(1.0)
+    elif args.bp == 5:
+        a.add_diffusion(1.0, rule="gauss_lobatto", nq=p + 1)
+    else:
+        a.add_diffusion(1.0)
     a.assemble()
     ess = sp.essential_true_dofs()
     op = tf.ConstrainedOperator(a, ess)
     diag = op.diagonal()
     dev.sync()
     setup_s = time.perf_counter() - t0
+    pc = None if args.bp == 1 else diag  # BP1: unpreconditioned CG
     N = sp.n_dofs
     E = sp.n_elements
     b_host = np.random.default_rng(2020).uniform(-1.0, 1.0, N)
@@ -274,7 +286,7 @@ def run_tfem(args):
     x = tf.Vector(dev, N)
 
     def step():
-        return tf.cg_solve(op, b, 0.0, args.iters, diag, x=x)
+        return tf.cg_solve(op, b, 0.0, args.iters, pc, x=x)
 
     for _ in range(args.warmup):
         res = step()
@@ -313,8 +325,8 @@ def run_tfem(args):
         dev.set_numerics(args.numerics)
 
     # ---- roofline of the dominant kernel: the operator application
-    nc = 3 if args.dim == 2 else 6
-    nq = p + 2
+    nc = 1 if args.bp == 1 else (3 if args.dim == 2 else 6)
+    nq = p + 1 if args.bp == 5 else p + 2
     b_op = E * (nc * nq ** args.dim * 8 + (p + 1) ** args.dim * 4) + 16 * N
     xin = tf.Vector.from_numpy(dev, b_host)
     yout = tf.Vector(dev, N)
@@ -335,18 +347,20 @@ def run_tfem(args):
     # does not see.
     seg = (C.c_double * 3)()
     xprof = tf.Vector(dev, N)
-    tf.abi.check(lib.tfem_cg_profile(dev.h, op.h, xin.h, min(args.iters, 100), diag.h, xprof.h, seg))
+    tf.abi.check(lib.tfem_cg_profile(dev.h, op.h, xin.h, min(args.iters, 100),
+                                     pc.h if pc is not None else None, xprof.h, seg))
     t_op = seg[0] * 1e-6
     peak, peak_kind = peaks()
     achieved = b_op / t_op / 1e9
-    b_it = b_op + 96 * N
+    b_it = b_op + (80 if args.bp == 1 else 96) * N
     cg_achieved = b_it * args.iters * args.steps / t_value / 1e9
+    bu, bd = (48, 24) if args.bp == 1 else (56, 32)  # no diag stream in BP1
     cg_kernels = {
         "operator": {"us": seg[0], "bytes_per_dof": b_op / N, "frac": achieved / peak},
-        "update": {"us": seg[1], "bytes_per_dof": 56,
-                   "frac": 56 * N / (seg[1] * 1e-6) / 1e9 / peak},
-        "direction": {"us": seg[2], "bytes_per_dof": 32,
-                      "frac": 32 * N / (seg[2] * 1e-6) / 1e9 / peak},
+        "update": {"us": seg[1], "bytes_per_dof": bu,
+                   "frac": bu * N / (seg[1] * 1e-6) / 1e9 / peak},
+        "direction": {"us": seg[2], "bytes_per_dof": bd,
+                      "frac": bd * N / (seg[2] * 1e-6) / 1e9 / peak},
         "standalone_operator_us": 1e6 * t_op_alone,
         "source": "tfem_cg_profile (CUDA events between the launches of eager iterations)",
     }
@@ -358,6 +372,8 @@ def run_tfem(args):
         dp = torch.from_numpy(diag.numpy()).pin_memory()
         xp = torch.empty(N, dtype=torch.float64).pin_memory()
         bh, dh, xh = bp.numpy(), dp.numpy(), xp.numpy()
+        if pc is None:
+            dh = None
         tf.cg_solve_host(op, bh, 0.0, args.iters, dh, out=xh)
         dev.sync()
         w0 = time.perf_counter()
