@@ -177,20 +177,22 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             for (int qz = 0; qz < Q; qz++) { // contract c, point factors, back over qz
                const int q = qx + Q * (qy + Q * qz);
                if (KIND == TFEM_MASS) {
+                  // (qz, c) are compile-time here: table operands come from
+                  // the constant bank, not shared memory
                   double u = 0.0;
 #pragma unroll
-                  for (int c = 0; c < D1; c++) u = fma(sB[qz][c], UBB[c], u);
+                  for (int c = 0; c < D1; c++) u = fma(a.t.B[qz][c], UBB[c], u);
                   const double w = u * qd[q];
                   if (EDOT) dot = fma(u, w, dot);
 #pragma unroll
-                  for (int c = 0; c < D1; c++) Px[c] = fma(sB[qz][c], w, Px[c]);
+                  for (int c = 0; c < D1; c++) Px[c] = fma(a.t.B[qz][c], w, Px[c]);
                } else {
                   double ux = 0.0, uy = 0.0, uz = 0.0;
 #pragma unroll
                   for (int c = 0; c < D1; c++) {
-                     ux = fma(sB[qz][c], UGB[c], ux);
-                     uy = fma(sB[qz][c], UBG[c], uy);
-                     uz = fma(sG[qz][c], UBB[c], uz);
+                     ux = fma(a.t.B[qz][c], UGB[c], ux);
+                     uy = fma(a.t.B[qz][c], UBG[c], uy);
+                     uz = fma(a.t.G[qz][c], UBB[c], uz);
                   }
                   const double D00 = qd[q], D01 = qd[NQD + q], D02 = qd[2 * NQD + q];
                   const double D11 = qd[3 * NQD + q], D12 = qd[4 * NQD + q], D22 = qd[5 * NQD + q];
@@ -200,9 +202,9 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                   if (EDOT) dot = fma(uz, wz, fma(uy, wy, fma(ux, wx, dot)));
 #pragma unroll
                   for (int c = 0; c < D1; c++) {
-                     Px[c] = fma(sB[qz][c], wx, Px[c]);
-                     Py[c] = fma(sB[qz][c], wy, Py[c]);
-                     Pz[c] = fma(sG[qz][c], wz, Pz[c]);
+                     Px[c] = fma(a.t.B[qz][c], wx, Px[c]);
+                     Py[c] = fma(a.t.B[qz][c], wy, Py[c]);
+                     Pz[c] = fma(a.t.G[qz][c], wz, Pz[c]);
                   }
                }
             }
