@@ -1,5 +1,6 @@
-// K2, 3D with Q^2 <= 32 (BP1 / BP3 p <= 3, BP5 p <= 4): one element per
-// warp, fed by a bulk-copy pipeline (cp.async.bulk + mbarrier, LDGSTS).
+// K2, 3D with Q^2 <= 32 (BP1 / BP3 p <= 3, BP5 p <= 4): one group of
+// EPW = 32 / Q^2 elements per warp (1 for Q = 5, 2 for Q = 4, 3 for Q = 3),
+// fed by a bulk-copy pipeline (cp.async.bulk + mbarrier, LDGSTS).
 //
 // Persistent block per SM: warps 0..kW-1 compute, warp kW is the producer.
 // Warp w of block b takes elements e = (b kW + w) + k (grid kW), k = 0, 1, ..
@@ -23,15 +24,21 @@ namespace tfem {
 
 namespace {
 
+// Elements per warp: Q^2 <= 32 lanes per element in the column stage, so
+// low orders pack several elements into one warp (p=1: 3, p=2: 2).
+template <int Q>
+constexpr int epw() { return 32 / (Q * Q) > 0 ? 32 / (Q * Q) : 1; }
+
 template <int P, int Q, int KIND>
 struct alignas(16) Warp3 {
    static constexpr int D1 = P + 1, ND = D1 * D1 * D1, NQD = Q * Q * Q;
    static constexpr int NC = KIND == TFEM_MASS ? 1 : 6;
+   static constexpr int EPW = epw<Q>();
    static constexpr int kSlots = 2;
-   double q[kSlots][NC * NQD];            // the element's point factors
-   double V[2][ND];                       // x of the open / next element
-   double TB[D1 * D1 * Q], TG[D1 * D1 * Q]; // [c][b][qx]
-   double Px[D1 * Q * Q], Py[D1 * Q * Q], Pz[D1 * Q * Q]; // [c][qy][qx]
+   double q[kSlots][EPW * NC * NQD];                  // the group's point factors
+   double V[2][EPW * ND];                             // x of the open / next group
+   double TB[EPW * D1 * D1 * Q], TG[EPW * D1 * D1 * Q]; // [e][c][b][qx]
+   double Px[EPW * D1 * Q * Q], Py[EPW * D1 * Q * Q], Pz[EPW * D1 * Q * Q]; // [e][c][qy][qx]
    uint64_t full[kSlots], empty[kSlots];
 };
 
@@ -48,10 +55,11 @@ template <int P, int Q, int KIND, bool EDOT>
 __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kernel(const ApplyArgs a)
 {
    using W = Warp3<P, Q, KIND>;
-   constexpr int D1 = W::D1, ND = W::ND, NQD = W::NQD, NC = W::NC;
+   constexpr int D1 = W::D1, ND = W::ND, NQD = W::NQD, NC = W::NC, EPW = W::EPW;
    constexpr int kW = Cfg3<P, Q, KIND>::kW, kBlock = Cfg3<P, Q, KIND>::kBlock;
    constexpr int kSlots = W::kSlots;
-   constexpr int GPL = (ND + 31) / 32; // map entries per lane
+   constexpr int NT = D1 * D1 * Q;         // contraction outputs per element
+   constexpr int GPL = (EPW * ND + 31) / 32; // map entries per lane
    constexpr unsigned kQBytes = NC * NQD * 8;
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -71,8 +79,14 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
    }
    __syncthreads();
+   // warp w of block b takes element groups g = (b kW + w) + k (grid kW);
+   // group g is elements [g EPW, g EPW + EPW)
    const int64_t stride = (int64_t)gridDim.x * kW;
-   auto elem = [&](int w, int64_t k) { return (int64_t)blockIdx.x * kW + w + k * stride; };
+   auto group = [&](int w, int64_t k) { return (int64_t)blockIdx.x * kW + w + k * stride; };
+   auto count = [&](int64_t g) {
+      const int64_t left = a.ne - g * EPW;
+      return static_cast<int>(left < EPW ? (left > 0 ? left : 0) : EPW);
+   };
    double dot = 0.0;
    if (warp == kW) {
       // ---------------------------------------------------------- producer
@@ -80,14 +94,16 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          for (int64_t k = 0;; k++) {
             bool any = false;
             for (int w = 0; w < kW; w++) {
-               const int64_t e = elem(w, k);
-               if (e >= a.ne) continue;
+               const int64_t g = group(w, k);
+               const int cnt = count(g);
+               if (cnt == 0) continue;
                any = true;
                const int s = static_cast<int>(k % kSlots);
                if (k >= kSlots)
                   mbar_wait(&ws[w].empty[s], static_cast<unsigned>((k / kSlots - 1) & 1));
-               mbar_expect_tx(&ws[w].full[s], kQBytes);
-               bulk_g2s(ws[w].q[s], a.qdata + e * (int64_t)(NC * NQD), kQBytes, &ws[w].full[s]);
+               mbar_expect_tx(&ws[w].full[s], kQBytes * cnt);
+               bulk_g2s(ws[w].q[s], a.qdata + g * EPW * (int64_t)(NC * NQD), kQBytes * cnt,
+                        &ws[w].full[s]);
             }
             if (!any) break;
          }
@@ -96,29 +112,34 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    } else {
       // ---------------------------------------------------------- consumer
       W &sm = ws[warp];
-      const int qx = lane % Q, qy = lane / Q;
+      // column stage: lane -> (element ej, qx, qy)
+      const int ej = lane / (Q * Q), col = lane % (Q * Q);
+      const int qx = col % Q, qy = col / Q;
       uint32_t gcur[GPL], gnext[GPL];
-      auto load_map = [&](int64_t e, uint32_t (&g)[GPL]) {
+      auto load_map = [&](int64_t g, uint32_t (&m_)[GPL]) {
+         const int64_t lim = (int64_t)count(g) * ND;
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
             const int i = lane + 32 * m;
-            g[m] = (e < a.ne && i < ND) ? __ldg(a.gmap + e * ND + i) : 0u;
+            m_[m] = i < lim ? __ldg(a.gmap + g * EPW * ND + i) : 0u;
          }
       };
-      auto prefetch_x = [&](int64_t e, const uint32_t (&g)[GPL], int buf) {
-         if (e >= a.ne) return;
+      auto prefetch_x = [&](int64_t g, const uint32_t (&m_)[GPL], int buf) {
+         const int64_t lim = (int64_t)count(g) * ND;
+         if (lim == 0) return;
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
             const int i = lane + 32 * m;
-            if (i < ND) gather8(&sm.V[buf][i], a.x + (g[m] & kDofMask));
+            if (i < lim) gather8(&sm.V[buf][i], a.x + (m_[m] & kDofMask));
          }
          cp_async_commit();
       };
-      load_map(elem(warp, 0), gcur);
-      prefetch_x(elem(warp, 0), gcur, 0);
+      load_map(group(warp, 0), gcur);
+      prefetch_x(group(warp, 0), gcur, 0);
       for (int64_t k = 0;; k++) {
-         const int64_t e = elem(warp, k);
-         if (e >= a.ne) break;
+         const int64_t g = group(warp, k);
+         const int cnt = count(g);
+         if (cnt == 0) break;
          const int vb = static_cast<int>(k & 1);
          cp_async_wait_all();
          // essential DOFs read as zero (masked gather)
@@ -126,41 +147,43 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
 #pragma unroll
             for (int m = 0; m < GPL; m++) {
                const int i = lane + 32 * m;
-               if (i < ND && bit_set(a.mask_in, gcur[m] & kDofMask)) sm.V[vb][i] = 0.0;
+               if (i < cnt * ND && bit_set(a.mask_in, gcur[m] & kDofMask)) sm.V[vb][i] = 0.0;
             }
          }
          __syncwarp();
-         const int64_t en = elem(warp, k + 1);
-         load_map(en, gnext);
+         const int64_t gn = group(warp, k + 1);
+         load_map(gn, gnext);
          const double *V = sm.V[vb];
-         // contract a -> TB / TG [c][b][qx]
-         for (int j = lane; j < D1 * D1 * Q; j += 32) {
-            const int jx = j % Q, cb = j / Q;
+         // contract a -> TB / TG [e][c][b][qx]
+         for (int jj = lane; jj < EPW * NT; jj += 32) {
+            const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q;
             double sb = 0.0, sg = 0.0;
 #pragma unroll
             for (int kk = 0; kk < D1; kk++) {
-               const double v = V[cb * D1 + kk];
+               const double v = V[j * ND + cb * D1 + kk];
                sb = fma(sB[jx][kk], v, sb);
                if (KIND == TFEM_DIFFUSION) sg = fma(sG[jx][kk], v, sg);
             }
-            sm.TB[j] = sb;
-            sm.TG[j] = sg;
+            sm.TB[jj] = sb;
+            sm.TG[jj] = sg;
          }
-         prefetch_x(en, gnext, vb ^ 1); // the other buffer is free
+         prefetch_x(gn, gnext, vb ^ 1); // the other buffer is free
          __syncwarp();
          const int s = static_cast<int>(k % kSlots);
          mbar_wait(&sm.full[s], static_cast<unsigned>((k / kSlots) & 1));
-         if (lane < Q * Q) {
+         if (ej < EPW) {
+            const bool live = ej < cnt;
+            const double *TB = sm.TB + ej * NT, *TG = sm.TG + ej * NT;
             double UBB[D1], UBG[D1], UGB[D1];
 #pragma unroll
             for (int c = 0; c < D1; c++) { // contract b
                double bb = 0.0, bg = 0.0, gb = 0.0;
 #pragma unroll
                for (int b = 0; b < D1; b++) {
-                  const double tb = sm.TB[(c * D1 + b) * Q + qx];
+                  const double tb = TB[(c * D1 + b) * Q + qx];
                   bb = fma(sB[qy][b], tb, bb);
                   if (KIND == TFEM_DIFFUSION) {
-                     const double tg = sm.TG[(c * D1 + b) * Q + qx];
+                     const double tg = TG[(c * D1 + b) * Q + qx];
                      bg = fma(sG[qy][b], tb, bg);
                      gb = fma(sB[qy][b], tg, gb);
                   }
@@ -172,18 +195,18 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             double Px[D1], Py[D1], Pz[D1];
 #pragma unroll
             for (int c = 0; c < D1; c++) Px[c] = Py[c] = Pz[c] = 0.0;
-            const double *qd = sm.q[s];
+            const double *qd = sm.q[s] + ej * NC * NQD;
 #pragma unroll
             for (int qz = 0; qz < Q; qz++) { // contract c, point factors, back over qz
                const int q = qx + Q * (qy + Q * qz);
+               // (qz, c) are compile-time here: table operands come from the
+               // constant bank, not shared memory
                if (KIND == TFEM_MASS) {
-                  // (qz, c) are compile-time here: table operands come from
-                  // the constant bank, not shared memory
                   double u = 0.0;
 #pragma unroll
                   for (int c = 0; c < D1; c++) u = fma(a.t.B[qz][c], UBB[c], u);
                   const double w = u * qd[q];
-                  if (EDOT) dot = fma(u, w, dot);
+                  if (EDOT && live) dot = fma(u, w, dot);
 #pragma unroll
                   for (int c = 0; c < D1; c++) Px[c] = fma(a.t.B[qz][c], w, Px[c]);
                } else {
@@ -199,7 +222,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                   const double wx = fma(D02, uz, fma(D01, uy, D00 * ux));
                   const double wy = fma(D12, uz, fma(D11, uy, D01 * ux));
                   const double wz = fma(D22, uz, fma(D12, uy, D02 * ux));
-                  if (EDOT) dot = fma(uz, wz, fma(uy, wy, fma(ux, wx, dot)));
+                  if (EDOT && live) dot = fma(uz, wz, fma(uy, wy, fma(ux, wx, dot)));
 #pragma unroll
                   for (int c = 0; c < D1; c++) {
                      Px[c] = fma(a.t.B[qz][c], wx, Px[c]);
@@ -208,50 +231,54 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                   }
                }
             }
+            const int po = ej * D1 * Q * Q;
 #pragma unroll
             for (int c = 0; c < D1; c++) {
-               sm.Px[(c * Q + qy) * Q + qx] = Px[c];
+               sm.Px[po + (c * Q + qy) * Q + qx] = Px[c];
                if (KIND == TFEM_DIFFUSION) {
-                  sm.Py[(c * Q + qy) * Q + qx] = Py[c];
-                  sm.Pz[(c * Q + qy) * Q + qx] = Pz[c];
+                  sm.Py[po + (c * Q + qy) * Q + qx] = Py[c];
+                  sm.Pz[po + (c * Q + qy) * Q + qx] = Pz[c];
                }
             }
          }
          __syncwarp();
          if (lane == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
-         // contract qy -> [c][b][qx] (x-gradient part in TB, y + z in TG)
-         for (int j = lane; j < D1 * D1 * Q; j += 32) {
-            const int jx = j % Q, cb = j / Q, b = cb % D1, c = cb / D1;
+         // contract qy -> [e][c][b][qx] (x-gradient part in TB, y + z in TG)
+         for (int jj = lane; jj < EPW * NT; jj += 32) {
+            const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q, b = cb % D1, c = cb / D1;
+            const int po = j * D1 * Q * Q;
             double sx = 0.0, syz = 0.0;
 #pragma unroll
             for (int y = 0; y < Q; y++) {
-               const int o = (c * Q + y) * Q + jx;
+               const int o = po + (c * Q + y) * Q + jx;
                sx = fma(sB[y][b], sm.Px[o], sx);
                if (KIND == TFEM_DIFFUSION) {
                   syz = fma(sG[y][b], sm.Py[o], syz);
                   syz = fma(sB[y][b], sm.Pz[o], syz);
                }
             }
-            sm.TB[j] = sx;
-            sm.TG[j] = syz;
+            sm.TB[jj] = sx;
+            sm.TG[jj] = syz;
          }
          __syncwarp();
          // contract qx -> r(a, b, c) and the epilogue
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
-            const int i = lane + 32 * m;
-            if (i >= ND) continue;
-            const int ia = i % D1, cb = i / D1;
+            const int ii = lane + 32 * m;
+            if (ii >= cnt * ND) continue;
+            const int j = ii / ND, i = ii % ND, ia = i % D1, cb = i / D1;
+            const double *TB = sm.TB + j * NT + cb * Q, *TG = sm.TG + j * NT + cb * Q;
             double r = 0.0;
 #pragma unroll
             for (int x = 0; x < Q; x++) {
                if (KIND == TFEM_MASS) {
-                  r = fma(sB[x][ia], sm.TB[cb * Q + x], r);
+                  r = fma(sB[x][ia], TB[x], r);
                } else {
-                  r = fma(sG[x][ia], sm.TB[cb * Q + x], r);
-                  r = fma(sB[x][ia], sm.TG[cb * Q + x], r);
+                  r = fma(sG[x][ia], TB[x], r);
+                  r = fma(sB[x][ia], TG[x], r);
                }
             }
+            const int64_t e = g * EPW + j;
             const uint32_t gg = gcur[m];
             if (is_exclusive(gg)) {
                const uint32_t d = gg & kDofMask;
@@ -268,7 +295,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                a.evec[e * ND + i] = r;
             }
          }
-         __syncwarp(); // TB / TG / P reused by the next element
+         __syncwarp(); // TB / TG / P reused by the next group
 #pragma unroll
          for (int m = 0; m < GPL; m++) gcur[m] = gnext[m];
       }
@@ -294,7 +321,9 @@ void launch(const ApplyArgs &a, cudaStream_t s, unsigned /*blocks*/)
       return true;
    }();
    (void)once;
-   const int64_t nblk = (a.ne + C::kW - 1) / C::kW;
+   constexpr int EPW = Warp3<P, Q, KIND>::EPW;
+   const int64_t groups = (a.ne + EPW - 1) / EPW;
+   const int64_t nblk = (groups + C::kW - 1) / C::kW;
    const unsigned grid = static_cast<unsigned>(nblk < g_sm3 ? nblk : g_sm3);
    if (a.energy_dot)
       apply3d_tma_kernel<P, Q, KIND, true><<<grid, C::kBlock, C::kSmem, s>>>(a);
@@ -309,7 +338,7 @@ KernelPick make()
    // bulk copies need 16-byte sizes and element strides
    if constexpr ((Warp3<P, Q, KIND>::NC * Q * Q * Q) % 2 == 0) {
       k.launch = launch<P, Q, KIND>;
-      k.elems_per_block = Cfg3<P, Q, KIND>::kW;
+      k.elems_per_block = Cfg3<P, Q, KIND>::kW * Warp3<P, Q, KIND>::EPW;
       k.threads = Cfg3<P, Q, KIND>::kBlock;
       k.persistent_blocks = g_sm3;
       k.energy_dot = true;
