@@ -218,7 +218,7 @@ KernelPick pick(const tfem_ctx *ctx, const tfem_pa *pa)
    }();
    const bool exact = pa->dim == 2 && ctx->numerics == TFEM_NUMERICS_REFERENCE;
    KernelPick k;
-   // TFEM_APPLY3D=grp selects the thread-group kernel for 3D (A/B).
+   // TFEM_APPLY3D=grp selects the thread-group kernel for 3D and 2D p >= 4 (A/B).
    static const bool use_tma3 = [] {
       const char *v = std::getenv("TFEM_APPLY3D");
       return !(v && std::string(v) == "grp");
@@ -227,6 +227,9 @@ KernelPick pick(const tfem_ctx *ctx, const tfem_pa *pa)
       k = use_tma ? pick_apply2d_tma(pa->p, pa->nq, pa->kind, exact, ctx->sm_count)
                   : pick_apply2d_reg(pa->p, pa->nq, pa->kind, exact);
    else if (pa->dim == 3 && use_tma3 && (k = pick_apply3d_tma(pa->p, pa->nq, pa->kind, ctx->sm_count)).launch)
+      ;
+   else if (pa->dim == 2 && use_tma3 &&
+            (k = pick_apply2d_hi(pa->p, pa->nq, pa->kind, exact, ctx->sm_count)).launch)
       ;
    else
       k = pick_apply_grp(pa->dim, pa->p, pa->nq, pa->kind, exact);

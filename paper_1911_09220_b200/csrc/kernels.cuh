@@ -50,6 +50,8 @@ KernelPick pick_apply2d_reg(int p, int nq, int kind, bool exact);
 // The same arithmetic fed by a cp.async.bulk / mbarrier qdata pipeline
 // (persistent blocks): 2D, p <= 3.
 KernelPick pick_apply2d_tma(int p, int nq, int kind, bool exact, int sm_count);
+// One element per warp with a bulk-copy qdata pipeline: 2D p >= 4.
+KernelPick pick_apply2d_hi(int p, int nq, int kind, bool exact, int sm_count);
 // One element per warp with a bulk-copy qdata pipeline: 3D, q^2 <= 32.
 KernelPick pick_apply3d_tma(int p, int nq, int kind, int sm_count);
 // Thread-group-per-element kernels through shared memory: 2D p >= 4, 3D.
