@@ -1,6 +1,7 @@
-// K2, 3D with Q^2 <= 32 (BP1 / BP3 p <= 3, BP5 p <= 4): one group of
-// EPW = 32 / Q^2 elements per warp (1 for Q = 5, 2 for Q = 4, 3 for Q = 3),
-// fed by a bulk-copy pipeline (cp.async.bulk + mbarrier, LDGSTS).
+// K2, 3D with q <= 7 (BP1 / BP3 p <= 5, BP5 p <= 5): one group of
+// EPW = max(1, 32 / Q^2) elements per warp (1 for Q >= 5, 2 for Q = 4, 3 for
+// Q = 3; for Q^2 > 32 a lane walks several (qx, qy) columns), fed by a
+// bulk-copy pipeline (cp.async.bulk + mbarrier, LDGSTS).
 //
 // Persistent block per SM: warps 0..kW-1 compute, warp kW is the producer.
 // Warp w of block b takes elements e = (b kW + w) + k (grid kW), k = 0, 1, ..
@@ -112,9 +113,6 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    } else {
       // ---------------------------------------------------------- consumer
       W &sm = ws[warp];
-      // column stage: lane -> (element ej, qx, qy)
-      const int ej = lane / (Q * Q), col = lane % (Q * Q);
-      const int qx = col % Q, qy = col / Q;
       uint32_t gcur[GPL], gnext[GPL];
       auto load_map = [&](int64_t g, uint32_t (&m_)[GPL]) {
          const int64_t lim = (int64_t)count(g) * ND;
@@ -171,7 +169,10 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          __syncwarp();
          const int s = static_cast<int>(k % kSlots);
          mbar_wait(&sm.full[s], static_cast<unsigned>((k / kSlots) & 1));
-         if (ej < EPW) {
+         // column stage: (element ej, qx, qy) columns over the lanes
+         for (int cl = lane; cl < EPW * Q * Q; cl += 32) {
+            const int ej = cl / (Q * Q), col = cl % (Q * Q);
+            const int qx = col % Q, qy = col / Q;
             const bool live = ej < cnt;
             const double *TB = sm.TB + ej * NT, *TG = sm.TG + ej * NT;
             double UBB[D1], UBG[D1], UGB[D1];
@@ -349,12 +350,13 @@ KernelPick make()
 template <int KIND>
 KernelPick pick_kind(int p, int nq)
 {
-   // Q^2 <= 32: one (qx, qy) column per lane
+   // up to Q = 7; larger Q leaves too few warps per SM (the group kernel)
    switch (p) {
    case 1: return nq == 3 ? make<1, 3, KIND>() : nq == 2 ? make<1, 2, KIND>() : KernelPick{};
    case 2: return nq == 4 ? make<2, 4, KIND>() : nq == 3 ? make<2, 3, KIND>() : KernelPick{};
    case 3: return nq == 5 ? make<3, 5, KIND>() : nq == 4 ? make<3, 4, KIND>() : KernelPick{};
-   case 4: return nq == 5 ? make<4, 5, KIND>() : KernelPick{};
+   case 4: return nq == 5 ? make<4, 5, KIND>() : nq == 6 ? make<4, 6, KIND>() : KernelPick{};
+   case 5: return nq == 6 ? make<5, 6, KIND>() : nq == 7 ? make<5, 7, KIND>() : KernelPick{};
    }
    return {};
 }
