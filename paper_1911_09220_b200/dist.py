@@ -237,6 +237,8 @@ def bench_distributed(args, rank: int, world: int, local: int):
     import torch.distributed as tdist
     import paper_1911_09220_b200 as tf
 
+    if getattr(args, "bp", 3) != 3:
+        raise SystemExit("bench: the distributed run is BP3 (diffusion, Jacobi) only")
     # Test-only knobs (one-GPU boxes): all ranks on device 0 over gloo.  The
     # production path is NCCL with one GPU per rank.
     if os.environ.get("TFEM_DIST_SAME_DEVICE") == "1":
@@ -312,7 +314,11 @@ def bench_distributed(args, rank: int, world: int, local: int):
     if rank == 0:
         from bench import METRIC, config_of, peaks
         peak, _ = peaks()
-        b_it = 185.7 if args.dim == 2 else 340.5
+        # algorithmic bytes per DOF-iteration of BP3, this rank's slab
+        nc, nq = (3 if args.dim == 2 else 6), args.order + 2
+        E = d.space.n_elements
+        b_op = E * (nc * nq ** args.dim * 8 + (args.order + 1) ** args.dim * 4) + 16 * N_local
+        b_it = (b_op + 96 * N_local) / N_local
         line = {
             "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
