@@ -218,6 +218,14 @@ int tfem_prolongation_local_to_true(tfem_ctx *ctx, const tfem_prolongation *P,
 int tfem_pa_diagonal_p(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r,
                        const tfem_prolongation *P, tfem_vec *diag_true);
 
+/* ----------------------------------------------------------- linear form */
+/* LinearForm(space, f) (forms.cpp:400-431), 2D: b = G^T B^T (w detJ f) with
+ * q = p + 2 Gauss-Legendre points; f_host[e][qy * nq + qx] holds f at the
+ * physical points tfem_geometry_points(nq, TFEM_GAUSS_LEGENDRE) returns.
+ * b is overwritten (L-vector of the restriction). */
+int tfem_linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
+                     const double *f_host, tfem_vec *b);
+
 /* ------------------------------------------------------------- operator */
 /* BilinearForm::mult_true (forms.cpp:527-543) over n_pa integrators applied
  * in insertion order; with n_ess > 0 the ConstrainedOperator of

@@ -108,6 +108,8 @@ class Ref:
                                                             C.POINTER(C.c_longlong)]
             L.ref_cg_csr.argtypes = [C.c_int, _ip, _ip, _dp, _dp, C.c_double, C.c_int, _dp,
                                      _dp, _ip, _ip]
+            L.ref_linear_form.argtypes = [C.c_void_p, C.c_int, _dp]
+            L.ref_solution_f.argtypes = [C.c_int, _dp, C.c_int, _dp]
             L.ref_gauss_legendre.argtypes = [C.c_int, _dp, _dp]
             L.ref_gauss_lobatto.argtypes = [C.c_int, _dp, _dp]
             L.ref_eval_matrices.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp]
@@ -192,6 +194,11 @@ class RefSpace:
         Ref.check(Ref.lib().ref_space_prolongation(self.h, _i(rp), _i(cols), _d(vals),
                                                    C.byref(nnz)))
         return rp, cols, vals
+
+    def linear_form(self, solution="front"):
+        out = np.zeros(self.n_dofs)
+        Ref.check(Ref.lib().ref_linear_form(self.h, 0 if solution == "sine" else 1, _d(out)))
+        return out
 
     def element_vertices(self):
         out = np.zeros((self.n_elem, 4, 2))
@@ -320,6 +327,15 @@ class RefSystem:
         Ref.check(Ref.lib().ref_system_l2_error(self.h, _d(np.ascontiguousarray(x_cg)),
                                                 C.byref(e)))
         return e.value
+
+
+def ref_solution_f(solution, xy):
+    """The reference's manufactured source f (driver.cpp) at points xy[..., 2]."""
+    pts = np.ascontiguousarray(xy, dtype=np.float64)
+    out = np.zeros(pts.shape[:-1])
+    Ref.check(Ref.lib().ref_solution_f(0 if solution == "sine" else 1, _d(pts),
+                                       int(np.prod(pts.shape[:-1])), _d(out)))
+    return out
 
 
 def ref_cg_csr(rowptr, cols, vals, b, tol, max_iters, diag=None):

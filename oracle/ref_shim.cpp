@@ -524,6 +524,29 @@ int ref_system_l2_error(void *sp, const double *x_cg, double *err)
    });
 }
 
+// LinearForm(space, f) (forms.cpp:400-431) for the manufactured source of
+// `solution` (0 sine, 1 front): the L-vector b.
+int ref_linear_form(void *sp, int solution, double *out)
+{
+   return guarded([&] {
+      const FeSpace &space = *static_cast<Space *>(sp)->fes;
+      const ManufacturedSolution sol =
+         manufactured_solution(solution == 0 ? SolutionId::Sine : SolutionId::Front);
+      const LinearForm b(space, sol.f);
+      for (int i = 0; i < b.values().size(); i++) out[i] = b.values()[i];
+   });
+}
+
+// The manufactured source f of `solution` at n points xy[2n].
+int ref_solution_f(int solution, const double *xy, int n, double *out)
+{
+   return guarded([&] {
+      const ManufacturedSolution sol =
+         manufactured_solution(solution == 0 ? SolutionId::Sine : SolutionId::Front);
+      for (int i = 0; i < n; i++) out[i] = sol.f(Vec2{xy[2 * i], xy[2 * i + 1]});
+   });
+}
+
 // Whole reference driver (driver.cpp:187-194) for table-level parity.
 int ref_solve_poisson(int n, int p, int solution, int jacobi, double tol,
                       int max_iters, int threads, int *iters, int *converged,

@@ -11,14 +11,15 @@ Layers:
 from .abi import (CudaError, InvalidArgument, LogicError, TfemError, TfemRuntimeError, lib,
                   SO_PATH)
 from .tensorfem import (DIFFUSION, MASS, BilinearForm, CgResult, ConstrainedOperator, Device,
-                        FeSpace, LinearOperator, PaData, SparseOperator, Vector, cg_solve,
+                        FeSpace, LinearForm, LinearOperator, PaData, SparseOperator, Vector,
+                        cg_solve,
                         cg_solve_host, count_multiplies, default_device, multiply_count,
                         pa_apply, pa_apply_local, pa_diagonal, pa_setup, reset_multiply_count)
 
 __all__ = [
     "CudaError", "InvalidArgument", "LogicError", "TfemError", "TfemRuntimeError", "lib",
     "SO_PATH", "DIFFUSION", "MASS", "BilinearForm", "CgResult", "ConstrainedOperator",
-    "Device", "FeSpace", "LinearOperator", "PaData", "SparseOperator", "Vector", "cg_solve",
+    "Device", "FeSpace", "LinearForm", "LinearOperator", "PaData", "SparseOperator", "Vector", "cg_solve",
     "cg_solve_host", "count_multiplies", "default_device", "multiply_count", "pa_apply",
     "pa_apply_local", "pa_diagonal", "pa_setup", "reset_multiply_count",
 ]

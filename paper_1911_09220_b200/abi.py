@@ -124,6 +124,7 @@ _PROTOS = {
     "tfem_pa_basis": (C.c_int, [vp, dp, dp]),
     "tfem_pa_apply_local": (C.c_int, [vp, vp, vp, vp, vp]),
     "tfem_pa_diagonal": (C.c_int, [vp, vp, vp, vp]),
+    "tfem_linear_form": (C.c_int, [vp, vp, vp, C.c_int, dp, vp]),
     "tfem_pa_diagonal_p": (C.c_int, [vp, vp, vp, vp, vp]),
     "tfem_prolongation_create": (C.c_int, [vp, i64, i64, i32p, i32p, dp, i32p, C.POINTER(vp)]),
     "tfem_prolongation_destroy": (C.c_int, [vp]),

@@ -563,6 +563,19 @@ int tfem_operator_create_p(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa,
    });
 }
 
+int tfem_linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
+                     const double *f_host, tfem_vec *b)
+{
+   return guard([&] {
+      need(ctx, "LinearForm");
+      need(g, "LinearForm");
+      need(r, "LinearForm");
+      need(f_host, "LinearForm: load function is empty");
+      if (!b || b->n != r->ndofs) invalid("LinearForm: size mismatch");
+      linear_form(ctx, g, r, p, f_host, b->d);
+   });
+}
+
 // ------------------------------------------------------------ prolongation
 int tfem_prolongation_create(tfem_ctx *ctx, int64_t n_local, int64_t n_true, const int32_t *rowptr,
                              const int32_t *cols, const double *vals, const int32_t *true_index,

@@ -334,6 +334,8 @@ void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, do
 tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq, int rule,
                   const double *coeff_host, double coeff_const, int64_t *bad_elem);
 void geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq, int rule, double *host_xyz);
+void linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
+                 const double *f_host, double *b);
 
 // Prolongation (prolong.cu)
 void prolongation_mult(tfem_ctx *ctx, const tfem_prolongation *P, const double *x_true,

@@ -208,6 +208,42 @@ __global__ void points_kernel(GeoSource g, GeoTables t, double *xyz /* [e][q][di
    for (int r = 0; r < DIM; r++) xyz[idx * DIM + r] = X[r];
 }
 
+// LinearForm (forms.cpp:400-431), 2D: per element q(qx, qy) =
+// ((w_x w_y) detJ) f at the Gauss points, then tensor_interp_2d_transpose =
+// mat_mult(mat_mult_tn(B, q), B) (tensor_kernels.cpp:18-65, 89-97) -- every
+// sum from 0.0 in ascending index -- into the element vector [e][b D1 + a].
+struct Basis1D {
+   double B[kMaxQ][kMaxP + 1];
+};
+
+__global__ void linear_form_kernel(GeoSource g, GeoTables t, Basis1D bt, int p, const double *f,
+                                   double *evec)
+{
+   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (e >= g.ne) return;
+   const int nq = t.npts, nd = p + 1;
+   double q[kMaxQ][kMaxQ]; // q[qx][qy]
+   for (int qy = 0; qy < nq; qy++)
+      for (int qx = 0; qx < nq; qx++) {
+         double J[3][3];
+         jacobian<2>(g, t, e, qx, qy, 0, J);
+         const double det = det_of<2>(J);
+         q[qx][qy] = M(M(M(t.w[qx], t.w[qy]), det), f[e * nq * nq + qy * nq + qx]);
+      }
+   double T[kMaxP + 1][kMaxQ]; // mat_mult_tn(B, q): k (= qx) outermost
+   for (int a = 0; a < nd; a++)
+      for (int qy = 0; qy < nq; qy++) T[a][qy] = 0.0;
+   for (int k = 0; k < nq; k++)
+      for (int a = 0; a < nd; a++)
+         for (int qy = 0; qy < nq; qy++) T[a][qy] = A(T[a][qy], M(bt.B[k][a], q[k][qy]));
+   for (int a = 0; a < nd; a++)
+      for (int b = 0; b < nd; b++) {
+         double s = 0.0; // mat_mult: k (= qy) ascending
+         for (int k = 0; k < nq; k++) s = A(s, M(T[a][k], bt.B[k][b]));
+         evec[e * nd * nd + b * nd + a] = s;
+      }
+}
+
 GeoTables tables_at(int m, const std::vector<double> &pts, const std::vector<double> *w)
 {
    GeoTables t{};
@@ -342,6 +378,40 @@ void geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq, int rule, do
    TFEM_CUDA(cudaMemcpyAsync(host_xyz, d, bytes, cudaMemcpyDeviceToHost, ctx->stream));
    TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
    cudaFree(d);
+}
+
+void linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
+                 const double *f_host, double *b)
+{
+   if (g->dim != 2 || r->dim != 2) invalid("LinearForm: 2D spaces (forms.cpp:400-431)");
+   if (r->p != p || r->ne != g->ne) invalid("LinearForm: geometry / space mismatch");
+   if (p < 1 || p > kMaxP || p + 2 > kMaxQ) invalid("LinearForm: order must be in [1, 8]");
+   const int nq = p + 2, nd = p + 1;
+   std::vector<double> w;
+   const std::vector<double> pts = gauss_points(TFEM_GAUSS_LEGENDRE, nq, &w);
+   const GeoTables t = tables_at(g->order, pts, &w);
+   Basis1D bt{};
+   std::vector<double> B(static_cast<size_t>(nq) * nd), G(B.size());
+   eval_matrices(p, TFEM_NODES_GAUSS_LOBATTO, nq, TFEM_GAUSS_LEGENDRE, B.data(), G.data());
+   for (int q = 0; q < nq; q++)
+      for (int i = 0; i < nd; i++) bt.B[q][i] = B[q * nd + i];
+   const GeoSource src = source_of(g);
+   const int64_t ne = g->ne;
+   double *d_f = nullptr, *d_e = nullptr;
+   TFEM_CUDA(cudaMalloc(&d_f, sizeof(double) * static_cast<size_t>(ne) * nq * nq));
+   TFEM_CUDA(cudaMalloc(&d_e, sizeof(double) * static_cast<size_t>(ne) * nd * nd));
+   TFEM_CUDA(cudaMemcpyAsync(d_f, f_host, sizeof(double) * static_cast<size_t>(ne) * nq * nq,
+                             cudaMemcpyHostToDevice, ctx->stream));
+   const int T = 128;
+   linear_form_kernel<<<blocks_for(ne, T), T, 0, ctx->stream>>>(src, t, bt, p, d_f, d_e);
+   ctx->launched();
+   TFEM_CUDA(cudaGetLastError());
+   // b = 0, then b[dofs[b D1 + a]] += bl(a, b) in element order (forms.cpp:424-428)
+   vec_fill(ctx, b, r->ndofs, 0.0);
+   restriction_mult_transpose(ctx, r, d_e, b);
+   TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   cudaFree(d_f);
+   cudaFree(d_e);
 }
 
 } // namespace tfem

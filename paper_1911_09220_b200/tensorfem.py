@@ -488,6 +488,29 @@ def pa_diagonal(pa: PaData, space: FeSpace) -> Vector:
     return d
 
 
+class LinearForm:
+    """LinearForm(space, f) (forms.cpp:400-431): b_i = sum_q w detJ f(x_q)
+    phi_i(x_q), q = p + 2 Gauss-Legendre points, f evaluated on the host at
+    the device-computed physical points, contraction and element-ordered
+    scatter on the device (bit-identical to the reference)."""
+
+    def __init__(self, space: FeSpace, f: Coefficient):
+        if f is None:
+            raise InvalidArgument("LinearForm: load function is empty")
+        self.space = space
+        nq = space.order() + 2
+        arr, const = _coeff_values(space, f, nq, "gauss_legendre")
+        if arr is None:
+            arr = np.full((space.n_elements, nq * nq), const)
+        vals = np.ascontiguousarray(arr, dtype=np.float64)
+        self._b = Vector(space.dev, space.n_dofs)
+        check(lib().tfem_linear_form(space.dev.h, space.g, space.r, space.order(), _dptr(vals),
+                                     self._b.h))
+
+    def values(self) -> Vector:
+        return self._b
+
+
 # --------------------------------------------------------------- operators
 class LinearOperator:
     """The virtual mult seam cg_solve drives (solvers.hpp:16-23)."""
