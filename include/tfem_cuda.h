@@ -226,6 +226,19 @@ int tfem_pa_diagonal_p(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction 
 int tfem_linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
                      const double *f_host, tfem_vec *b);
 
+/* project_coefficient (fespace.cpp:334-356), 2D H1: the physical points of
+ * every element's basis nodes, host_xy[e][b * (p+1) + a][2]; the caller
+ * evaluates f there and tfem_project assigns out[dofs[i]] = f_nodes[e][i]
+ * with the last element winning on shared DOFs (the reference's loop). */
+int tfem_geometry_node_points(tfem_ctx *ctx, const tfem_geometry *g, int p, double *host_xy);
+int tfem_project(tfem_ctx *ctx, const tfem_restriction *r, const double *f_nodes,
+                 tfem_vec *out);
+/* compute_l2_error (fespace.cpp:358-394), 2D H1, q = p + 3 Gauss-Legendre:
+ * u_exact_host[e][qy * nq + qx] at tfem_geometry_points(p + 3, GL).  Per-point
+ * terms on the device, the reference's sequential sum on the host. */
+int tfem_l2_error(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
+                  const tfem_vec *x, const double *u_exact_host, double *err);
+
 /* ------------------------------------------------------------- operator */
 /* BilinearForm::mult_true (forms.cpp:527-543) over n_pa integrators applied
  * in insertion order; with n_ess > 0 the ConstrainedOperator of

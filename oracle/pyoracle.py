@@ -109,6 +109,9 @@ class Ref:
             L.ref_cg_csr.argtypes = [C.c_int, _ip, _ip, _dp, _dp, C.c_double, C.c_int, _dp,
                                      _dp, _ip, _ip]
             L.ref_linear_form.argtypes = [C.c_void_p, C.c_int, _dp]
+            L.ref_project.argtypes = [C.c_void_p, C.c_int, _dp]
+            L.ref_l2_error.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+            L.ref_solution_u.argtypes = [C.c_int, _dp, C.c_int, _dp]
             L.ref_solution_f.argtypes = [C.c_int, _dp, C.c_int, _dp]
             L.ref_gauss_legendre.argtypes = [C.c_int, _dp, _dp]
             L.ref_gauss_lobatto.argtypes = [C.c_int, _dp, _dp]
@@ -199,6 +202,18 @@ class RefSpace:
         out = np.zeros(self.n_dofs)
         Ref.check(Ref.lib().ref_linear_form(self.h, 0 if solution == "sine" else 1, _d(out)))
         return out
+
+    def project(self, solution="front"):
+        out = np.zeros(self.n_dofs)
+        Ref.check(Ref.lib().ref_project(self.h, 0 if solution == "sine" else 1, _d(out)))
+        return out
+
+    def l2_error(self, x, solution="front"):
+        err = C.c_double()
+        Ref.check(Ref.lib().ref_l2_error(self.h, 0 if solution == "sine" else 1,
+                                         _d(np.ascontiguousarray(x, dtype=np.float64)),
+                                         C.byref(err)))
+        return err.value
 
     def element_vertices(self):
         out = np.zeros((self.n_elem, 4, 2))
@@ -327,6 +342,15 @@ class RefSystem:
         Ref.check(Ref.lib().ref_system_l2_error(self.h, _d(np.ascontiguousarray(x_cg)),
                                                 C.byref(e)))
         return e.value
+
+
+def ref_solution_u(solution, xy):
+    """The reference's manufactured solution u (driver.cpp) at points xy[..., 2]."""
+    pts = np.ascontiguousarray(xy, dtype=np.float64)
+    out = np.zeros(pts.shape[:-1])
+    Ref.check(Ref.lib().ref_solution_u(0 if solution == "sine" else 1, _d(pts),
+                                       int(np.prod(pts.shape[:-1])), _d(out)))
+    return out
 
 
 def ref_solution_f(solution, xy):

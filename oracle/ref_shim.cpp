@@ -537,6 +537,41 @@ int ref_linear_form(void *sp, int solution, double *out)
    });
 }
 
+// project_coefficient(space, u) of the manufactured solution, L-vector.
+int ref_project(void *sp, int solution, double *out)
+{
+   return guarded([&] {
+      const FeSpace &space = *static_cast<Space *>(sp)->fes;
+      const ManufacturedSolution sol =
+         manufactured_solution(solution == 0 ? SolutionId::Sine : SolutionId::Front);
+      const GridFunction g = project_coefficient(space, sol.u);
+      for (int i = 0; i < g.values().size(); i++) out[i] = g.values()[i];
+   });
+}
+
+// compute_l2_error of the L-vector x against the manufactured solution.
+int ref_l2_error(void *sp, int solution, const double *x, double *err)
+{
+   return guarded([&] {
+      const FeSpace &space = *static_cast<Space *>(sp)->fes;
+      const ManufacturedSolution sol =
+         manufactured_solution(solution == 0 ? SolutionId::Sine : SolutionId::Front);
+      GridFunction g(space);
+      for (int i = 0; i < g.values().size(); i++) g.values()[i] = x[i];
+      *err = compute_l2_error(g, sol.u);
+   });
+}
+
+// The manufactured solution u of `solution` at n points xy[2n].
+int ref_solution_u(int solution, const double *xy, int n, double *out)
+{
+   return guarded([&] {
+      const ManufacturedSolution sol =
+         manufactured_solution(solution == 0 ? SolutionId::Sine : SolutionId::Front);
+      for (int i = 0; i < n; i++) out[i] = sol.u(Vec2{xy[2 * i], xy[2 * i + 1]});
+   });
+}
+
 // The manufactured source f of `solution` at n points xy[2n].
 int ref_solution_f(int solution, const double *xy, int n, double *out)
 {

@@ -13,13 +13,14 @@ from .abi import (CudaError, InvalidArgument, LogicError, TfemError, TfemRuntime
 from .tensorfem import (DIFFUSION, MASS, BilinearForm, CgResult, ConstrainedOperator, Device,
                         FeSpace, LinearForm, LinearOperator, PaData, SparseOperator, Vector,
                         cg_solve,
-                        cg_solve_host, count_multiplies, default_device, multiply_count,
+                        cg_solve_host, compute_l2_error, count_multiplies, default_device,
+                        multiply_count, project_coefficient,
                         pa_apply, pa_apply_local, pa_diagonal, pa_setup, reset_multiply_count)
 
 __all__ = [
     "CudaError", "InvalidArgument", "LogicError", "TfemError", "TfemRuntimeError", "lib",
     "SO_PATH", "DIFFUSION", "MASS", "BilinearForm", "CgResult", "ConstrainedOperator",
     "Device", "FeSpace", "LinearForm", "LinearOperator", "PaData", "SparseOperator", "Vector", "cg_solve",
-    "cg_solve_host", "count_multiplies", "default_device", "multiply_count", "pa_apply",
+    "cg_solve_host", "compute_l2_error", "project_coefficient", "count_multiplies", "default_device", "multiply_count", "pa_apply",
     "pa_apply_local", "pa_diagonal", "pa_setup", "reset_multiply_count",
 ]

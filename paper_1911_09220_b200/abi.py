@@ -125,6 +125,9 @@ _PROTOS = {
     "tfem_pa_apply_local": (C.c_int, [vp, vp, vp, vp, vp]),
     "tfem_pa_diagonal": (C.c_int, [vp, vp, vp, vp]),
     "tfem_linear_form": (C.c_int, [vp, vp, vp, C.c_int, dp, vp]),
+    "tfem_geometry_node_points": (C.c_int, [vp, vp, C.c_int, dp]),
+    "tfem_project": (C.c_int, [vp, vp, dp, vp]),
+    "tfem_l2_error": (C.c_int, [vp, vp, vp, C.c_int, vp, dp, dp]),
     "tfem_pa_diagonal_p": (C.c_int, [vp, vp, vp, vp, vp]),
     "tfem_prolongation_create": (C.c_int, [vp, i64, i64, i32p, i32p, dp, i32p, C.POINTER(vp)]),
     "tfem_prolongation_destroy": (C.c_int, [vp]),

@@ -576,6 +576,47 @@ int tfem_linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restricti
    });
 }
 
+int tfem_geometry_node_points(tfem_ctx *ctx, const tfem_geometry *g, int p, double *host_xy)
+{
+   return guard([&] {
+      need(ctx, "project_coefficient");
+      need(g, "project_coefficient");
+      need(host_xy, "project_coefficient");
+      geometry_node_points(ctx, g, p, host_xy);
+   });
+}
+
+int tfem_project(tfem_ctx *ctx, const tfem_restriction *r, const double *f_nodes, tfem_vec *out)
+{
+   return guard([&] {
+      need(ctx, "project_coefficient");
+      need(r, "project_coefficient");
+      need(f_nodes, "project_coefficient: function is empty");
+      if (!out || out->n != r->ndofs) invalid("project_coefficient: size mismatch");
+      double *e = nullptr;
+      const size_t bytes = sizeof(double) * static_cast<size_t>(r->ne) * r->nd;
+      TFEM_CUDA(cudaMalloc(&e, bytes));
+      h2d(ctx->stream, e, f_nodes, bytes);
+      restriction_assign_last(ctx, r, e, out->d);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(e);
+   });
+}
+
+int tfem_l2_error(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
+                  const tfem_vec *x, const double *u_exact_host, double *err)
+{
+   return guard([&] {
+      need(ctx, "compute_l2_error");
+      need(g, "compute_l2_error");
+      need(r, "compute_l2_error");
+      need(u_exact_host, "compute_l2_error: exact solution is empty");
+      need(err, "compute_l2_error");
+      if (!x || x->n != r->ndofs) invalid("compute_l2_error: size mismatch");
+      *err = l2_error(ctx, g, r, p, x->d, u_exact_host);
+   });
+}
+
 // ------------------------------------------------------------ prolongation
 int tfem_prolongation_create(tfem_ctx *ctx, int64_t n_local, int64_t n_true, const int32_t *rowptr,
                              const int32_t *cols, const double *vals, const int32_t *true_index,

@@ -336,6 +336,10 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
 void geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq, int rule, double *host_xyz);
 void linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
                  const double *f_host, double *b);
+void geometry_node_points(tfem_ctx *ctx, const tfem_geometry *g, int p, double *host_xy);
+double l2_error(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
+                const double *x, const double *u_exact_host);
+void restriction_assign_last(tfem_ctx *ctx, const tfem_restriction *r, const double *e, double *l);
 
 // Prolongation (prolong.cu)
 void prolongation_mult(tfem_ctx *ctx, const tfem_prolongation *P, const double *x_true,

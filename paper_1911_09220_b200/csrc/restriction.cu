@@ -255,6 +255,25 @@ __global__ void to_internal_kernel(Layout L, const double *api, double *evec)
    evec[L.slot_e(static_cast<int>(t % L.nd), t / L.nd)] = api[t];
 }
 
+// project_coefficient's `g.values()[dofs[...]] = v` (fespace.cpp:334-356):
+// every DOF takes the value of its last element.  Exclusive slots directly,
+// shared DOFs from the last slot of their (element-sorted) bucket row.
+__global__ void assign_exclusive_kernel(const uint32_t *gmap, Layout L,
+                                        const double *evec /* [e][i] */, double *l)
+{
+   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (t >= L.ne * L.nd) return;
+   const uint32_t g = gmap[L.slot_e(static_cast<int>(t % L.nd), t / L.nd)];
+   if (is_exclusive(g)) l[g & kDofMask] = evec[t];
+}
+
+__global__ void assign_last_kernel(const int32_t *dofs, const uint32_t *slots, int64_t n, int c,
+                                   const double *evec_internal, double *l)
+{
+   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (k < n) l[dofs[k]] = evec_internal[slots[k * c + c - 1]];
+}
+
 // Boundary of a Cartesian mesh: DOFs at lattice positions on the domain
 // boundary (the set essential_true_dofs collects over all attributes).
 __global__ void boundary_mark_kernel(const uint32_t *gmap, Layout L, int dim, int nx, int ny,
@@ -630,6 +649,27 @@ void restriction_mult(tfem_ctx *ctx, const tfem_restriction *r, const double *l,
    TFEM_CUDA(cudaGetLastError());
 }
 
+void restriction_assign_last(tfem_ctx *ctx, const tfem_restriction *r, const double *e,
+                             double *l)
+{
+   const int64_t nslots = r->ne * r->nd;
+   const Layout L{r->elem_major, r->nd, r->ne, r->ne_pad, r->order};
+   assign_exclusive_kernel<<<blocks_for(nslots), kThreads, 0, ctx->stream>>>(r->gmap, L, e, l);
+   ctx->launched();
+   if (r->n_shared > 0) {
+      double *ev = const_cast<tfem_restriction *>(r)->ensure_evec();
+      to_internal_kernel<<<blocks_for(nslots), kThreads, 0, ctx->stream>>>(L, e, ev);
+      ctx->launched();
+      for (int b = 0; b < r->n_buckets; b++) {
+         const auto &bk = r->buckets[b];
+         assign_last_kernel<<<blocks_for(bk.n), kThreads, 0, ctx->stream>>>(bk.dofs, bk.slots,
+                                                                          bk.n, bk.c, ev, l);
+         ctx->launched();
+      }
+   }
+   TFEM_CUDA(cudaGetLastError());
+}
+
 } // namespace tfem
 
 double *tfem_restriction::ensure_evec()
@@ -637,4 +677,3 @@ double *tfem_restriction::ensure_evec()
    if (!evec) TFEM_CUDA(cudaMalloc(&evec, sizeof(double) * static_cast<size_t>(nd) * ne_pad));
    return evec;
 }
-

@@ -244,6 +244,32 @@ __global__ void linear_form_kernel(GeoSource g, GeoTables t, Basis1D bt, int p, 
       }
 }
 
+// compute_l2_error's per-point terms (fespace.cpp:358-394), 2D: u_h at the
+// point from the element values [e][b D1 + a] (s over a, then u over b, each
+// from 0.0), det J, d = u_h - u_exact, term ((((w_x w_y) det) d) d).
+__global__ void l2_terms_kernel(GeoSource g, GeoTables t, Basis1D bt, int p, const double *ev,
+                                const double *uex, double *terms)
+{
+   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (e >= g.ne) return;
+   const int nq = t.npts, nd = p + 1;
+   for (int qy = 0; qy < nq; qy++)
+      for (int qx = 0; qx < nq; qx++) {
+         double u = 0.0;
+         for (int b = 0; b < nd; b++) {
+            double s = 0.0;
+            for (int a = 0; a < nd; a++) s = A(s, M(bt.B[qx][a], ev[e * nd * nd + b * nd + a]));
+            u = A(u, M(bt.B[qy][b], s));
+         }
+         double J[3][3];
+         jacobian<2>(g, t, e, qx, qy, 0, J);
+         const double det = det_of<2>(J);
+         const int64_t q = e * nq * nq + qy * nq + qx;
+         const double d = S(u, uex[q]);
+         terms[q] = M(M(M(M(t.w[qx], t.w[qy]), det), d), d);
+      }
+}
+
 GeoTables tables_at(int m, const std::vector<double> &pts, const std::vector<double> *w)
 {
    GeoTables t{};
@@ -412,6 +438,74 @@ void linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *
    TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
    cudaFree(d_f);
    cudaFree(d_e);
+}
+
+// ElementTransformation::point at the basis nodes (the GLL lattice),
+// [e][b D1 + a][2] (project_coefficient, fespace.cpp:334-356).
+void geometry_node_points(tfem_ctx *ctx, const tfem_geometry *g, int p, double *host_xy)
+{
+   if (g->dim != 2) invalid("project_coefficient: 2D spaces");
+   if (p < 1 || p > kMaxP) invalid("project_coefficient: order must be in [1, 8]");
+   std::vector<double> nodes, bary;
+   basis_nodes(p, TFEM_NODES_GAUSS_LOBATTO, nodes, bary);
+   const GeoTables t = tables_at(g->order, nodes, nullptr);
+   const GeoSource src = source_of(g);
+   const int nd = p + 1;
+   double *d = nullptr;
+   const size_t bytes = sizeof(double) * static_cast<size_t>(g->ne) * nd * nd * 2;
+   TFEM_CUDA(cudaMalloc(&d, bytes));
+   const int T = 256;
+   points_kernel<2><<<blocks_for(static_cast<int64_t>(nd) * nd * g->ne, T), T, 0, ctx->stream>>>(
+      src, t, d);
+   ctx->launched();
+   TFEM_CUDA(cudaGetLastError());
+   TFEM_CUDA(cudaMemcpyAsync(host_xy, d, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+   TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   cudaFree(d);
+}
+
+void restriction_mult(tfem_ctx *ctx, const tfem_restriction *r, const double *l, double *e);
+
+// compute_l2_error (fespace.cpp:358-394): per-point terms on the device, the
+// reference's sequential sum over elements and points on the host.
+double l2_error(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r, int p,
+                const double *x, const double *u_exact_host)
+{
+   if (g->dim != 2 || r->dim != 2) invalid("compute_l2_error: 2D spaces");
+   if (r->p != p || r->ne != g->ne) invalid("compute_l2_error: geometry / space mismatch");
+   const int nq = p + 3, nd = p + 1;
+   if (nq > kMaxQ) invalid("compute_l2_error: order must be <= 7 on the device");
+   std::vector<double> w;
+   const std::vector<double> pts = gauss_points(TFEM_GAUSS_LEGENDRE, nq, &w);
+   const GeoTables t = tables_at(g->order, pts, &w);
+   Basis1D bt{};
+   std::vector<double> B(static_cast<size_t>(nq) * nd), G(B.size());
+   eval_matrices(p, TFEM_NODES_GAUSS_LOBATTO, nq, TFEM_GAUSS_LEGENDRE, B.data(), G.data());
+   for (int q = 0; q < nq; q++)
+      for (int i = 0; i < nd; i++) bt.B[q][i] = B[q * nd + i];
+   const int64_t ne = g->ne, npts = ne * nq * nq;
+   double *ev = nullptr, *uex = nullptr, *terms = nullptr;
+   TFEM_CUDA(cudaMalloc(&ev, sizeof(double) * static_cast<size_t>(ne) * nd * nd));
+   TFEM_CUDA(cudaMalloc(&uex, sizeof(double) * static_cast<size_t>(npts)));
+   TFEM_CUDA(cudaMalloc(&terms, sizeof(double) * static_cast<size_t>(npts)));
+   restriction_mult(ctx, r, x, ev); // element values [e][b D1 + a]
+   TFEM_CUDA(cudaMemcpyAsync(uex, u_exact_host, sizeof(double) * npts, cudaMemcpyHostToDevice,
+                             ctx->stream));
+   const int T = 128;
+   l2_terms_kernel<<<blocks_for(ne, T), T, 0, ctx->stream>>>(source_of(g), t, bt, p, ev, uex,
+                                                            terms);
+   ctx->launched();
+   TFEM_CUDA(cudaGetLastError());
+   std::vector<double> h(static_cast<size_t>(npts));
+   TFEM_CUDA(cudaMemcpyAsync(h.data(), terms, sizeof(double) * npts, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+   TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   cudaFree(ev);
+   cudaFree(uex);
+   cudaFree(terms);
+   volatile double err2 = 0.0; // the reference's left-to-right sum
+   for (double v : h) err2 = err2 + v;
+   return std::sqrt(static_cast<double>(err2));
 }
 
 } // namespace tfem

@@ -511,6 +511,35 @@ class LinearForm:
         return self._b
 
 
+def project_coefficient(space: FeSpace, f: Callable[[np.ndarray], np.ndarray]) -> Vector:
+    """project_coefficient (fespace.cpp:334-356): nodal interpolation of f,
+    the last element winning on shared DOFs (L-vector)."""
+    if f is None:
+        raise InvalidArgument("project_coefficient: function is empty")
+    nd = space.order() + 1
+    xy = np.empty((space.n_elements, nd * nd, 2))
+    check(lib().tfem_geometry_node_points(space.dev.h, space.g, space.order(), _dptr(xy)))
+    vals = np.ascontiguousarray(np.broadcast_to(np.asarray(f(xy), dtype=np.float64),
+                                                xy.shape[:2]))
+    out = Vector(space.dev, space.n_dofs)
+    check(lib().tfem_project(space.dev.h, space.r, _dptr(vals), out.h))
+    return out
+
+
+def compute_l2_error(space: FeSpace, x, u_exact: Callable[[np.ndarray], np.ndarray]) -> float:
+    """compute_l2_error (fespace.cpp:358-394) of the L-vector x against
+    u_exact, q = p + 3 Gauss-Legendre points; bit-identical to the reference."""
+    xv = as_vector(space.dev, x)
+    nq = space.order() + 3
+    pts = space.physical_points(nq, "gauss_legendre")
+    ue = np.ascontiguousarray(np.broadcast_to(np.asarray(u_exact(pts), dtype=np.float64),
+                                              pts.shape[:2]))
+    err = C.c_double()
+    check(lib().tfem_l2_error(space.dev.h, space.g, space.r, space.order(), xv.h, _dptr(ue),
+                              C.byref(err)))
+    return err.value
+
+
 # --------------------------------------------------------------- operators
 class LinearOperator:
     """The virtual mult seam cg_solve drives (solvers.hpp:16-23)."""

@@ -45,3 +45,33 @@ def test_linear_form_errors(dev):
     sp2 = tf.FeSpace.cartesian(dev, (2, 2), 1)
     with pytest.raises(tf.InvalidArgument, match="empty"):
         tf.LinearForm(sp2, None)
+
+
+def spaces(dev, p):
+    """(reference space, device space) pairs: Cartesian, curved, forest."""
+    out = [(RefSpace.cartesian(5, 4, p, 2.0, 1.0),
+            tf.FeSpace.cartesian(dev, (5, 4), p, extents=(2.0, 1.0)))]
+    rs = RefSpace.curved(4, p)
+    out.append((rs, tf.FeSpace.from_mesh(dev, 2, p, rs.element_dofs(), rs.n_dofs,
+                                         rs.ctrl_points(), rs.geom_order)))
+    rs = RefSpace.random_forest(4, p, 6, 3)
+    rp, cols, vals = rs.prolongation()
+    out.append((rs, tf.FeSpace.from_mesh(dev, 2, p, rs.element_dofs(), rs.n_dofs,
+                                         rs.ctrl_points(), rs.geom_order,
+                                         prolongation=(rp, cols, vals, rs.true_index(),
+                                                       rs.n_true))))
+    return out
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5])
+@pytest.mark.parametrize("solution", ["front", "sine"])
+def test_project_and_l2_error_bitwise(dev, p, solution):
+    """project_coefficient and compute_l2_error (fespace.cpp:334-394)."""
+    from oracle.pyoracle import ref_solution_u
+    u = lambda pts: ref_solution_u(solution, pts)
+    for rs, sp in spaces(dev, p):
+        g = tf.project_coefficient(sp, u).numpy()
+        assert (g == rs.project(solution)).all()
+        assert tf.compute_l2_error(sp, g, u) == rs.l2_error(g, solution)
+        x = np.random.default_rng(p).uniform(-1, 1, rs.n_dofs)
+        assert tf.compute_l2_error(sp, x, u) == rs.l2_error(x, solution)
