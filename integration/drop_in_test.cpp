@@ -200,6 +200,61 @@ int main()
              detail);
    }
 
+   // The driver: the reference's solve_poisson /
+   // convergence_study / amr_loop next to the same loops with every numeric
+   // step on the device.  Rows: same DOF counts and stored reals, CG
+   // iterations equal (+-1 on forests), L2 errors to 1e-9.
+   auto compare_rows = [&](const char *name, const RunResult &r, const RunResult &d, int slack) {
+      bool ok = r.rows.size() == d.rows.size() && r.converged == d.converged;
+      double worst = 0.0;
+      for (size_t i = 0; ok && i < r.rows.size(); i++) {
+         const ConvergenceRow &a = r.rows[i], &b = d.rows[i];
+         ok = a.n_true_dofs == b.n_true_dofs && a.pa_stored_reals == b.pa_stored_reals &&
+              std::abs(a.cg_iterations - b.cg_iterations) <= slack && a.h == b.h;
+         const double rel = std::abs(a.l2_error - b.l2_error) / a.l2_error;
+         worst = std::max(worst, rel);
+         ok = ok && rel <= 1e-9;
+      }
+      char detail[160];
+      std::snprintf(detail, sizeof detail, "(%zu rows; last: ref %d / device %d iterations, "
+                    "l2 %.6e / %.6e; worst l2 rel diff %.1e)", r.rows.size(),
+                    r.rows.empty() ? 0 : r.rows.back().cg_iterations,
+                    d.rows.empty() ? 0 : d.rows.back().cg_iterations,
+                    r.rows.empty() ? 0.0 : r.rows.back().l2_error,
+                    d.rows.empty() ? 0.0 : d.rows.back().l2_error, worst);
+      report(name, ok, detail);
+   };
+   for (int p : {2, 3}) {
+      RunConfig c;
+      c.cartesian_n = 16;
+      c.order = p;
+      c.solution = SolutionId::Front;
+      char what[96];
+      std::snprintf(what, sizeof what, "driver solve_poisson front n=16 p=%d", p);
+      compare_rows(what, solve_poisson(c), b200::solve_poisson(dev, c), 0);
+   }
+   {
+      RunConfig c;
+      c.cartesian_n = 4;
+      c.order = 2;
+      c.solution = SolutionId::Sine;
+      c.convergence_levels = 4;
+      compare_rows("driver convergence_study sine n=4 p=2, 4 levels", convergence_study(c),
+                   b200::convergence_study(dev, c), 1);
+   }
+   {
+      RunConfig c;
+      c.cartesian_n = 4;
+      c.order = 2;
+      c.solution = SolutionId::Front;
+      c.amr.iters = 4;
+      c.amr.theta = 0.5;
+      compare_rows("driver amr_loop front n=4 p=2, 4 rounds", amr_loop(c), b200::amr_loop(dev, c),
+                   1);
+      c.amr.anisotropic = true;
+      compare_rows("driver amr_loop front anisotropic", amr_loop(c), b200::amr_loop(dev, c), 1);
+   }
+
    // Error mapping: the reference's exception classes come back.
    {
       const FeSpace space(make_cartesian(2, 2), FeCollection(FeFamily::H1, 1));

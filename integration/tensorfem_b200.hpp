@@ -17,12 +17,26 @@
 //   ConstrainedOperator                    tfem_operator_create_p(..., ess)
 //   FeSpace::prolongation() (NC forests)   tfem_prolongation_create
 //   cg_solve(op, b, tol, it, diag)         tfem_cg_solve (device loop)
+//   LinearForm(space, f)                   tfem_linear_form
+//   project_coefficient / compute_l2_error tfem_project / tfem_l2_error
+//   solve_on_space / convergence_study /   b200::solve_on_space & co. below:
+//   amr_loop (driver.cpp:129-258)          every numeric step on the device,
+//                                          forest refinement and marking on
+//                                          the host (reference code)
 #pragma once
 
+#include "tensorfem/driver.hpp"
 #include "tensorfem/forms.hpp"
+#include "tensorfem/mesh_io.hpp"
+#include "tensorfem/ncmesh.hpp"
 #include "tfem_cuda.h"
 
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
 #include <memory>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -249,6 +263,49 @@ private:
    tfem_operator *op_ = nullptr;
 };
 
+// ----------------------------------------------------------- rhs / post
+// Host values of a point function at device-computed physical points.
+inline std::vector<double> eval_at(const std::vector<double> &xy,
+                                   const std::function<double(Vec2)> &f)
+{
+   std::vector<double> v(xy.size() / 2);
+   for (size_t i = 0; i < v.size(); i++) v[i] = f(Vec2{xy[2 * i], xy[2 * i + 1]});
+   return v;
+}
+
+/// LinearForm(space, f) (forms.cpp:400-431) as a device L-vector.
+inline void linear_form(const DeviceSpace &s, const std::function<double(Vec2)> &f, DVec &b)
+{
+   const int p = s.space().collection().order(), nq = p + 2;
+   std::vector<double> xy(static_cast<size_t>(s.space().mesh().n_elements()) * nq * nq * 2);
+   check(tfem_geometry_points(s.device().get(), s.geometry(), nq, TFEM_GAUSS_LEGENDRE, xy.data()));
+   const std::vector<double> fv = eval_at(xy, f);
+   check(tfem_linear_form(s.device().get(), s.geometry(), s.restriction(), p, fv.data(), b.get()));
+}
+
+/// project_coefficient (fespace.cpp:334-356) as a device L-vector.
+inline void project(const DeviceSpace &s, const std::function<double(Vec2)> &f, DVec &g)
+{
+   const int p = s.space().collection().order(), nd = p + 1;
+   std::vector<double> xy(static_cast<size_t>(s.space().mesh().n_elements()) * nd * nd * 2);
+   check(tfem_geometry_node_points(s.device().get(), s.geometry(), p, xy.data()));
+   const std::vector<double> fv = eval_at(xy, f);
+   check(tfem_project(s.device().get(), s.restriction(), fv.data(), g.get()));
+}
+
+/// compute_l2_error (fespace.cpp:358-394) of a device L-vector.
+inline double l2_error(const DeviceSpace &s, const DVec &x, const std::function<double(Vec2)> &u)
+{
+   const int p = s.space().collection().order(), nq = p + 3;
+   std::vector<double> xy(static_cast<size_t>(s.space().mesh().n_elements()) * nq * nq * 2);
+   check(tfem_geometry_points(s.device().get(), s.geometry(), nq, TFEM_GAUSS_LEGENDRE, xy.data()));
+   const std::vector<double> uv = eval_at(xy, u);
+   double err = 0.0;
+   check(tfem_l2_error(s.device().get(), s.geometry(), s.restriction(), p, x.get(), uv.data(),
+                       &err));
+   return err;
+}
+
 /// cg_solve (solvers.cpp:11-97) with the whole loop on the device when the
 /// operator is a DeviceOperator.
 inline CgResult cg_solve(const DeviceOperator &a, const Vector &b, double rel_tol,
@@ -265,6 +322,181 @@ inline CgResult cg_solve(const DeviceOperator &a, const Vector &b, double rel_to
    res.iterations = r.iterations;
    res.converged = r.converged != 0;
    return res;
+}
+
+// ------------------------------------------------------------- driver
+// driver.cpp's file-local helpers (driver.cpp:28-67), restated.
+inline Mesh build_mesh(const RunConfig &c)
+{
+   return c.mesh_path.empty() ? make_cartesian(c.cartesian_n, c.cartesian_n)
+                              : load_native_file(c.mesh_path);
+}
+
+inline std::vector<int> boundary_attributes(const Mesh &mesh)
+{
+   std::set<int> attrs;
+   for (const BoundarySegment &s : mesh.boundary_segments()) attrs.insert(s.attribute);
+   if (attrs.empty()) throw std::runtime_error("driver: mesh has no boundary to constrain");
+   return {attrs.begin(), attrs.end()};
+}
+
+inline double max_diameter(const Mesh &mesh)
+{
+   double h = 0.0;
+   for (int k = 0; k < mesh.n_elements(); k++) h = std::max(h, mesh.element_diameter(k));
+   return h;
+}
+
+inline void fill_orders(std::vector<ConvergenceRow> &rows)
+{
+   for (size_t i = 1; i < rows.size(); i++) {
+      const double prev = rows[i - 1].l2_error, cur = rows[i].l2_error;
+      if (prev > 0.0 && cur > 0.0 && std::isfinite(prev) && std::isfinite(cur))
+         rows[i].order = std::log2(prev / cur);
+   }
+}
+
+/// solve_on_space (driver.cpp:129-185) on the device: PA assembly, the rhs,
+/// the projection of the boundary data, form_linear_system (forms.cpp:
+/// 591-630: P^T b - A x0, rhs[ess] = values[ess]), the Jacobi diagonal, CG,
+/// recover_fem_solution (P x) and the L2 error all run on the device; the
+/// driver's bookkeeping stays on the host.  Partial assembly only.
+inline RunResult solve_on_space(const Device &dev, std::shared_ptr<const FeSpace> space,
+                                const ManufacturedSolution &sol, const RunConfig &config)
+{
+   if (config.assembly != AssemblyMode::Partial)
+      throw std::invalid_argument("b200: the device driver runs partial assembly");
+   const FeSpace &fes = *space;
+   const int n = fes.n_true_dofs(), nl = fes.n_dofs();
+   DeviceSpace ds(dev, fes);
+   DevicePa pa(ds, IntegratorKind::Diffusion, [](Vec2) { return 1.0; });
+   DVec b(dev, nl);
+   linear_form(ds, sol.f, b);
+   const std::vector<int> ess = fes.essential_true_dofs(boundary_attributes(fes.mesh()));
+   DVec interp(dev, nl), values(dev, n);
+   project(ds, sol.u, interp);
+   if (ds.prolongation())
+      check(tfem_prolongation_local_to_true(dev.get(), ds.prolongation(), interp.get(), values.get()));
+   else
+      check(tfem_vec_axpy(dev.get(), 1.0, interp.get(), values.get()));
+   // form_linear_system: rhs = P^T b; x0 = values on ess; rhs -= A x0;
+   // rhs[ess] = values[ess] -- then the driver zeroes rhs[ess]
+   DVec rhs(dev, n);
+   if (ds.prolongation())
+      check(tfem_prolongation_mult_transpose(dev.get(), ds.prolongation(), b.get(), rhs.get()));
+   else
+      check(tfem_vec_axpy(dev.get(), 1.0, b.get(), rhs.get()));
+   Vector hval(n), x0(n);
+   values.download(hval);
+   for (int e : ess) x0[e] = hval[e];
+   if (!ess.empty()) {
+      const DeviceOperator a(ds, {&pa});
+      DVec dx0(dev, x0), ax(dev, n);
+      check(tfem_operator_mult(dev.get(), a.get(), dx0.get(), ax.get()));
+      check(tfem_vec_axpy(dev.get(), -1.0, ax.get(), rhs.get()));
+   }
+   Vector hrhs(n);
+   rhs.download(hrhs);
+   for (int e : ess) hrhs[e] = 0.0;
+   const DeviceOperator op(ds, {&pa}, ess);
+   Vector diag;
+   const Vector *precond = nullptr;
+   if (config.prec == Preconditioner::Jacobi) {
+      diag = op.diagonal(); // diagonal_true with diag[ess] = 1
+      precond = &diag;
+   }
+   const auto t0 = std::chrono::steady_clock::now();
+   const CgResult cg = b200::cg_solve(op, hrhs, config.tol, config.max_iters, precond);
+   const std::chrono::duration<double> elapsed = std::chrono::steady_clock::now() - t0;
+   Vector x = cg.x;
+   for (int i = 0; i < x.size(); i++) x[i] += x0[i];
+   // recover_fem_solution: u = P x
+   DVec dxt(dev, x), ul(dev, nl);
+   if (ds.prolongation())
+      check(tfem_prolongation_mult(dev.get(), ds.prolongation(), dxt.get(), ul.get()));
+   else
+      check(tfem_vec_axpy(dev.get(), 1.0, dxt.get(), ul.get()));
+   RunResult out;
+   out.space = space;
+   GridFunction g(fes);
+   ul.download(g.values());
+   out.converged = cg.converged;
+   ConvergenceRow row;
+   row.n_true_dofs = n;
+   row.h = max_diameter(fes.mesh());
+   row.l2_error = l2_error(ds, ul, sol.u);
+   row.order = std::numeric_limits<double>::quiet_NaN();
+   row.cg_iterations = cg.iterations;
+   row.solve_seconds = elapsed.count();
+   row.pa_stored_reals = pa.stored_reals();
+   out.rows.push_back(row);
+   out.u = std::move(g);
+   return out;
+}
+
+/// solve_poisson (driver.cpp:187-194) on the device.
+inline RunResult solve_poisson(const Device &dev, const RunConfig &config)
+{
+   validate(config);
+   const auto space =
+      std::make_shared<const FeSpace>(build_mesh(config), FeCollection(FeFamily::H1, config.order));
+   return solve_on_space(dev, space, manufactured_solution(config.solution), config);
+}
+
+/// convergence_study (driver.cpp:196-228): uniform forest refinement on the
+/// host, every level solved on the device.
+inline RunResult convergence_study(const Device &dev, const RunConfig &config)
+{
+   validate(config);
+   if (config.convergence_levels < 1)
+      throw std::invalid_argument("driver: study needs at least one level");
+   const ManufacturedSolution sol = manufactured_solution(config.solution);
+   const auto forest = std::make_shared<NcForest>(build_mesh(config));
+   RunResult out;
+   out.forest = forest;
+   for (int level = 0;; level++) {
+      const auto space = std::make_shared<const FeSpace>(*forest, FeCollection(FeFamily::H1, config.order));
+      RunResult solve = solve_on_space(dev, space, sol, config);
+      out.rows.push_back(solve.rows[0]);
+      out.converged = out.converged && solve.converged;
+      out.space = solve.space;
+      out.u = std::move(solve.u);
+      if (level == config.convergence_levels - 1 || !out.converged) break;
+      std::vector<std::pair<int, SplitKind>> marks;
+      marks.reserve(forest->n_leaves());
+      for (int leaf = 0; leaf < forest->n_leaves(); leaf++) marks.emplace_back(leaf, SplitKind::Iso);
+      forest->refine(marks);
+   }
+   fill_orders(out.rows);
+   return out;
+}
+
+/// amr_loop (driver.cpp:230-258): solve on the device, estimate / mark /
+/// refine on the host with the reference's element_errors and
+/// select_refinements.
+inline RunResult amr_loop(const Device &dev, const RunConfig &config)
+{
+   validate(config);
+   const ManufacturedSolution sol = manufactured_solution(config.solution);
+   const auto forest = std::make_shared<NcForest>(build_mesh(config), config.amr.irregularity_limit);
+   RunResult out;
+   out.forest = forest;
+   for (int iter = 0;; iter++) {
+      const auto space = std::make_shared<const FeSpace>(*forest, FeCollection(FeFamily::H1, config.order));
+      RunResult solve = solve_on_space(dev, space, sol, config);
+      out.rows.push_back(solve.rows[0]);
+      out.converged = out.converged && solve.converged;
+      out.space = solve.space;
+      out.u = std::move(solve.u);
+      if (iter == config.amr.iters || !out.converged) break;
+      const ElementErrors err = element_errors(*out.u, sol, config.amr.anisotropic);
+      const std::vector<std::pair<int, SplitKind>> marks =
+         select_refinements(err.l2, err.directional, config.amr.theta);
+      if (marks.empty()) break;
+      forest->refine(marks);
+   }
+   fill_orders(out.rows);
+   return out;
 }
 
 } // namespace b200
