@@ -185,7 +185,10 @@ struct tfem_restriction {
    int n_gbuckets = 0;
    Bucket gbuckets[kMaxBuckets];
    int64_t n_gshared = 0;
-   double *evec = nullptr;       // E-vector scratch, gmap layout (lazy)
+   // E-vector scratch (lazy), [i][ne_pad] for every map layout ("ev_index"):
+   // slot (e, i) at i * ne_pad + e; element-major maps store their bucket
+   // slot lists in this index space
+   double *evec = nullptr;
    bool cartesian = false;
    int n[3] = {0, 0, 0};
    double *ensure_evec();

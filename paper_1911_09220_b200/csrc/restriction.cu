@@ -252,7 +252,18 @@ __global__ void to_internal_kernel(Layout L, const double *api, double *evec)
 {
    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    if (t >= L.ne * L.nd) return;
-   evec[L.slot_e(static_cast<int>(t % L.nd), t / L.nd)] = api[t];
+   evec[(t % L.nd) * L.ne_pad + L.order.pos_of(t / L.nd)] = api[t]; // ev_index
+}
+
+// Bucket slot lists of element-major maps, once sorted, are rewritten as
+// internal E-vector indices (ev_index: [i][ne_pad] for every layout), so the
+// scatter reads consecutive elements' slots from adjacent words.
+__global__ void slots_to_ev_kernel(uint32_t *slots, int64_t n, int nd, int64_t ne_pad)
+{
+   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (k >= n) return;
+   const uint32_t s = slots[k];
+   slots[k] = static_cast<uint32_t>((s % nd) * ne_pad + s / nd);
 }
 
 // project_coefficient's `g.values()[dofs[...]] = v` (fespace.cpp:334-356):
@@ -481,6 +492,12 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
          sort_rows_kernel<<<blocks_for(r->buckets[b].n), kThreads, 0, s>>>(
             r->buckets[b].slots, r->buckets[b].n, r->buckets[b].c, L);
          ctx->launched();
+         if (elem_major) {
+            const int64_t n = r->buckets[b].n * r->buckets[b].c;
+            slots_to_ev_kernel<<<blocks_for(n), kThreads, 0, s>>>(r->buckets[b].slots, n, r->nd,
+                                                                 r->ne_pad);
+            ctx->launched();
+         }
       }
    }
    TFEM_CUDA(cudaGetLastError());
