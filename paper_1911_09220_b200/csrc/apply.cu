@@ -193,7 +193,7 @@ __global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne,
       const uint32_t d = g & kDofMask;
       y[d] = __dadd_rn(y[d], s);
    } else {
-      evec[(int64_t)i * ne_pad + e] = s; // ev_index
+      evec[elem_major ? ev_em(nd, ne_pad, e, i) : (int64_t)i * ne_pad + e] = s;
    }
 }
 

@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
                         dot = mac<EXACT>(dot, __ldg(a.x + d), rr);
                      }
                   } else {
-                     a.evec[t * a.ne_pad + e] = rr; // ev_index: [i][ne_pad]
+                     a.evec[ev_em(ND, a.ne_pad, e, t)] = rr;
                   }
                }
             }

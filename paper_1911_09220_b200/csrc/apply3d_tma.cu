@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                   dot = fma(__ldg(a.x + d), r, dot);
                }
             } else {
-               a.evec[i * a.ne_pad + e] = r; // ev_index: [i][ne_pad]
+               a.evec[ev_em(ND, a.ne_pad, e, i)] = r;
             }
          }
          __syncwarp(); // TB / TG / P reused by the next group

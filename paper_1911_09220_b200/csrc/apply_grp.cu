@@ -134,7 +134,7 @@ __global__ void apply2d_grp_kernel(const ApplyArgs a)
          a.y[d] = r;
          if (a.dot && !(a.notown && bit_set(a.notown, d))) dot = mul<EXACT>(__ldg(a.x + d), r);
       } else {
-         a.evec[t * a.ne_pad + e] = r; // ev_index: [i][ne_pad]
+         a.evec[ev_em(ND, a.ne_pad, e, t)] = r;
       }
    }
    if (a.dot) {
@@ -298,7 +298,7 @@ __global__ void apply3d_kernel(const ApplyArgs a)
             a.y[d] = r;
             if (a.dot && !(a.notown && bit_set(a.notown, d))) dot = fma(__ldg(a.x + d), r, dot);
          } else {
-            a.evec[i * a.ne_pad + e] = r; // ev_index: [i][ne_pad]
+            a.evec[ev_em(ND, a.ne_pad, e, i)] = r;
          }
       }
    }

@@ -252,19 +252,11 @@ __global__ void to_internal_kernel(Layout L, const double *api, double *evec)
 {
    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    if (t >= L.ne * L.nd) return;
-   evec[(t % L.nd) * L.ne_pad + L.order.pos_of(t / L.nd)] = api[t]; // ev_index
+   const int i = static_cast<int>(t % L.nd);
+   const int64_t pos = L.order.pos_of(t / L.nd);
+   evec[L.elem_major ? ev_em(L.nd, L.ne_pad, pos, i) : (int64_t)i * L.ne_pad + pos] = api[t];
 }
 
-// Bucket slot lists of element-major maps, once sorted, are rewritten as
-// internal E-vector indices (ev_index: [i][ne_pad] for every layout), so the
-// scatter reads consecutive elements' slots from adjacent words.
-__global__ void slots_to_ev_kernel(uint32_t *slots, int64_t n, int nd, int64_t ne_pad)
-{
-   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-   if (k >= n) return;
-   const uint32_t s = slots[k];
-   slots[k] = static_cast<uint32_t>((s % nd) * ne_pad + s / nd);
-}
 
 // project_coefficient's `g.values()[dofs[...]] = v` (fespace.cpp:334-356):
 // every DOF takes the value of its last element.  Exclusive slots directly,
@@ -326,6 +318,52 @@ void exclusive_scan(tfem_ctx *ctx, const int32_t *in, int32_t *out, int64_t n)
    TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
    cudaFree(tmp);
    ctx->launched();
+}
+
+__global__ void first_slot_kernel(const uint32_t *slots, int64_t n, int c, uint32_t *key,
+                                  int32_t *idx)
+{
+   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (k >= n) return;
+   key[k] = slots[k * c];
+   idx[k] = static_cast<int32_t>(k);
+}
+
+__global__ void permute_rows_kernel(const int32_t *perm, int64_t n, int c, const int32_t *dofs,
+                                    const uint32_t *slots, int32_t *dofs2, uint32_t *slots2)
+{
+   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (k >= n) return;
+   const int64_t src = perm[k];
+   dofs2[k] = dofs[src];
+   for (int j = 0; j < c; j++) slots2[k * c + j] = slots[src * c + j];
+}
+
+// Reorder a bucket's rows by their first slot (stable radix sort).
+void sort_rows_by_first_slot(tfem_ctx *ctx, tfem_restriction::Bucket &bk)
+{
+   cudaStream_t s = ctx->stream;
+   const int64_t n = bk.n;
+   uint32_t *key = dalloc<uint32_t>(n), *key2 = dalloc<uint32_t>(n);
+   int32_t *idx = dalloc<int32_t>(n), *perm = dalloc<int32_t>(n), *dofs2 = dalloc<int32_t>(n);
+   uint32_t *slots2 = dalloc<uint32_t>(n * bk.c);
+   first_slot_kernel<<<blocks_for(n), kThreads, 0, s>>>(bk.slots, n, bk.c, key, idx);
+   size_t bytes = 0;
+   TFEM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, key2, idx, perm, n, 0, 32, s));
+   void *tmp = dalloc<char>(static_cast<int64_t>(bytes));
+   TFEM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, key, key2, idx, perm, n, 0, 32, s));
+   permute_rows_kernel<<<blocks_for(n), kThreads, 0, s>>>(perm, n, bk.c, bk.dofs, bk.slots, dofs2,
+                                                         slots2);
+   ctx->launched(3);
+   TFEM_CUDA(cudaGetLastError());
+   TFEM_CUDA(cudaStreamSynchronize(s));
+   cudaFree(bk.dofs);
+   cudaFree(bk.slots);
+   bk.dofs = dofs2;
+   bk.slots = slots2;
+   for (void *p : {static_cast<void *>(key), static_cast<void *>(key2), static_cast<void *>(idx),
+                   static_cast<void *>(perm), tmp})
+      cudaFree(p);
 }
 
 // Warp-local DOFs of an ordered space (host side, once per space).  A
@@ -492,12 +530,9 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
          sort_rows_kernel<<<blocks_for(r->buckets[b].n), kThreads, 0, s>>>(
             r->buckets[b].slots, r->buckets[b].n, r->buckets[b].c, L);
          ctx->launched();
-         if (elem_major) {
-            const int64_t n = r->buckets[b].n * r->buckets[b].c;
-            slots_to_ev_kernel<<<blocks_for(n), kThreads, 0, s>>>(r->buckets[b].slots, n, r->nd,
-                                                                 r->ne_pad);
-            ctx->launched();
-         }
+         // element-major E-vector: rows in first-slot (element) order, so the
+         // scatter's threads read neighbouring slots of the same elements
+         if (elem_major) sort_rows_by_first_slot(ctx, r->buckets[b]);
       }
    }
    TFEM_CUDA(cudaGetLastError());
