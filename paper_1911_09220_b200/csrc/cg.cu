@@ -6,10 +6,10 @@
 //   1-2. q = A p          element kernel + shared-DOF scatter, fused p.q
 //                         partials; the last block to finish folds them and
 //                         takes alpha = rz / pq (emit, common.cuh)
-//   3.   update kernel    x' = x + alpha p, r -= alpha q, z = r / d, partials
-//                         of r.r and r.z; its last block takes ||r||, the
-//                         best-iterate bookkeeping, beta and the stop test
-//   4.   direction kernel p = r / d + beta p
+//   3.   update kernel    r -= alpha q, z = r / d, partials of r.r and r.z;
+//                         its last block takes ||r||, the best-iterate
+//                         bookkeeping, beta and the stop test
+//   4.   direction kernel x' = x + alpha p and p = r / d + beta p (p read once)
 // Vector updates use unfused multiply + add in the reference's order
 // (vector.cpp:20-23, solvers.cpp:84-87), so only the dot products differ from
 // the CPU (tree vs sequential sum).  The best iterate (solvers.cpp:78-81) costs
@@ -149,6 +149,8 @@ __device__ void init_step(CgState *st, double rr, double rz)
    st->status = 0;
    st->cur = 0;
    st->best = 0;
+   st->prev = 0;
+   st->xpend = 0;
    if (st->rnorm <= st->target) { // top of iteration 1 (solvers.cpp:61-65)
       st->done = 1;
       st->converged = 1;
@@ -197,28 +199,24 @@ struct XBufs {
 
 constexpr int kUnroll = 4;
 
-// x' = x + alpha p, r -= alpha q, z = r / d; partials of r.r, r.z.  Four
-// independent elements per trip keep ~20 loads in flight per thread.
+// r -= alpha q, z = r / d; partials of r.r, r.z.  Four independent
+// elements per trip keep ~16 loads in flight per thread.  (x' = x + alpha p
+// is taken by the direction kernel, which streams p anyway.)
 __global__ void __launch_bounds__(kVecThreads)
-cg_update_kernel(const CgState *st, XBufs xb, const double *__restrict__ p,
-                 const double *__restrict__ q, double *__restrict__ r,
+cg_update_kernel(const CgState *st, const double *__restrict__ q, double *__restrict__ r,
                  const double *__restrict__ diag, int64_t n, DotSink sink,
                  const uint32_t *notown)
 {
    if (st->done) return;
-   const double alpha = st->alpha, nalpha = -alpha;
-   const double *__restrict__ xc = xb.x[st->cur];
-   double *__restrict__ xn = xb.x[next_buffer(st->cur, st->best)];
+   const double nalpha = -st->alpha;
    double rr = 0.0, rz = 0.0;
    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
-      double xv[kUnroll], pv[kUnroll], rv[kUnroll], qv[kUnroll], dv[kUnroll];
+      double rv[kUnroll], qv[kUnroll], dv[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; u++) {
          const int64_t j = i + u * stride;
-         xv[u] = xc[j];
-         pv[u] = p[j];
          rv[u] = r[j];
          qv[u] = q[j];
          dv[u] = diag ? diag[j] : 1.0;
@@ -226,7 +224,6 @@ cg_update_kernel(const CgState *st, XBufs xb, const double *__restrict__ p,
 #pragma unroll
       for (int u = 0; u < kUnroll; u++) {
          const int64_t j = i + u * stride;
-         xn[j] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));
          const double ri = __dadd_rn(rv[u], __dmul_rn(nalpha, qv[u]));
          r[j] = ri;
          const double zi = diag ? __ddiv_rn(ri, dv[u]) : ri;
@@ -236,7 +233,6 @@ cg_update_kernel(const CgState *st, XBufs xb, const double *__restrict__ p,
       }
    }
    for (; i < n; i += stride) {
-      xn[i] = __dadd_rn(xc[i], __dmul_rn(alpha, p[i]));
       const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, q[i]));
       r[i] = ri;
       const double zi = diag ? __ddiv_rn(ri, diag[i]) : ri;
@@ -248,33 +244,64 @@ cg_update_kernel(const CgState *st, XBufs xb, const double *__restrict__ p,
    emit<kVecThreads, 2>(sink, v);
 }
 
-// p = z + beta p with z = r / d (solvers.cpp:84-87)
+// x[cur] = x[prev] + alpha p (the iteration's pending x update, solvers.cpp:
+// 66-67) and, unless the solve just ended, p = z + beta p with z = r / d
+// (solvers.cpp:84-87): p is read once for both.  The last block clears the
+// pending flag, so the no-op iterations after convergence skip it.
 __global__ void __launch_bounds__(kVecThreads)
-cg_direction_kernel(const CgState *st, const double *__restrict__ r,
-                    const double *__restrict__ diag, double *__restrict__ p, int64_t n)
+cg_direction_kernel(CgState *st, XBufs xb, const double *__restrict__ r,
+                    const double *__restrict__ diag, double *__restrict__ p, int64_t n,
+                    unsigned *ticket)
 {
-   if (st->done) return;
-   const double beta = st->beta;
+   const bool xu = st->xpend != 0, pu = !st->done;
+   if (!xu && !pu) return;
+   const double beta = st->beta, alpha = st->alpha;
+   const double *__restrict__ xo = xb.x[st->prev];
+   double *__restrict__ xn = xb.x[st->cur];
    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
-      double rv[kUnroll], dv[kUnroll], pv[kUnroll];
+      double rv[kUnroll], dv[kUnroll], pv[kUnroll], xv[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; u++) {
          const int64_t j = i + u * stride;
-         rv[u] = r[j];
-         dv[u] = diag ? diag[j] : 1.0;
          pv[u] = p[j];
+         if (xu) xv[u] = xo[j];
+         if (pu) {
+            rv[u] = r[j];
+            dv[u] = diag ? diag[j] : 1.0;
+         }
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; u++) {
-         const double zi = diag ? __ddiv_rn(rv[u], dv[u]) : rv[u];
-         p[i + u * stride] = __dadd_rn(zi, __dmul_rn(beta, pv[u]));
+         const int64_t j = i + u * stride;
+         if (xu) xn[j] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));
+         if (pu) {
+            const double zi = diag ? __ddiv_rn(rv[u], dv[u]) : rv[u];
+            p[j] = __dadd_rn(zi, __dmul_rn(beta, pv[u]));
+         }
       }
    }
    for (; i < n; i += stride) {
-      const double zi = diag ? __ddiv_rn(r[i], diag[i]) : r[i];
-      p[i] = __dadd_rn(zi, __dmul_rn(beta, p[i]));
+      const double pv = p[i];
+      if (xu) xn[i] = __dadd_rn(xo[i], __dmul_rn(alpha, pv));
+      if (pu) {
+         const double zi = diag ? __ddiv_rn(r[i], diag[i]) : r[i];
+         p[i] = __dadd_rn(zi, __dmul_rn(beta, pv));
+      }
+   }
+   if (xu) {
+      __shared__ bool last;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+         __threadfence();
+         last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+      }
+      __syncthreads();
+      if (last && threadIdx.x == 0) {
+         st->xpend = 0;
+         *ticket = 0u;
+      }
    }
 }
 
@@ -321,6 +348,7 @@ struct Workspace {
    double *r = nullptr, *p = nullptr, *q = nullptr, *xa = nullptr, *xb = nullptr;
    SinkStore s_elem, s_scatter, s_vec;
    CgState *st = nullptr;
+   unsigned *dir_ticket = nullptr; // last-block ticket of the direction kernel
    CgState *host_st = nullptr; // pinned
    cudaGraphExec_t graph = nullptr;
    const double *g_diag = nullptr, *g_x = nullptr;
@@ -337,6 +365,7 @@ struct Workspace {
       s_scatter.release();
       s_vec.release();
       cudaFree(st);
+      cudaFree(dir_ticket);
       if (host_st) cudaFreeHost(host_st);
       if (graph) cudaGraphExecDestroy(graph);
    }
@@ -375,6 +404,8 @@ Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
    }
    w->s_vec.alloc(ctx->stream, vec_blocks(ctx, op->n), 2);
    w->st = dalloc<CgState>(1);
+   w->dir_ticket = dalloc<unsigned>(1);
+   TFEM_CUDA(cudaMemsetAsync(w->dir_ticket, 0, sizeof(unsigned), ctx->stream));
    TFEM_CUDA(cudaMallocHost(&w->host_st, sizeof(CgState)));
    auto &ref = *w;
    m.emplace(op, std::move(w));
@@ -402,10 +433,10 @@ void enqueue_iteration(tfem_ctx *ctx, const tfem_operator *op, Workspace &w, XBu
    operator_mult(ctx, op, w.p, w.q, &se, w.s_scatter.grid ? &ss : nullptr, &w.st->done);
    if (ev) TFEM_CUDA(cudaEventRecord(ev[1], ctx->stream));
    const unsigned vb = vec_blocks(ctx, n);
-   cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.p, w.q, w.r, diag, n, sv,
-                                                         nullptr);
+   cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.q, w.r, diag, n, sv, nullptr);
    if (ev) TFEM_CUDA(cudaEventRecord(ev[2], ctx->stream));
-   cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.r, diag, w.p, n);
+   cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.r, diag, w.p, n,
+                                                            w.dir_ticket);
    if (ev) TFEM_CUDA(cudaEventRecord(ev[3], ctx->stream));
    ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
@@ -725,13 +756,14 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
                                                          1, op->red);
       comm->allreduce(1, comm->user);
       red_alpha_kernel<<<1, 1, 0, ctx->stream>>>(op->red, w.st);
-      cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.p, w.q, w.r, diag, n,
-                                                            w.s_vec.s, op->notown);
+      cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.q, w.r, diag, n, w.s_vec.s,
+                                                            op->notown);
       fold_to_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, nullptr,
                                                          0, 2, op->red);
       comm->allreduce(2, comm->user);
       red_beta_kernel<<<1, 1, 0, ctx->stream>>>(op->red, w.st);
-      cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.r, diag, w.p, n);
+      cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.r, diag, w.p, n,
+                                                            w.dir_ticket);
       ctx->launched(6);
       TFEM_CUDA(cudaGetLastError());
    };

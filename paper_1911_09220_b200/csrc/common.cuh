@@ -273,6 +273,9 @@ struct CgState {
    double rz, alpha, beta, rnorm, best_rnorm, target;
    int it, max_iters, done, converged, iterations, status;
    int cur, best;
+   // x' = x + alpha p is taken by the direction kernel (which reads p
+   // anyway): x buffer `prev` -> `cur`, pending while xpend != 0
+   int prev, xpend;
 };
 
 enum SinkFinish : int { kFinishNone = 0, kFinishAlpha = 1, kFinishBeta = 2 };
@@ -433,7 +436,9 @@ __device__ inline void beta_step(CgState *st, double rr, double rz_next)
    }
    st->it += 1;
    const int nxt = next_buffer(st->cur, st->best);
+   st->prev = st->cur;
    st->cur = nxt;
+   st->xpend = 1;
    if (rnorm < st->best_rnorm) { // solvers.cpp:78-81
       st->best_rnorm = rnorm;
       st->best = nxt;
