@@ -34,7 +34,7 @@ def test_layout_3d(dev, p):
     assert (sp.essential_true_dofs() == oc.boundary_dofs()).all()
 
 
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 6, 8])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 8])
 @pytest.mark.parametrize("kind", ["diffusion", "mass"])
 @pytest.mark.parametrize("rule", ["gl", "gll"])
 def test_qdata_apply_diag_3d(dev, p, kind, rule):
