@@ -1,10 +1,12 @@
 // K3 / K4 and the K2 dispatch: the deterministic shared-DOF scatter, the
 // exact diagonal, and pa_apply / pa_diagonal (forms.cpp:231-382).
 //
-// Element kernels (apply2d_reg.cu, apply_grp.cu) write DOFs owned by one
-// element ("exclusive") straight to y and the others to the E-vector;
-// scatter_kernel then sums each shared DOF's slots in ascending element order
-// (forms.cpp:289-295) -- deterministic, no atomics.
+// Element kernels (apply2d_tma.cu 2D p<=3, apply2d_hi.cu 2D p>=4,
+// apply3d_tma.cu 3D q<=7, apply_grp.cu otherwise; apply2d_reg.cu for A/B)
+// write DOFs owned by one element ("exclusive") straight to y -- the 2D p<=3
+// kernel also sums warp-local shared DOFs itself -- and the others to the
+// E-vector; scatter_kernel then sums each remaining shared DOF's slots in
+// ascending element order (forms.cpp:289-295) -- deterministic, no atomics.
 #include "kernels.cuh"
 
 #include <algorithm>

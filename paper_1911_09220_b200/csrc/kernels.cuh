@@ -1,5 +1,5 @@
-// Shared definitions of the element kernels (apply2d_reg.cu, apply_grp.cu)
-// and their dispatch (apply.cu).
+// Shared definitions of the element kernels (apply2d_tma.cu, apply2d_hi.cu,
+// apply3d_tma.cu, apply_grp.cu, apply2d_reg.cu) and their dispatch (apply.cu).
 #pragma once
 
 #include "common.cuh"
