@@ -32,6 +32,8 @@ struct alignas(16) Warp2 {
    double T1[GRP][Q * D1], T2[GRP][Q * D1]; // [e][qx][b]
    double W1[GRP][Q * Q], W2[GRP][Q * Q];   // [e][qx][qy]
    double S1[GRP][D1 * Q], S2[GRP][D1 * Q]; // [e][a][qy]
+   uint32_t gm[GRP * ND];                   // the slot's map entries, for the epilogue
+   uint8_t es[GRP * ND];                    // ... and their essential flags (ess_out)
    uint64_t full[kSlots], empty[kSlots];
 };
 
@@ -125,6 +127,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
          }
          cp_async_commit();
       };
+      const bool ess_is_mask = a.ess_out == a.mask_in;
       load_map(group(warp, 0), gcur);
       prefetch_x(group(warp, 0), gcur, 0);
       for (int64_t k = 0;; k++) {
@@ -133,17 +136,21 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
          if (cnt == 0) break;
          const int vb = static_cast<int>(k & 1);
          cp_async_wait_all();
-         if (a.mask_in) {
+         // masked gather; the map entries and essential flags go to shared
+         // memory for the epilogue (no global loads there)
 #pragma unroll
-            for (int m = 0; m < GPL; m++) {
-               const int i = lane + 32 * m;
-               if (i < cnt * ND && bit_set(a.mask_in, gcur[m] & kDofMask)) sm.V[vb][vslot(i)] = 0.0;
-            }
+         for (int m = 0; m < GPL; m++) {
+            const int i = lane + 32 * m;
+            if (i >= cnt * ND) continue;
+            const uint32_t d = gcur[m] & kDofMask;
+            const bool mk = a.mask_in && bit_set(a.mask_in, d);
+            if (mk) sm.V[vb][vslot(i)] = 0.0;
+            sm.gm[i] = gcur[m];
+            sm.es[i] = (ess_is_mask ? mk : (a.ess_out && bit_set(a.ess_out, d))) ? 1 : 0;
          }
          __syncwarp();
          const int64_t gn = group(warp, k + 1);
-         load_map(gn, gnext);
-         prefetch_x(gn, gnext, vb ^ 1);
+         load_map(gn, gnext); // consumed after the x contraction (latency hidden)
          const int s = static_cast<int>(k % kSlots);
          mbar_wait(&sm.full[s], static_cast<unsigned>((k / kSlots) & 1));
          {
@@ -164,6 +171,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
                   sm.T2[j][t] = s2;
                }
             }
+            prefetch_x(gn, gnext, vb ^ 1); // the other V buffer is free
             __syncwarp();
             for (int t = lane; t < NQD; t += 32) { // contract y, point factors: [qx][qy]
                const int qx = t % Q, qy = t / Q;
@@ -249,11 +257,11 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
                   if (j >= cnt) continue;
                   const int64_t e = g * GRP + j;
                   double rr = r[j];
-                  const uint32_t gg = __ldg(a.gmap + e * ND + t); // L1/L2-resident
+                  const uint32_t gg = sm.gm[j * ND + t];
                   if (is_exclusive(gg)) {
                      const uint32_t d = gg & kDofMask;
                      if (!a.overwrite) rr = add<EXACT>(a.y[d], rr);
-                     const bool es = a.ess_out && bit_set(a.ess_out, d);
+                     const bool es = sm.es[j * ND + t] != 0;
                      if (es) rr = __ldg(a.x + d);
                      a.y[d] = rr;
                      if (EDOT) {
