@@ -325,6 +325,13 @@ def bench_distributed(args, rank: int, world: int, local: int):
             "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(args, n, args.order, N_global // world, world=world),
+            # the distributed run times the whole CG iteration (no per-kernel
+            # split): algorithmic bytes of an iteration per GPU / its time
+            "roofline": {"bound": "hbm", "achieved": b_it * value / world, "peak": peak,
+                         "unit": "GB/s", "frac": b_it * value / world / peak, "traffic": None,
+                         "kernel": "whole CG iteration per GPU (operator + vector kernels "
+                                   "+ halo / allreduce)",
+                         "bytes_per_dof_iteration": b_it},
             "cg_roofline": {"achieved_per_gpu": b_it * value / world, "unit": "GB/s",
                             "frac": b_it * value / world / peak},
             "e2e": e2e, "cpu_baseline": None, "clocks": clk.summary(),
