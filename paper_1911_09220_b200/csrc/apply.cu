@@ -324,6 +324,7 @@ void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const
    a.overwrite = f.overwrite ? 1 : 0;
    a.mask_in = f.mask_in;
    a.ess_out = f.ess_out;
+   a.elem_ess = f.mask_in ? f.elem_ess : nullptr;
    a.notown = f.notown;
    a.warp_local = tl ? 1 : 0;
    static const bool edot_on = env_on("TFEM_EDOT");

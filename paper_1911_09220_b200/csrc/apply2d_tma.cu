@@ -44,6 +44,7 @@ struct TileSmem {
    static constexpr int kMaps = 3;   // the open tile's map stays until its epilogue
    double q[kStages][SLICE][kTile];
    uint32_t gmap[kMaps][ND][kTile];
+   uint32_t gess[kMaps][kTile];  // a.elem_ess words of the tile (when given)
    double xs[2][ND][kTile];      // x of the open / next tile [i][lane]
    uint32_t essm[kTile];         // per lane: slots whose DOF is essential (ess_out)
    uint64_t full[kStages];  // slice landed (tx count)
@@ -88,9 +89,11 @@ __device__ __forceinline__ void issue_gmap(TileSmem<P, Q, KIND, EXACT> &sm, cons
    const int64_t avail = a.ne_pad - e0;
    const unsigned bytes = static_cast<unsigned>(avail < kTile ? avail : kTile) * 4u;
    const int b = static_cast<int>(lt % TileSmem<P, Q, KIND, EXACT>::kMaps);
-   mbar_expect_tx(&sm.gfull[b], bytes * ND);
+   const unsigned ebytes = a.elem_ess ? bytes : 0u; // elem_ess: ne_pad words
+   mbar_expect_tx(&sm.gfull[b], bytes * ND + ebytes);
 #pragma unroll
    for (int i = 0; i < ND; i++) bulk_g2s(&sm.gmap[b][i][0], a.gmap + i * a.ne_pad + e0, bytes, &sm.gfull[b]);
+   if (ebytes) bulk_g2s(&sm.gess[b][0], a.elem_ess + e0, ebytes, &sm.gfull[b]);
 }
 
 // One qy slice of the diffusion chain for the calling thread's element:
@@ -295,15 +298,31 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       mbar_wait(&sm.xfull[xb], static_cast<unsigned>((lt >> 1) & 1));
       uint32_t essm = 0; // slots whose DOF is essential (ess_out)
       double V[D1][D1];
+      if (a.elem_ess) { // mask_in as one word per position
+         const uint32_t mw = live ? sm.gess[gb][tid] : 0u;
 #pragma unroll
-      for (int i = 0; i < ND; i++) {
-         const uint32_t d = sm.gmap[gb][i][tid] & kDofMask;
-         double v = live ? xs[i * kTile + tid] : 0.0;
-         const bool m = a.mask_in && live && bit_set(a.mask_in, d);
-         const bool es = ess_is_mask ? m : live && a.ess_out && bit_set(a.ess_out, d);
-         essm |= static_cast<uint32_t>(es) << i;
-         if (m) v = 0.0;
-         V[i % D1][i / D1] = v;
+         for (int i = 0; i < ND; i++) {
+            const double v = live ? xs[i * kTile + tid] : 0.0;
+            V[i % D1][i / D1] = (mw >> i) & 1u ? 0.0 : v;
+         }
+         if (ess_is_mask) {
+            essm = mw;
+         } else if (a.ess_out) {
+#pragma unroll
+            for (int i = 0; i < ND; i++)
+               essm |= static_cast<uint32_t>(live && bit_set(a.ess_out, sm.gmap[gb][i][tid] & kDofMask)) << i;
+         }
+      } else {
+#pragma unroll
+         for (int i = 0; i < ND; i++) {
+            const uint32_t d = sm.gmap[gb][i][tid] & kDofMask;
+            double v = live ? xs[i * kTile + tid] : 0.0;
+            const bool m = a.mask_in && live && bit_set(a.mask_in, d);
+            const bool es = ess_is_mask ? m : live && a.ess_out && bit_set(a.ess_out, d);
+            essm |= static_cast<uint32_t>(es) << i;
+            if (m) v = 0.0;
+            V[i % D1][i / D1] = v;
+         }
       }
       sm.essm[tid] = essm;
       // Gather of the next tile (issued after the x contraction, when V is

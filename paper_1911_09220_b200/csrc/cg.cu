@@ -88,6 +88,18 @@ __global__ void set_bits_kernel(const int32_t *list, int64_t n, uint32_t *mask)
    if (i < n) atomicOr(mask + (list[i] >> 5), 1u << (list[i] & 31));
 }
 
+// tfem_operator::elem_ess: word[pos] bit i = slot i's DOF is in the mask.
+__global__ void elem_ess_kernel(const uint32_t *gmap, int nd, int64_t npos, int64_t ne_pad,
+                                const uint32_t *mask, uint32_t *words)
+{
+   const int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (pos >= npos) return;
+   uint32_t w = 0;
+   for (int i = 0; i < nd; i++)
+      w |= static_cast<uint32_t>(bit_set(mask, gmap[i * ne_pad + pos] & kDofMask)) << i;
+   words[pos] = w;
+}
+
 __global__ void set_values_kernel(const int32_t *list, int64_t n, double v, double *y)
 {
    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -519,6 +531,15 @@ void operator_set_ess(tfem_ctx *ctx, tfem_operator *op, int64_t n_ess, const int
                                                                    op->ess_mask);
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
+   const tfem_restriction *r = op->r;
+   if (r && !op->P && !r->elem_major && r->nd <= 32 && r->npos > 0) {
+      op->elem_ess = dalloc<uint32_t>(r->ne_pad);
+      TFEM_CUDA(cudaMemsetAsync(op->elem_ess, 0, sizeof(uint32_t) * r->ne_pad, ctx->stream));
+      elem_ess_kernel<<<blocks_for(r->npos, 256), 256, 0, ctx->stream>>>(
+         r->gmap, r->nd, r->npos, r->ne_pad, op->ess_mask, op->elem_ess);
+      ctx->launched();
+      TFEM_CUDA(cudaGetLastError());
+   }
    TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -611,6 +632,7 @@ void operator_release(tfem_operator *op)
    workspaces().erase(op);
    cudaFree(op->ess);
    cudaFree(op->ess_mask);
+   cudaFree(op->elem_ess);
    cudaFree(op->notown);
    cudaFree(op->rowptr);
    cudaFree(op->cols);
@@ -653,6 +675,7 @@ void operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, doub
       ApplyFlags f;
       f.overwrite = (k == 0);
       f.mask_in = op->ess_mask;
+      f.elem_ess = op->elem_ess;
       const bool last = (k + 1 == op->pa.size());
       f.ess_out = last ? op->ess_mask : nullptr;
       f.notown = op->notown;

@@ -251,6 +251,10 @@ struct tfem_operator {
    int64_t n_ess = 0;
    int32_t *ess = nullptr;      // sorted list
    uint32_t *ess_mask = nullptr; // bitmap over DOFs
+   // per element position: the slots whose DOF is in ess_mask (slot-major
+   // maps with nd <= 32; read by the 2D bulk-copy kernel instead of one
+   // bitmap load per slot)
+   uint32_t *elem_ess = nullptr;
    uint32_t *notown = nullptr;   // bitmap: DOFs owned by another rank (dist)
    bool has_comm = false;        // distributed: CG calls the hooks below
    tfem_comm comm{};
@@ -332,6 +336,7 @@ struct ApplyFlags {
    bool overwrite = false;   // y = (else y +=)
    const uint32_t *mask_in = nullptr;  // zero gathered essential DOFs
    const uint32_t *ess_out = nullptr;  // y[ess] = x[ess]
+   const uint32_t *elem_ess = nullptr; // mask_in per position (tfem_operator::elem_ess)
    const uint32_t *notown = nullptr;   // excluded from the dot (other rank's DOFs)
    DotSink dot;                        // element-kernel x . y partials
    DotSink dot_scatter;                // scatter-kernel x . y partials

@@ -23,6 +23,7 @@ struct ApplyArgs {
    int overwrite;
    const uint32_t *mask_in;
    const uint32_t *ess_out;
+   const uint32_t *elem_ess; // optional: mask_in as a per-position slot word
    const uint32_t *notown; // DOFs owned by another rank: left out of the dot
    int warp_local;  // sum kWarpOwner/kWarpMember DOFs in-warp (else E-vector)
    int energy_dot;  // x . y = sum of element energies of the masked x + sum_ess x^2
