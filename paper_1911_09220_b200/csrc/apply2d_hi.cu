@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
       // ---------------------------------------------------------- consumer
       W &sm = ws[warp];
       uint32_t gcur[GPL], gnext[GPL];
+      uint32_t mcur[GPL], mnext[GPL]; // mask_in words of the map entries
       auto load_map = [&](int64_t g, uint32_t (&m_)[GPL]) {
          const int64_t lim = (int64_t)count(g) * ND;
 #pragma unroll
@@ -127,9 +128,19 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
          }
          cp_async_commit();
       };
+      // the mask words go out with the gather (tested a group later)
+      auto load_mask = [&](int64_t g, const uint32_t (&m_)[GPL], uint32_t (&w_)[GPL]) {
+         const int64_t lim = (int64_t)count(g) * ND;
+#pragma unroll
+         for (int m = 0; m < GPL; m++) {
+            const int i = lane + 32 * m;
+            w_[m] = a.mask_in && i < lim ? __ldg(a.mask_in + ((m_[m] & kDofMask) >> 5)) : 0u;
+         }
+      };
       const bool ess_is_mask = a.ess_out == a.mask_in;
       load_map(group(warp, 0), gcur);
       prefetch_x(group(warp, 0), gcur, 0);
+      load_mask(group(warp, 0), gcur, mcur);
       for (int64_t k = 0;; k++) {
          const int64_t g = group(warp, k);
          const int cnt = count(g);
@@ -143,7 +154,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
             const int i = lane + 32 * m;
             if (i >= cnt * ND) continue;
             const uint32_t d = gcur[m] & kDofMask;
-            const bool mk = a.mask_in && bit_set(a.mask_in, d);
+            const bool mk = (mcur[m] >> (d & 31)) & 1u;
             if (mk) sm.V[vb][vslot(i)] = 0.0;
             sm.gm[i] = gcur[m];
             sm.es[i] = (ess_is_mask ? mk : (a.ess_out && bit_set(a.ess_out, d))) ? 1 : 0;
@@ -172,6 +183,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
                }
             }
             prefetch_x(gn, gnext, vb ^ 1); // the other V buffer is free
+            load_mask(gn, gnext, mnext);
             __syncwarp();
             for (int t = lane; t < NQD; t += 32) { // contract y, point factors: [qx][qy]
                const int qx = t % Q, qy = t / Q;
@@ -277,7 +289,10 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
             __syncwarp(); // T / W / S reused by the next slot
          }
 #pragma unroll
-         for (int m = 0; m < GPL; m++) gcur[m] = gnext[m];
+         for (int m = 0; m < GPL; m++) {
+            gcur[m] = gnext[m];
+            mcur[m] = mnext[m];
+         }
       }
    }
    if (a.dot) {

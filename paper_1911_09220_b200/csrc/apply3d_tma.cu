@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
       // ---------------------------------------------------------- consumer
       W &sm = ws[warp];
       uint32_t gcur[GPL], gnext[GPL];
+      uint32_t mcur[GPL], mnext[GPL]; // mask_in words of the map entries
       auto load_map = [&](int64_t g, uint32_t (&m_)[GPL]) {
          const int64_t lim = (int64_t)count(g) * ND;
 #pragma unroll
@@ -132,8 +133,18 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          }
          cp_async_commit();
       };
+      // the mask words go out with the gather (tested a group later)
+      auto load_mask = [&](int64_t g, const uint32_t (&m_)[GPL], uint32_t (&w_)[GPL]) {
+         const int64_t lim = (int64_t)count(g) * ND;
+#pragma unroll
+         for (int m = 0; m < GPL; m++) {
+            const int i = lane + 32 * m;
+            w_[m] = a.mask_in && i < lim ? __ldg(a.mask_in + ((m_[m] & kDofMask) >> 5)) : 0u;
+         }
+      };
       load_map(group(warp, 0), gcur);
       prefetch_x(group(warp, 0), gcur, 0);
+      load_mask(group(warp, 0), gcur, mcur);
       for (int64_t k = 0;; k++) {
          const int64_t g = group(warp, k);
          const int cnt = count(g);
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
 #pragma unroll
             for (int m = 0; m < GPL; m++) {
                const int i = lane + 32 * m;
-               if (i < cnt * ND && bit_set(a.mask_in, gcur[m] & kDofMask)) sm.V[vb][i] = 0.0;
+               if (i < cnt * ND && ((mcur[m] >> (gcur[m] & 31)) & 1u)) sm.V[vb][i] = 0.0;
             }
          }
          __syncwarp();
@@ -166,6 +177,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             sm.TG[jj] = sg;
          }
          prefetch_x(gn, gnext, vb ^ 1); // the other buffer is free
+         load_mask(gn, gnext, mnext);
          __syncwarp();
          const int s = static_cast<int>(k % kSlots);
          mbar_wait(&sm.full[s], static_cast<unsigned>((k / kSlots) & 1));
@@ -298,7 +310,10 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          }
          __syncwarp(); // TB / TG / P reused by the next group
 #pragma unroll
-         for (int m = 0; m < GPL; m++) gcur[m] = gnext[m];
+         for (int m = 0; m < GPL; m++) {
+            gcur[m] = gnext[m];
+            mcur[m] = mnext[m];
+         }
       }
    }
    if (a.dot) {
