@@ -354,7 +354,9 @@ def run_tfem(args):
     achieved = b_op / t_op / 1e9
     b_it = b_op + (80 if args.bp == 1 else 96) * N
     cg_achieved = b_it * args.iters * args.steps / t_value / 1e9
-    bu, bd = (48, 24) if args.bp == 1 else (56, 32)  # no diag stream in BP1
+    # update: read r, q (, d), write r; direction: read x, p, r (, d), write
+    # x', p (the x update runs in the direction kernel; no diag in BP1)
+    bu, bd = (24, 40) if args.bp == 1 else (32, 48)
     cg_kernels = {
         "operator": {"us": seg[0], "bytes_per_dof": b_op / N, "frac": achieved / peak},
         "update": {"us": seg[1], "bytes_per_dof": bu,

@@ -7,7 +7,7 @@
 // seven 8 x 4 warp patches in ElemOrder), warp 7 is the producer.  A tile's
 // qdata is streamed as Q "slices" (one per qy: the nc*Q planes (c, qy, qx),
 // each a contiguous 1792 B run of the [(c*nqd+q)][ne_pad] layout) through a
-// 4-deep ring of shared-memory stages, and the element map (D1^2 planes)
+// 4- or 5-deep ring of shared-memory stages, and the element map (D1^2 planes)
 // through three buffers (the open tile's map is read again by its epilogue).
 // The producer waits on a stage's "empty" mbarrier (one arrive per compute
 // warp) before refilling it; compute warps wait on "full" and never on each
@@ -30,9 +30,10 @@ namespace tfem {
 
 namespace {
 
-constexpr int kCompute = 7;                 // compute warps per block
+
+constexpr int kCompute = 7;                 // compute warps per block (8 warps of 255
+                                            // registers fill the register file)
 constexpr int kTile = 32 * kCompute;        // elements per tile
-static_assert(kTile == kTmaTile, "kTmaTile is the tile of this kernel");
 constexpr int kBlock = 32 * (kCompute + 1); // + the producer warp
 
 template <int P, int Q, int KIND, bool EXACT>
@@ -40,17 +41,24 @@ struct TileSmem {
    static constexpr int D1 = P + 1, ND = D1 * D1;
    static constexpr int NC = KIND == TFEM_MASS ? 1 : 3;
    static constexpr int SLICE = NC * Q; // planes per qy slice
-   static constexpr int kStages = 4; // qdata slice ring
-   static constexpr int kMaps = 3;   // the open tile's map stays until its epilogue
+   // p = 3 with FMA numerics: one x buffer (the next tile's x lands in the
+   // open tile's columns once V is in registers) pays for a fifth slice
+   // stage, +2.5 %; measured slower for p <= 2 and for the exact numerics.
+   // Two map buffers instead of three cost 12-30 % (the prefetch then waits
+   // for the next map).
+   static constexpr bool kDeep = P == 3 && !EXACT;
+   static constexpr int kStages = kDeep ? 5 : 4; // qdata slice ring
+   static constexpr int kXb = kDeep ? 1 : 2;     // x buffers
+   static constexpr int kMaps = 3; // the open tile's map stays until its epilogue
    double q[kStages][SLICE][kTile];
    uint32_t gmap[kMaps][ND][kTile];
    uint32_t gess[kMaps][kTile];  // a.elem_ess words of the tile (when given)
-   double xs[2][ND][kTile];      // x of the open / next tile [i][lane]
+   double xs[kXb][ND][kTile];    // x of the open / next tile [i][lane]
    uint32_t essm[kTile];         // per lane: slots whose DOF is essential (ess_out)
    uint64_t full[kStages];  // slice landed (tx count)
    uint64_t empty[kStages]; // slice consumed (kCompute arrivals)
    uint64_t gfull[kMaps], gempty[kMaps];
-   uint64_t xfull[2];       // a tile's gathers landed (kTile lane arrivals)
+   uint64_t xfull[kXb];     // a tile's gathers landed (kTile lane arrivals)
 };
 
 // Issue qdata slice `k` of this block (tile lt = k / Q, qy = k % Q).
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
          mbar_init(&sm.gfull[b], 1);
          mbar_init(&sm.gempty[b], kCompute);
       }
-      for (int b = 0; b < 2; b++) mbar_init(&sm.xfull[b], kTile);
+      for (int b = 0; b < Smem::kXb; b++) mbar_init(&sm.xfull[b], kTile);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
    }
    __syncthreads();
@@ -291,11 +299,14 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
       const int64_t e = tile_elem(lt);
       const bool live = e < a.ne;
       const int gb = static_cast<int>(lt % Smem::kMaps);
-      const int xb = static_cast<int>(lt & 1);
+      // one buffer: a lane's V is in registers before it gathers the next
+      // tile into the same columns, and no arrival for tile lt + 1 precedes
+      // the completion of tile lt's phase
+      const int xb = static_cast<int>(lt % Smem::kXb), xn = static_cast<int>((lt + 1) % Smem::kXb);
       double *xs = &sm.xs[xb][0][0];
       // x: gathered one tile ahead (or in the prologue).  The map is read
       // again by the epilogue (no registers held across the qy loop).
-      mbar_wait(&sm.xfull[xb], static_cast<unsigned>((lt >> 1) & 1));
+      mbar_wait(&sm.xfull[xb], static_cast<unsigned>((lt / Smem::kXb) & 1));
       uint32_t essm = 0; // slots whose DOF is essential (ess_out)
       double V[D1][D1];
       if (a.elem_ess) { // mask_in as one word per position
@@ -334,9 +345,9 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
          if (tile_elem(lt + 1) < a.ne) {
 #pragma unroll 4
             for (int i = 0; i < ND; i++)
-               gather8(&sm.xs[xb ^ 1][i][tid], a.x + (sm.gmap[nb][i][tid] & kDofMask));
+               gather8(&sm.xs[xn][i][tid], a.x + (sm.gmap[nb][i][tid] & kDofMask));
          }
-         gather_arrive(&sm.xfull[xb ^ 1]);
+         gather_arrive(&sm.xfull[xn]);
       };
       double R[D1][D1];
       // EDOT: the element energies go straight into dot (live lanes)

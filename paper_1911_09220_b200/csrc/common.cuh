@@ -61,7 +61,6 @@ constexpr uint32_t kExclusive = 0x80000000u;
 constexpr uint32_t kWarpMember = 0x40000000u;
 constexpr uint32_t kWarpOwner = 0xc0000000u;
 constexpr uint32_t kDofMask = 0x3fffffffu;
-constexpr int kTmaTile = 224; // elements per tile of apply2d_tma.cu (7 warp patches)
 
 // E-vector index of slot (element position e, local i) of an element-major
 // map ([e][nd], the map's own layout); slot-major maps use i * ne_pad + e.
