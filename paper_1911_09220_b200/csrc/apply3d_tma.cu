@@ -41,6 +41,8 @@ struct alignas(16) Warp3 {
    double TB[EPW * D1 * D1 * Q], TG[EPW * D1 * D1 * Q]; // [e][c][b][qx]
    double Px[EPW * D1 * Q * Q], Py[EPW * D1 * Q * Q], Pz[EPW * D1 * Q * Q]; // [e][c][qy][qx]
    uint64_t full[kSlots], empty[kSlots];
+   uint32_t gm[EPW * ND]; // the open group's map entries and essential flags
+   uint8_t es[EPW * ND];  // (read by the epilogue)
 };
 
 template <int P, int Q, int KIND>
@@ -61,6 +63,9 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    constexpr int kSlots = W::kSlots;
    constexpr int NT = D1 * D1 * Q;         // contraction outputs per element
    constexpr int GPL = (EPW * ND + 31) / 32; // map entries per lane
+   // row-wise contractions (basis operands compile-time) when a warp covers
+   // the rows in one pass; measured slower at q = 7 (two passes, spills)
+   constexpr bool kRows = EPW * D1 * D1 <= 32 && EPW * Q * D1 <= 32;
    constexpr unsigned kQBytes = NC * NQD * 8;
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -151,30 +156,56 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          if (cnt == 0) break;
          const int vb = static_cast<int>(k & 1);
          cp_async_wait_all();
-         // essential DOFs read as zero (masked gather)
-         if (a.mask_in) {
+         // essential DOFs read as zero (masked gather); map entries and
+         // essential flags to shared memory for the epilogue
 #pragma unroll
-            for (int m = 0; m < GPL; m++) {
-               const int i = lane + 32 * m;
-               if (i < cnt * ND && ((mcur[m] >> (gcur[m] & 31)) & 1u)) sm.V[vb][i] = 0.0;
-            }
+         for (int m = 0; m < GPL; m++) {
+            const int i = lane + 32 * m;
+            if (i >= cnt * ND) continue;
+            const uint32_t d = gcur[m] & kDofMask;
+            const bool mk = (mcur[m] >> (d & 31)) & 1u;
+            if (mk) sm.V[vb][i] = 0.0;
+            sm.gm[i] = gcur[m];
+            sm.es[i] = (a.ess_out == a.mask_in ? mk : (a.ess_out && bit_set(a.ess_out, d))) ? 1 : 0;
          }
          __syncwarp();
          const int64_t gn = group(warp, k + 1);
          load_map(gn, gnext);
          const double *V = sm.V[vb];
-         // contract a -> TB / TG [e][c][b][qx]
-         for (int jj = lane; jj < EPW * NT; jj += 32) {
-            const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q;
-            double sb = 0.0, sg = 0.0;
+         // contract a -> TB / TG [e][c][b][qx]: a lane per (e, c, b) row, qx
+         // unrolled (basis operands from the constant bank) when the rows
+         // fit one pass of the warp; else a lane per output
+         if constexpr (!kRows) {
+            for (int jj = lane; jj < EPW * NT; jj += 32) {
+               const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q;
+               double sb = 0.0, sg = 0.0;
 #pragma unroll
-            for (int kk = 0; kk < D1; kk++) {
-               const double v = V[j * ND + cb * D1 + kk];
-               sb = fma(sB[jx][kk], v, sb);
-               if (KIND == TFEM_DIFFUSION) sg = fma(sG[jx][kk], v, sg);
+               for (int kk = 0; kk < D1; kk++) {
+                  const double v = V[j * ND + cb * D1 + kk];
+                  sb = fma(sB[jx][kk], v, sb);
+                  if (KIND == TFEM_DIFFUSION) sg = fma(sG[jx][kk], v, sg);
+               }
+               sm.TB[jj] = sb;
+               sm.TG[jj] = sg;
             }
-            sm.TB[jj] = sb;
-            sm.TG[jj] = sg;
+         } else
+         for (int it = lane; it < EPW * D1 * D1; it += 32) {
+            const int j = it / (D1 * D1), cb = it % (D1 * D1);
+            double v[D1];
+#pragma unroll
+            for (int kk = 0; kk < D1; kk++) v[kk] = V[j * ND + cb * D1 + kk];
+            double *TBo = sm.TB + j * NT + cb * Q, *TGo = sm.TG + j * NT + cb * Q;
+#pragma unroll
+            for (int jx = 0; jx < Q; jx++) {
+               double sb = 0.0, sg = 0.0;
+#pragma unroll
+               for (int kk = 0; kk < D1; kk++) {
+                  sb = fma(a.t.B[jx][kk], v[kk], sb);
+                  if (KIND == TFEM_DIFFUSION) sg = fma(a.t.G[jx][kk], v[kk], sg);
+               }
+               TBo[jx] = sb;
+               if (KIND == TFEM_DIFFUSION) TGo[jx] = sg;
+            }
          }
          prefetch_x(gn, gnext, vb ^ 1); // the other buffer is free
          load_mask(gn, gnext, mnext);
@@ -256,56 +287,98 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          }
          __syncwarp();
          if (lane == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
-         // contract qy -> [e][c][b][qx] (x-gradient part in TB, y + z in TG)
-         for (int jj = lane; jj < EPW * NT; jj += 32) {
-            const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q, b = cb % D1, c = cb / D1;
-            const int po = j * D1 * Q * Q;
-            double sx = 0.0, syz = 0.0;
+         // contract qy -> [e][c][b][qx] (x-gradient part in TB, y + z in TG):
+         // a lane per (e, c, qx), b unrolled (or a lane per output)
+         if constexpr (!kRows) {
+            for (int jj = lane; jj < EPW * NT; jj += 32) {
+               const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q, b = cb % D1, c = cb / D1;
+               const int po = j * D1 * Q * Q;
+               double sx = 0.0, syz = 0.0;
+#pragma unroll
+               for (int y = 0; y < Q; y++) {
+                  const int o = po + (c * Q + y) * Q + jx;
+                  sx = fma(sB[y][b], sm.Px[o], sx);
+                  if (KIND == TFEM_DIFFUSION) {
+                     syz = fma(sG[y][b], sm.Py[o], syz);
+                     syz = fma(sB[y][b], sm.Pz[o], syz);
+                  }
+               }
+               sm.TB[jj] = sx;
+               sm.TG[jj] = syz;
+            }
+         } else
+         for (int it = lane; it < EPW * Q * D1; it += 32) {
+            const int j = it / (Q * D1), r = it % (Q * D1), jx = r % Q, c = r / Q;
+            const int po = j * D1 * Q * Q + c * Q * Q + jx;
+            double px[Q], py[Q], pz[Q];
 #pragma unroll
             for (int y = 0; y < Q; y++) {
-               const int o = po + (c * Q + y) * Q + jx;
-               sx = fma(sB[y][b], sm.Px[o], sx);
+               px[y] = sm.Px[po + y * Q];
                if (KIND == TFEM_DIFFUSION) {
-                  syz = fma(sG[y][b], sm.Py[o], syz);
-                  syz = fma(sB[y][b], sm.Pz[o], syz);
+                  py[y] = sm.Py[po + y * Q];
+                  pz[y] = sm.Pz[po + y * Q];
                }
             }
-            sm.TB[jj] = sx;
-            sm.TG[jj] = syz;
+#pragma unroll
+            for (int b = 0; b < D1; b++) {
+               double sx = 0.0, syz = 0.0;
+#pragma unroll
+               for (int y = 0; y < Q; y++) {
+                  sx = fma(a.t.B[y][b], px[y], sx);
+                  if (KIND == TFEM_DIFFUSION) {
+                     syz = fma(a.t.G[y][b], py[y], syz);
+                     syz = fma(a.t.B[y][b], pz[y], syz);
+                  }
+               }
+               const int o = j * NT + (c * D1 + b) * Q + jx;
+               sm.TB[o] = sx;
+               if (KIND == TFEM_DIFFUSION) sm.TG[o] = syz;
+            }
          }
          __syncwarp();
-         // contract qx -> r(a, b, c) and the epilogue
-#pragma unroll
-         for (int m = 0; m < GPL; m++) {
-            const int ii = lane + 32 * m;
-            if (ii >= cnt * ND) continue;
-            const int j = ii / ND, i = ii % ND, ia = i % D1, cb = i / D1;
-            const double *TB = sm.TB + j * NT + cb * Q, *TG = sm.TG + j * NT + cb * Q;
-            double r = 0.0;
+         // contract qx -> r(a, b, c) and the epilogue: a lane per (e, c, b),
+         // a unrolled (or a lane per output)
+         constexpr int kA = kRows ? D1 : 1; // outputs per work item
+         for (int it = lane; it < cnt * ND / kA; it += 32) {
+            const int j = it / (ND / kA), cb = kRows ? it % (D1 * D1) : (it % ND) / D1;
+            double tb[Q], tg[Q];
 #pragma unroll
             for (int x = 0; x < Q; x++) {
-               if (KIND == TFEM_MASS) {
-                  r = fma(sB[x][ia], TB[x], r);
-               } else {
-                  r = fma(sG[x][ia], TB[x], r);
-                  r = fma(sB[x][ia], TG[x], r);
-               }
+               tb[x] = sm.TB[j * NT + cb * Q + x];
+               if (KIND == TFEM_DIFFUSION) tg[x] = sm.TG[j * NT + cb * Q + x];
             }
             const int64_t e = g * EPW + j;
-            const uint32_t gg = gcur[m];
-            if (is_exclusive(gg)) {
-               const uint32_t d = gg & kDofMask;
-               if (!a.overwrite) r += a.y[d];
-               const bool es = a.ess_out && bit_set(a.ess_out, d);
-               if (es) r = __ldg(a.x + d);
-               a.y[d] = r;
-               if (EDOT) {
-                  if (es) dot = fma(r, r, dot);
-               } else if (a.dot && !(a.notown && bit_set(a.notown, d))) {
-                  dot = fma(__ldg(a.x + d), r, dot);
+#pragma unroll
+            for (int ka = 0; ka < kA; ka++) {
+               const int ia = kRows ? ka : it % D1;
+               double r = 0.0;
+#pragma unroll
+               for (int x = 0; x < Q; x++) {
+                  const double gx = kRows ? a.t.G[x][ka] : sG[x][ia];
+                  const double bx = kRows ? a.t.B[x][ka] : sB[x][ia];
+                  if (KIND == TFEM_MASS) {
+                     r = fma(bx, tb[x], r);
+                  } else {
+                     r = fma(gx, tb[x], r);
+                     r = fma(bx, tg[x], r);
+                  }
                }
-            } else {
-               a.evec[ev_em(ND, a.ne_pad, e, i)] = r;
+               const int i = cb * D1 + ia;
+               const uint32_t gg = sm.gm[j * ND + i];
+               if (is_exclusive(gg)) {
+                  const uint32_t d = gg & kDofMask;
+                  if (!a.overwrite) r += a.y[d];
+                  const bool es = sm.es[j * ND + i] != 0;
+                  if (es) r = __ldg(a.x + d);
+                  a.y[d] = r;
+                  if (EDOT) {
+                     if (es) dot = fma(r, r, dot);
+                  } else if (a.dot && !(a.notown && bit_set(a.notown, d))) {
+                     dot = fma(__ldg(a.x + d), r, dot);
+                  }
+               } else {
+                  a.evec[ev_em(ND, a.ne_pad, e, i)] = r;
+               }
             }
          }
          __syncwarp(); // TB / TG / P reused by the next group
