@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
    } else {
       // ---------------------------------------------------------- consumer
       W &sm = ws[warp];
-      uint32_t gcur[GPL], gnext[GPL];
+      uint32_t gcur[GPL], gnext[GPL], gnn[GPL]; // map entries: this, next, next-but-one group
       uint32_t mcur[GPL], mnext[GPL]; // mask_in words of the map entries
       auto load_map = [&](int64_t g, uint32_t (&m_)[GPL]) {
          const int64_t lim = (int64_t)count(g) * ND;
@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
       };
       const bool ess_is_mask = a.ess_out == a.mask_in;
       load_map(group(warp, 0), gcur);
+      load_map(group(warp, 1), gnext);
       prefetch_x(group(warp, 0), gcur, 0);
       load_mask(group(warp, 0), gcur, mcur);
       for (int64_t k = 0;; k++) {
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
          }
          __syncwarp();
          const int64_t gn = group(warp, k + 1);
-         load_map(gn, gnext); // consumed after the x contraction (latency hidden)
+         load_map(group(warp, k + 2), gnn); // two groups ahead: used a group later
          const int s = static_cast<int>(k % kSlots);
          mbar_wait(&sm.full[s], static_cast<unsigned>((k / kSlots) & 1));
          {
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
             gcur[m] = gnext[m];
+            gnext[m] = gnn[m];
             mcur[m] = mnext[m];
          }
       }

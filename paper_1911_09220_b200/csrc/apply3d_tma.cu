@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    } else {
       // ---------------------------------------------------------- consumer
       W &sm = ws[warp];
-      uint32_t gcur[GPL], gnext[GPL];
+      uint32_t gcur[GPL], gnext[GPL], gnn[GPL]; // map entries: this, next, next-but-one group
       uint32_t mcur[GPL], mnext[GPL]; // mask_in words of the map entries
       auto load_map = [&](int64_t g, uint32_t (&m_)[GPL]) {
          const int64_t lim = (int64_t)count(g) * ND;
@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          }
       };
       load_map(group(warp, 0), gcur);
+      load_map(group(warp, 1), gnext);
       prefetch_x(group(warp, 0), gcur, 0);
       load_mask(group(warp, 0), gcur, mcur);
       for (int64_t k = 0;; k++) {
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          }
          __syncwarp();
          const int64_t gn = group(warp, k + 1);
-         load_map(gn, gnext);
+         load_map(group(warp, k + 2), gnn); // two groups ahead: used a group later
          const double *V = sm.V[vb];
          // contract a -> TB / TG [e][c][b][qx]: a lane per (e, c, b) row, qx
          // unrolled (basis operands from the constant bank) when the rows
@@ -385,6 +386,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
             gcur[m] = gnext[m];
+            gnext[m] = gnn[m];
             mcur[m] = mnext[m];
          }
       }
