@@ -55,13 +55,9 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
    constexpr int kSlots = W::kSlots;
    constexpr int GPL = (GRP * ND + 31) / 32;
    constexpr unsigned kQBytes = NC * NQD * 8;
+   static_assert(GRP * D1 <= 32 && GRP * Q <= 32, "row-wise stages: one row per lane");
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
-   __shared__ double sB[Q][D1], sG[Q][D1];
-   for (int j = threadIdx.x; j < Q * D1; j += blockDim.x) {
-      sB[j / D1][j % D1] = a.t.B[j / D1][j % D1];
-      sG[j / D1][j % D1] = a.t.G[j / D1][j % D1];
-   }
    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
    auto *ws = reinterpret_cast<W *>(smem_raw);
    if (threadIdx.x == 0) {
@@ -167,38 +163,52 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
          mbar_wait(&sm.full[s], static_cast<unsigned>((k / kSlots) & 1));
          {
             const double *qs = sm.q[s];
-            for (int t = lane; t < Q * D1; t += 32) { // contract x: [qx][b]
-               const int qx = t / D1, b = t % D1;
+            // Every stage is row-wise: a lane per (element, row) loads the
+            // row once and runs the unrolled outputs along it with the basis
+            // operands as compile-time constant-bank operands (the
+            // per-output lane mapping was shared-memory bound).
+            if (lane < GRP * D1) { // contract x: T[qx][b], a lane per (e, b)
+               const int j = lane / D1, b = lane % D1;
+               const double *V = sm.V[vb] + j * ND;
+               double v[D1];
 #pragma unroll
-               for (int j = 0; j < GRP; j++) {
-                  const double *V = sm.V[vb] + j * ND;
-                  double s1 = mul<EXACT>(sG[qx][0], V[b]);
-                  double s2 = mul<EXACT>(sB[qx][0], V[b]);
+               for (int kk = 0; kk < D1; kk++) v[kk] = V[kk * D1 + b];
+#pragma unroll
+               for (int qx = 0; qx < Q; qx++) {
+                  double s1 = mul<EXACT>(a.t.G[qx][0], v[0]);
+                  double s2 = mul<EXACT>(a.t.B[qx][0], v[0]);
 #pragma unroll
                   for (int kk = 1; kk < D1; kk++) {
-                     if (KIND == TFEM_DIFFUSION) s1 = mac<EXACT>(s1, sG[qx][kk], V[kk * D1 + b]);
-                     s2 = mac<EXACT>(s2, sB[qx][kk], V[kk * D1 + b]);
+                     if (KIND == TFEM_DIFFUSION) s1 = mac<EXACT>(s1, a.t.G[qx][kk], v[kk]);
+                     s2 = mac<EXACT>(s2, a.t.B[qx][kk], v[kk]);
                   }
-                  sm.T1[j][t] = s1;
-                  sm.T2[j][t] = s2;
+                  if (KIND == TFEM_DIFFUSION) sm.T1[j][qx * D1 + b] = s1;
+                  sm.T2[j][qx * D1 + b] = s2;
                }
             }
             prefetch_x(gn, gnext, vb ^ 1); // the other V buffer is free
             load_mask(gn, gnext, mnext);
             __syncwarp();
-            for (int t = lane; t < NQD; t += 32) { // contract y, point factors: [qx][qy]
-               const int qx = t % Q, qy = t / Q;
+            if (lane < GRP * Q) { // contract y, point factors: W[qx][qy], a lane per (e, qx)
+               const int j = lane / Q, qx = lane % Q;
+               const double *qd = qs + j * NC * NQD;
+               const bool live = j < cnt;
+               double t1[D1], t2[D1];
 #pragma unroll
-               for (int j = 0; j < GRP; j++) {
-                  const double *qd = qs + j * NC * NQD;
-                  const bool live = j < cnt;
+               for (int b = 0; b < D1; b++) {
+                  if (KIND == TFEM_DIFFUSION) t1[b] = sm.T1[j][qx * D1 + b];
+                  t2[b] = sm.T2[j][qx * D1 + b];
+               }
+#pragma unroll
+               for (int qy = 0; qy < Q; qy++) {
+                  const int t = qy * Q + qx;
                   if (KIND == TFEM_DIFFUSION) {
-                     double dx = mul<EXACT>(sm.T1[j][qx * D1], sB[qy][0]);
-                     double dy = mul<EXACT>(sm.T2[j][qx * D1], sG[qy][0]);
+                     double dx = mul<EXACT>(t1[0], a.t.B[qy][0]);
+                     double dy = mul<EXACT>(t2[0], a.t.G[qy][0]);
 #pragma unroll
                      for (int b = 1; b < D1; b++) {
-                        dx = mac<EXACT>(dx, sm.T1[j][qx * D1 + b], sB[qy][b]);
-                        dy = mac<EXACT>(dy, sm.T2[j][qx * D1 + b], sG[qy][b]);
+                        dx = mac<EXACT>(dx, t1[b], a.t.B[qy][b]);
+                        dy = mac<EXACT>(dy, t2[b], a.t.G[qy][b]);
                      }
                      const double d0 = qd[t], d1 = qd[NQD + t], d2 = qd[2 * NQD + t];
                      const double w1 = add<EXACT>(mul<EXACT>(d0, dx), mul<EXACT>(d1, dy));
@@ -207,9 +217,9 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
                      sm.W1[j][qx * Q + qy] = w1;
                      sm.W2[j][qx * Q + qy] = w2;
                   } else {
-                     double u = mul<EXACT>(sm.T2[j][qx * D1], sB[qy][0]);
+                     double u = mul<EXACT>(t2[0], a.t.B[qy][0]);
 #pragma unroll
-                     for (int b = 1; b < D1; b++) u = mac<EXACT>(u, sm.T2[j][qx * D1 + b], sB[qy][b]);
+                     for (int b = 1; b < D1; b++) u = mac<EXACT>(u, t2[b], a.t.B[qy][b]);
                      const double w = mul<EXACT>(u, qd[t]);
                      if (EDOT && live) dot = mac<EXACT>(dot, u, w);
                      sm.W2[j][qx * Q + qy] = w;
@@ -218,58 +228,62 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
-            for (int t = lane; t < D1 * Q; t += 32) { // contract qx: [a][qy]
-               const int i = t / Q, qy = t % Q;
+            if (lane < GRP * Q) { // contract qx: S[a][qy], a lane per (e, qy)
+               const int j = lane / Q, qy = lane % Q;
+               double w1[Q], w2[Q];
 #pragma unroll
-               for (int j = 0; j < GRP; j++) {
+               for (int qx = 0; qx < Q; qx++) {
+                  if (KIND == TFEM_DIFFUSION) w1[qx] = sm.W1[j][qx * Q + qy];
+                  w2[qx] = sm.W2[j][qx * Q + qy];
+               }
+#pragma unroll
+               for (int i = 0; i < D1; i++) {
                   if (KIND == TFEM_DIFFUSION) {
-                     double s1 = mul<EXACT>(sG[0][i], sm.W1[j][qy]);
-                     double s2 = mul<EXACT>(sB[0][i], sm.W2[j][qy]);
+                     double s1 = mul<EXACT>(a.t.G[0][i], w1[0]);
+                     double s2 = mul<EXACT>(a.t.B[0][i], w2[0]);
 #pragma unroll
                      for (int qx = 1; qx < Q; qx++) {
-                        s1 = mac<EXACT>(s1, sG[qx][i], sm.W1[j][qx * Q + qy]);
-                        s2 = mac<EXACT>(s2, sB[qx][i], sm.W2[j][qx * Q + qy]);
+                        s1 = mac<EXACT>(s1, a.t.G[qx][i], w1[qx]);
+                        s2 = mac<EXACT>(s2, a.t.B[qx][i], w2[qx]);
                      }
-                     sm.S1[j][t] = s1;
-                     sm.S2[j][t] = s2;
+                     sm.S1[j][i * Q + qy] = s1;
+                     sm.S2[j][i * Q + qy] = s2;
                   } else {
-                     double sv = mul<EXACT>(sB[0][i], sm.W2[j][qy]);
+                     double sv = mul<EXACT>(a.t.B[0][i], w2[0]);
 #pragma unroll
-                     for (int qx = 1; qx < Q; qx++) sv = mac<EXACT>(sv, sB[qx][i], sm.W2[j][qx * Q + qy]);
-                     sm.S2[j][t] = sv;
+                     for (int qx = 1; qx < Q; qx++) sv = mac<EXACT>(sv, a.t.B[qx][i], w2[qx]);
+                     sm.S2[j][i * Q + qy] = sv;
                   }
                }
             }
             __syncwarp();
+            if (lane < cnt * D1) { // contract qy: r(a, b), a lane per (e, a); epilogue
+               const int j = lane / D1, ia = lane % D1;
+               double s1[Q], s2[Q];
 #pragma unroll
-            for (int m = 0; m < (ND + 31) / 32; m++) { // contract qy: r(a, b)
-               const int t = lane + 32 * m;
-               if (t >= ND) continue;
-               const int ia = t % D1, b = t / D1;
-               double r[GRP];
+               for (int qy = 0; qy < Q; qy++) {
+                  if (KIND == TFEM_DIFFUSION) s1[qy] = sm.S1[j][ia * Q + qy];
+                  s2[qy] = sm.S2[j][ia * Q + qy];
+               }
+               const int64_t e = g * GRP + j;
 #pragma unroll
-               for (int j = 0; j < GRP; j++) {
+               for (int b = 0; b < D1; b++) {
+                  double rr;
                   if (KIND == TFEM_DIFFUSION) {
-                     double vx = mul<EXACT>(sm.S1[j][ia * Q], sB[0][b]);
-                     double vy = mul<EXACT>(sm.S2[j][ia * Q], sG[0][b]);
+                     double vx = mul<EXACT>(s1[0], a.t.B[0][b]);
+                     double vy = mul<EXACT>(s2[0], a.t.G[0][b]);
 #pragma unroll
                      for (int qy = 1; qy < Q; qy++) {
-                        vx = mac<EXACT>(vx, sm.S1[j][ia * Q + qy], sB[qy][b]);
-                        vy = mac<EXACT>(vy, sm.S2[j][ia * Q + qy], sG[qy][b]);
+                        vx = mac<EXACT>(vx, s1[qy], a.t.B[qy][b]);
+                        vy = mac<EXACT>(vy, s2[qy], a.t.G[qy][b]);
                      }
-                     r[j] = add<EXACT>(vx, vy);
+                     rr = add<EXACT>(vx, vy);
                   } else {
-                     double rv = mul<EXACT>(sm.S2[j][ia * Q], sB[0][b]);
+                     rr = mul<EXACT>(s2[0], a.t.B[0][b]);
 #pragma unroll
-                     for (int qy = 1; qy < Q; qy++) rv = mac<EXACT>(rv, sm.S2[j][ia * Q + qy], sB[qy][b]);
-                     r[j] = rv;
+                     for (int qy = 1; qy < Q; qy++) rr = mac<EXACT>(rr, s2[qy], a.t.B[qy][b]);
                   }
-               }
-#pragma unroll
-               for (int j = 0; j < GRP; j++) {
-                  if (j >= cnt) continue;
-                  const int64_t e = g * GRP + j;
-                  double rr = r[j];
+                  const int t = ia + D1 * b;
                   const uint32_t gg = sm.gm[j * ND + t];
                   if (is_exclusive(gg)) {
                      const uint32_t d = gg & kDofMask;
