@@ -25,7 +25,10 @@ template <int P, int Q, int KIND>
 struct alignas(16) Warp2 {
    static constexpr int D1 = P + 1, ND = D1 * D1, NQD = Q * Q;
    static constexpr int NC = KIND == TFEM_MASS ? 1 : 3;
-   static constexpr int GRP = P <= 6 ? 4 : 2; // elements per slot, in lockstep
+   // elements per slot, in lockstep: as many rows of the widest stage as
+   // fit one warp, even (whole 16-byte qdata copies)
+   static constexpr int kRow = D1 > Q ? D1 : Q;
+   static constexpr int GRP = (32 / kRow) / 2 * 2 > 2 ? (32 / kRow) / 2 * 2 : 2;
    static constexpr int kSlots = 2;
    double q[kSlots][GRP * NC * NQD];
    double V[2][GRP * ND];             // [e][a * D1 + b]
