@@ -177,18 +177,25 @@ __global__ void apply3d_kernel(const ApplyArgs a)
       }
    }
    __syncthreads();
-   if (live) { // contract a -> TB / TG [c][b][qx]
-      for (int j = t; j < D1 * D1 * Q; j += NT) {
-         const int qx = j % Q, cb = j / Q;
-         double sb = 0.0, sg = 0.0;
+   // The contractions between the column stage and the element's ends are
+   // row-wise: a thread per row loads it once and runs the unrolled outputs
+   // with the basis operands from the constant bank.
+   if (live) { // contract a -> TB / TG [c][b][qx]: a thread per (c, b)
+      for (int cb = t; cb < D1 * D1; cb += NT) {
+         double v[D1];
 #pragma unroll
-         for (int k = 0; k < D1; k++) {
-            const double v = sm.V[cb * D1 + k];
-            sb = fma(sB[qx][k], v, sb);
-            if (KIND == TFEM_DIFFUSION) sg = fma(sG[qx][k], v, sg);
+         for (int k = 0; k < D1; k++) v[k] = sm.V[cb * D1 + k];
+#pragma unroll
+         for (int qx = 0; qx < Q; qx++) {
+            double sb = 0.0, sg = 0.0;
+#pragma unroll
+            for (int k = 0; k < D1; k++) {
+               sb = fma(a.t.B[qx][k], v[k], sb);
+               if (KIND == TFEM_DIFFUSION) sg = fma(a.t.G[qx][k], v[k], sg);
+            }
+            sm.TB[cb * Q + qx] = sb;
+            if (KIND == TFEM_DIFFUSION) sm.TG[cb * Q + qx] = sg;
          }
-         sm.TB[j] = sb;
-         sm.TG[j] = sg;
       }
    }
    __syncthreads();
@@ -222,17 +229,17 @@ __global__ void apply3d_kernel(const ApplyArgs a)
          if (KIND == TFEM_MASS) {
             double u = 0.0;
 #pragma unroll
-            for (int c = 0; c < D1; c++) u = fma(sB[qz][c], UBB[c], u);
+            for (int c = 0; c < D1; c++) u = fma(a.t.B[qz][c], UBB[c], u);
             const double w = u * __ldg(qd + q);
 #pragma unroll
-            for (int c = 0; c < D1; c++) Px[c] = fma(sB[qz][c], w, Px[c]);
+            for (int c = 0; c < D1; c++) Px[c] = fma(a.t.B[qz][c], w, Px[c]);
          } else {
             double ux = 0.0, uy = 0.0, uz = 0.0;
 #pragma unroll
             for (int c = 0; c < D1; c++) {
-               ux = fma(sB[qz][c], UGB[c], ux);
-               uy = fma(sB[qz][c], UBG[c], uy);
-               uz = fma(sG[qz][c], UBB[c], uz);
+               ux = fma(a.t.B[qz][c], UGB[c], ux);
+               uy = fma(a.t.B[qz][c], UBG[c], uy);
+               uz = fma(a.t.G[qz][c], UBB[c], uz);
             }
             const double D00 = __ldg(qd + q), D01 = __ldg(qd + NQD + q);
             const double D02 = __ldg(qd + 2 * NQD + q), D11 = __ldg(qd + 3 * NQD + q);
@@ -242,9 +249,9 @@ __global__ void apply3d_kernel(const ApplyArgs a)
             const double wz = fma(D22, uz, fma(D12, uy, D02 * ux));
 #pragma unroll
             for (int c = 0; c < D1; c++) {
-               Px[c] = fma(sB[qz][c], wx, Px[c]);
-               Py[c] = fma(sB[qz][c], wy, Py[c]);
-               Pz[c] = fma(sG[qz][c], wz, Pz[c]);
+               Px[c] = fma(a.t.B[qz][c], wx, Px[c]);
+               Py[c] = fma(a.t.B[qz][c], wy, Py[c]);
+               Pz[c] = fma(a.t.G[qz][c], wz, Pz[c]);
             }
          }
       }
@@ -258,47 +265,70 @@ __global__ void apply3d_kernel(const ApplyArgs a)
       }
    }
    __syncthreads();
-   if (live) { // contract qy -> [c][b][qx] (x-gradient part in TB, rest in TG)
-      for (int j = t; j < D1 * D1 * Q; j += NT) {
-         const int jx = j % Q, cb = j / Q, b = cb % D1, c = cb / D1;
-         double sx = 0.0, syz = 0.0;
+   // contract qy -> [c][b][qx] (x-gradient part in TB, rest in TG): a
+   // thread per (c, qx)
+   if (live) {
+      for (int j = t; j < D1 * Q; j += NT) {
+         const int jx = j % Q, c = j / Q;
+         double px[Q], py[Q], pz[Q];
 #pragma unroll
          for (int y = 0; y < Q; y++) {
             const int o = (c * Q + y) * Q + jx;
-            sx = fma(sB[y][b], sm.Px[o], sx);
+            px[y] = sm.Px[o];
             if (KIND == TFEM_DIFFUSION) {
-               syz = fma(sG[y][b], sm.Py[o], syz);
-               syz = fma(sB[y][b], sm.Pz[o], syz);
+               py[y] = sm.Py[o];
+               pz[y] = sm.Pz[o];
             }
          }
-         sm.TB[j] = sx;
-         sm.TG[j] = syz;
+#pragma unroll
+         for (int b = 0; b < D1; b++) {
+            double sx = 0.0, syz = 0.0;
+#pragma unroll
+            for (int y = 0; y < Q; y++) {
+               sx = fma(a.t.B[y][b], px[y], sx);
+               if (KIND == TFEM_DIFFUSION) {
+                  syz = fma(a.t.G[y][b], py[y], syz);
+                  syz = fma(a.t.B[y][b], pz[y], syz);
+               }
+            }
+            sm.TB[(c * D1 + b) * Q + jx] = sx;
+            if (KIND == TFEM_DIFFUSION) sm.TG[(c * D1 + b) * Q + jx] = syz;
+         }
       }
    }
    __syncthreads();
    double dot = 0.0;
-   if (live) { // contract qx -> r(a, b, c)
-      for (int i = t; i < ND; i += NT) {
-         const int ia = i % D1, cb = i / D1;
-         double r = 0.0;
+   if (live) { // contract qx -> r(a, b, c): a thread per (c, b)
+      for (int cb = t; cb < D1 * D1; cb += NT) {
+         double tb[Q], tg[Q];
 #pragma unroll
          for (int x = 0; x < Q; x++) {
-            if (KIND == TFEM_MASS) {
-               r = fma(sB[x][ia], sm.TB[cb * Q + x], r);
-            } else {
-               r = fma(sG[x][ia], sm.TB[cb * Q + x], r);
-               r = fma(sB[x][ia], sm.TG[cb * Q + x], r);
-            }
+            tb[x] = sm.TB[cb * Q + x];
+            if (KIND == TFEM_DIFFUSION) tg[x] = sm.TG[cb * Q + x];
          }
-         const uint32_t gg = __ldg(gm + i);
-         if (is_exclusive(gg)) {
-            const uint32_t d = gg & kDofMask;
-            if (!a.overwrite) r += a.y[d];
-            if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
-            a.y[d] = r;
-            if (a.dot && !(a.notown && bit_set(a.notown, d))) dot = fma(__ldg(a.x + d), r, dot);
-         } else {
-            a.evec[ev_em(ND, a.ne_pad, e, i)] = r;
+#pragma unroll
+         for (int ia = 0; ia < D1; ia++) {
+            const int i = cb * D1 + ia;
+            double r = 0.0;
+#pragma unroll
+            for (int x = 0; x < Q; x++) {
+               if (KIND == TFEM_MASS) {
+                  r = fma(a.t.B[x][ia], tb[x], r);
+               } else {
+                  r = fma(a.t.G[x][ia], tb[x], r);
+                  r = fma(a.t.B[x][ia], tg[x], r);
+               }
+            }
+            const uint32_t gg = __ldg(gm + i);
+            if (is_exclusive(gg)) {
+               const uint32_t d = gg & kDofMask;
+               if (!a.overwrite) r += a.y[d];
+               if (a.ess_out && bit_set(a.ess_out, d)) r = __ldg(a.x + d);
+               a.y[d] = r;
+               if (a.dot && !(a.notown && bit_set(a.notown, d))) dot = fma(__ldg(a.x + d), r, dot);
+            } else {
+               a.evec[ev_em(ND, a.ne_pad, e, i)] = r;
+            }
          }
       }
    }
