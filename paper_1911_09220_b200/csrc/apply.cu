@@ -18,6 +18,7 @@ namespace tfem {
 namespace {
 
 constexpr int kScatterThreads = 256;
+constexpr int kScatterRows = 4; // rows per thread: all their loads in flight together
 
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
@@ -57,29 +58,55 @@ __device__ __forceinline__ void load_row(const uint32_t *__restrict__ row, uint3
    }
 }
 
+// Rows s0 + k * kScatterThreads (k < kScatterRows) of bucket b: every load
+// of the rows is issued before the first sum.
 template <bool EXACT, int C>
-__device__ __forceinline__ double scatter_row(const BucketArgs &B, int b, int64_t s,
-                                              const double *__restrict__ evec,
-                                              const double *__restrict__ x, double *y,
-                                              int overwrite, const uint32_t *ess_out, bool want_dot,
-                                              const uint32_t *notown, bool ess_only)
+__device__ __forceinline__ double scatter_rows(const BucketArgs &B, int b, int64_t s0,
+                                               const double *__restrict__ evec,
+                                               const double *__restrict__ x, double *y,
+                                               int overwrite, const uint32_t *ess_out,
+                                               bool want_dot, const uint32_t *notown, bool ess_only)
 {
-   const int32_t d = __ldg(B.dofs[b] + s);
-   uint32_t sl[C];
-   load_row<C>(B.slots[b] + s * C, sl);
-   double v[C];
+   constexpr int R = kScatterRows;
+   const int64_t n = B.n[b];
+   int32_t d[R];
+   uint32_t sl[R][C];
+   double v[R][C];
+   uint32_t ew[R];
 #pragma unroll
-   for (int k = 0; k < C; k++) v[k] = __ldg(evec + sl[k]);
-   double acc = overwrite ? v[0] : add<EXACT>(y[d], v[0]);
+   for (int k = 0; k < R; k++) {
+      const int64_t s = s0 + k * kScatterThreads;
+      if (s < n) {
+         d[k] = __ldg(B.dofs[b] + s);
+         load_row<C>(B.slots[b] + s * C, sl[k]);
+      }
+   }
 #pragma unroll
-   for (int k = 1; k < C; k++) acc = add<EXACT>(acc, v[k]);
-   const bool es = ess_out && bit_set(ess_out, d);
-   if (es) acc = __ldg(x + d);
-   y[d] = acc;
-   // ess_only: the element kernel took x . y as element energies; only the
-   // essential DOFs' x_d^2 is missing
-   if (ess_only) return want_dot && es ? mul<EXACT>(acc, acc) : 0.0;
-   return want_dot && !(notown && bit_set(notown, d)) ? mul<EXACT>(__ldg(x + d), acc) : 0.0;
+   for (int k = 0; k < R; k++) {
+      if (s0 + k * kScatterThreads >= n) continue;
+#pragma unroll
+      for (int c = 0; c < C; c++) v[k][c] = __ldg(evec + sl[k][c]);
+      ew[k] = ess_out ? __ldg(ess_out + (static_cast<uint32_t>(d[k]) >> 5)) : 0u;
+   }
+   double dv = 0.0;
+#pragma unroll
+   for (int k = 0; k < R; k++) {
+      if (s0 + k * kScatterThreads >= n) continue;
+      double acc = overwrite ? v[k][0] : add<EXACT>(y[d[k]], v[k][0]);
+#pragma unroll
+      for (int c = 1; c < C; c++) acc = add<EXACT>(acc, v[k][c]);
+      const bool es = (ew[k] >> (d[k] & 31)) & 1u;
+      if (es) acc = __ldg(x + d[k]);
+      y[d[k]] = acc;
+      // ess_only: the element kernel took x . y as element energies; only
+      // the essential DOFs' x_d^2 is missing
+      if (ess_only) {
+         if (want_dot && es) dv = add<EXACT>(dv, mul<EXACT>(acc, acc));
+      } else if (want_dot && !(notown && bit_set(notown, d[k]))) {
+         dv = add<EXACT>(dv, mul<EXACT>(__ldg(x + d[k]), acc));
+      }
+   }
+   return dv;
 }
 
 template <bool EXACT>
@@ -91,18 +118,19 @@ scatter_kernel(const BucketArgs B, const double *__restrict__ evec, const double
    if (done && *done) return;
    int b = 0;
    while (b + 1 < B.nb && (int64_t)blockIdx.x >= B.start[b + 1]) b++;
-   const int64_t s = ((int64_t)blockIdx.x - B.start[b]) * kScatterThreads + threadIdx.x;
+   const int64_t s = ((int64_t)blockIdx.x - B.start[b]) * (kScatterThreads * kScatterRows) +
+                     threadIdx.x;
    double dv = 0.0;
    if (s < B.n[b]) {
       const bool wd = static_cast<bool>(dot), eo = ess_only != 0;
       switch (B.c[b]) {
-      case 2: dv = scatter_row<EXACT, 2>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
-      case 3: dv = scatter_row<EXACT, 3>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
-      case 4: dv = scatter_row<EXACT, 4>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
-      case 5: dv = scatter_row<EXACT, 5>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
-      case 6: dv = scatter_row<EXACT, 6>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
-      case 7: dv = scatter_row<EXACT, 7>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
-      case 8: dv = scatter_row<EXACT, 8>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 2: dv = scatter_rows<EXACT, 2>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 3: dv = scatter_rows<EXACT, 3>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 4: dv = scatter_rows<EXACT, 4>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 5: dv = scatter_rows<EXACT, 5>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 6: dv = scatter_rows<EXACT, 6>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 7: dv = scatter_rows<EXACT, 7>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
+      case 8: dv = scatter_rows<EXACT, 8>(B, b, s, evec, x, y, overwrite, ess_out, wd, notown, eo); break;
       }
    }
    if (dot) {
@@ -124,7 +152,7 @@ BucketArgs bucket_args(const tfem_restriction *r, bool global_only)
       B.dofs[b] = bk[b].dofs;
       B.slots[b] = bk[b].slots;
       B.start[b] = blk;
-      blk += blocks_for(bk[b].n, kScatterThreads);
+      blk += blocks_for(bk[b].n, kScatterThreads * kScatterRows);
    }
    B.start[nb] = blk;
    return B;
