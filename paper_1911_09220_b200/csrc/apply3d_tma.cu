@@ -64,8 +64,11 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    constexpr int NT = D1 * D1 * Q;         // contraction outputs per element
    constexpr int GPL = (EPW * ND + 31) / 32; // map entries per lane
    // row-wise contractions (basis operands compile-time) when a warp covers
-   // the rows in one pass; measured slower at q = 7 (two passes, spills)
-   constexpr bool kRows = EPW * D1 * D1 <= 32 && EPW * Q * D1 <= 32;
+   // the rows in one pass, or two at q <= 6 (BP5 p=5 +7 %); measured slower
+   // at q = 7 (two passes, spills)
+   constexpr int kRowMax = Q <= 6 ? 64 : 32;
+   constexpr bool kRows1 = EPW * D1 * D1 <= kRowMax; // stages a and x
+   constexpr bool kRows3 = EPW * Q * D1 <= kRowMax;  // stage y
    constexpr unsigned kQBytes = NC * NQD * 8;
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          // contract a -> TB / TG [e][c][b][qx]: a lane per (e, c, b) row, qx
          // unrolled (basis operands from the constant bank) when the rows
          // fit one pass of the warp; else a lane per output
-         if constexpr (!kRows) {
+         if constexpr (!kRows1) {
             for (int jj = lane; jj < EPW * NT; jj += 32) {
                const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q;
                double sb = 0.0, sg = 0.0;
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          if (lane == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
          // contract qy -> [e][c][b][qx] (x-gradient part in TB, y + z in TG):
          // a lane per (e, c, qx), b unrolled (or a lane per output)
-         if constexpr (!kRows) {
+         if constexpr (!kRows3) {
             for (int jj = lane; jj < EPW * NT; jj += 32) {
                const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q, b = cb % D1, c = cb / D1;
                const int po = j * D1 * Q * Q;
@@ -339,9 +342,9 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          __syncwarp();
          // contract qx -> r(a, b, c) and the epilogue: a lane per (e, c, b),
          // a unrolled (or a lane per output)
-         constexpr int kA = kRows ? D1 : 1; // outputs per work item
+         constexpr int kA = kRows1 ? D1 : 1; // outputs per work item
          for (int it = lane; it < cnt * ND / kA; it += 32) {
-            const int j = it / (ND / kA), cb = kRows ? it % (D1 * D1) : (it % ND) / D1;
+            const int j = it / (ND / kA), cb = kRows1 ? it % (D1 * D1) : (it % ND) / D1;
             double tb[Q], tg[Q];
 #pragma unroll
             for (int x = 0; x < Q; x++) {
@@ -351,12 +354,12 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             const int64_t e = g * EPW + j;
 #pragma unroll
             for (int ka = 0; ka < kA; ka++) {
-               const int ia = kRows ? ka : it % D1;
+               const int ia = kRows1 ? ka : it % D1;
                double r = 0.0;
 #pragma unroll
                for (int x = 0; x < Q; x++) {
-                  const double gx = kRows ? a.t.G[x][ka] : sG[x][ia];
-                  const double bx = kRows ? a.t.B[x][ka] : sB[x][ia];
+                  const double gx = kRows1 ? a.t.G[x][ka] : sG[x][ia];
+                  const double bx = kRows1 ? a.t.B[x][ka] : sB[x][ia];
                   if (KIND == TFEM_MASS) {
                      r = fma(bx, tb[x], r);
                   } else {
