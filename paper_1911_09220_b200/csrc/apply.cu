@@ -18,7 +18,8 @@ namespace tfem {
 namespace {
 
 constexpr int kScatterThreads = 256;
-constexpr int kScatterRows = 4; // rows per thread: all their loads in flight together
+constexpr int kScatterRows = 4;      // rows per thread: all their loads in flight together
+constexpr int kScatterMinBlocks = 4; // <= 64 registers: occupancy for the gathers (+1-2 %)
 
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
@@ -110,7 +111,7 @@ __device__ __forceinline__ double scatter_rows(const BucketArgs &B, int b, int64
 }
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kScatterThreads)
+__global__ void __launch_bounds__(kScatterThreads, kScatterMinBlocks)
 scatter_kernel(const BucketArgs B, const double *__restrict__ evec, const double *__restrict__ x,
                double *y, int overwrite, const uint32_t *ess_out, DotSink dot, const int *done,
                const uint32_t *notown, int ess_only)
