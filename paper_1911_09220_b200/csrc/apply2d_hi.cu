@@ -21,6 +21,28 @@ namespace tfem {
 
 namespace {
 
+// Row strides padded against shared-memory bank conflicts of the row-wise
+// stages (64-bit accesses, half-warp phases; chosen by an exhaustive search
+// of the stage access patterns).  qdata is padded per element only when an
+// element's point factors are whole 16-byte units (even q), one bulk copy
+// per element then (measured: +8 % at q = 8; the smaller copies of q = 6
+// cost 20 %, q = 10 6 %).
+constexpr int pad_q(int Q) { return Q == 8 ? 8 : 0; }
+constexpr int pad_t(int P, int Q)
+{
+   return (P == 4 && Q == 6) ? 5 : (P == 5 && Q == 6) ? 3 : (P == 5 && Q == 7) ? 1
+        : (P == 6 && Q == 7) ? 7 : (P == 7 && Q == 9) ? 1 : 0;
+}
+constexpr int pad_w(int P, int Q)
+{
+   return (P == 4 && Q == 6) ? 3 : (P == 5 && Q == 6) ? 3 : (P == 5 && Q == 7) ? 7
+        : (P == 6 && Q == 7) ? 7 : (P == 6 && Q == 8) ? 1 : 0;
+}
+constexpr int pad_s(int P, int Q)
+{
+   return (P == 5 && Q == 6) ? 3 : (P == 6 && Q == 7) ? 7 : (P == 6 && Q == 8) ? 1 : 0;
+}
+
 template <int P, int Q, int KIND>
 struct alignas(16) Warp2 {
    static constexpr int D1 = P + 1, ND = D1 * D1, NQD = Q * Q;
@@ -30,11 +52,14 @@ struct alignas(16) Warp2 {
    static constexpr int kRow = D1 > Q ? D1 : Q;
    static constexpr int GRP = (32 / kRow) / 2 * 2 > 2 ? (32 / kRow) / 2 * 2 : 2;
    static constexpr int kSlots = 2;
-   double q[kSlots][GRP * NC * NQD];
-   double V[2][GRP * ND];             // [e][a * D1 + b]
-   double T1[GRP][Q * D1], T2[GRP][Q * D1]; // [e][qx][b]
-   double W1[GRP][Q * Q], W2[GRP][Q * Q];   // [e][qx][qy]
-   double S1[GRP][D1 * Q], S2[GRP][D1 * Q]; // [e][a][qy]
+   static constexpr int kQe = NC * NQD + ((NC * NQD) % 2 == 0 ? pad_q(Q) : 0); // element stride
+   static constexpr bool kPerElem = kQe != NC * NQD; // one bulk copy per element
+   static constexpr int kT = Q * D1 + pad_t(P, Q), kW2 = Q * Q + pad_w(P, Q), kS = D1 * Q + pad_s(P, Q);
+   double q[kSlots][GRP * kQe];
+   double V[2][GRP * ND];           // [e][a * D1 + b]
+   double T1[GRP][kT], T2[GRP][kT]; // [e][qx][b]
+   double W1[GRP][kW2], W2[GRP][kW2]; // [e][qx][qy]
+   double S1[GRP][kS], S2[GRP][kS];   // [e][a][qy]
    uint32_t gm[GRP * ND];                   // the slot's map entries, for the epilogue
    uint8_t es[GRP * ND];                    // ... and their essential flags (ess_out)
    uint64_t full[kSlots], empty[kSlots];
@@ -94,9 +119,16 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
                   mbar_wait(&ws[w].empty[s], static_cast<unsigned>((k / kSlots - 1) & 1));
                // a partial last pair still copies whole 16-byte units: the
                // padded qdata allocation (ne_pad) covers the tail
-               const unsigned bytes = (kQBytes * cnt + 15u) & ~15u;
-               mbar_expect_tx(&ws[w].full[s], bytes);
-               bulk_g2s(ws[w].q[s], a.qdata + g * GRP * (int64_t)(NC * NQD), bytes, &ws[w].full[s]);
+               if constexpr (W::kPerElem) {
+                  mbar_expect_tx(&ws[w].full[s], kQBytes * cnt);
+                  for (int e = 0; e < cnt; e++)
+                     bulk_g2s(ws[w].q[s] + e * W::kQe, a.qdata + (g * GRP + e) * (int64_t)(NC * NQD),
+                              kQBytes, &ws[w].full[s]);
+               } else {
+                  const unsigned bytes = (kQBytes * cnt + 15u) & ~15u;
+                  mbar_expect_tx(&ws[w].full[s], bytes);
+                  bulk_g2s(ws[w].q[s], a.qdata + g * GRP * (int64_t)(NC * NQD), bytes, &ws[w].full[s]);
+               }
             }
             if (!any) break;
          }
@@ -194,7 +226,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
             __syncwarp();
             if (lane < GRP * Q) { // contract y, point factors: W[qx][qy], a lane per (e, qx)
                const int j = lane / Q, qx = lane % Q;
-               const double *qd = qs + j * NC * NQD;
+               const double *qd = qs + j * W::kQe;
                const bool live = j < cnt;
                double t1[D1], t2[D1];
 #pragma unroll
