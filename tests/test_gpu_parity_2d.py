@@ -152,6 +152,27 @@ def test_constrained_operator_bitwise(dev, p):
 
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 6])
+def test_constrained_two_integrators_bitwise(dev, p):
+    """Essential DOFs with two integrators: the first gathers with the mask
+    and leaves y[ess] alone, the last sets y[ess] = x[ess] (the per-position
+    essential words of the element kernels with mask_in != ess_out)."""
+    rs = RefSpace.cartesian(8, 7, p)
+    f = RefForm(rs, [("diffusion", "varying", 0.0), ("mass", "const", 2.0)])
+    rsys = RefSystem(f, "front")
+    sp = tf.FeSpace.cartesian(dev, (8, 7), p)
+    a = tf.BilinearForm(sp)
+    a.add_diffusion(varying)
+    a.add_mass(2.0)
+    a.assemble()
+    op = tf.ConstrainedOperator(a, sp.essential_true_dofs())
+    x = rng_vec(sp.n_dofs, 13 + p)
+    y = tf.Vector(dev, sp.n_dofs)
+    op.mult(x, y)
+    assert (y.numpy() == rsys.op_mult(x)).all()
+    assert (op.diagonal().numpy() == rsys.diag).all()
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 6])
 @pytest.mark.parametrize("jacobi", [True, False])
 def test_cg_front_iterations_match(dev, p, jacobi):
     """Driver system (front solution, tol 1e-12): same iteration count as the
