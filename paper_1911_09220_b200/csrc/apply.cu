@@ -167,7 +167,7 @@ BucketArgs bucket_args(const tfem_restriction *r, bool global_only)
 template <int DIM>
 __global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne, int64_t ne_pad,
                             const double *__restrict__ qdata, const uint32_t *gmap,
-                            int elem_major, double *evec, double *y)
+                            int elem_major, const uint16_t *evperm, double *evec, double *y)
 {
    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; // position
    const int i = blockIdx.y;
@@ -224,7 +224,7 @@ __global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne,
       const uint32_t d = g & kDofMask;
       y[d] = __dadd_rn(y[d], s);
    } else {
-      evec[elem_major ? ev_em(nd, ne_pad, e, i) : (int64_t)i * ne_pad + e] = s;
+      evec[elem_major ? ev_em_p(evperm, nd, e, i) : (int64_t)i * ne_pad + e] = s;
    }
 }
 
@@ -350,6 +350,7 @@ void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const
    a.x = x;
    a.y = y;
    a.evec = r->needs_evec() ? const_cast<tfem_restriction *>(r)->ensure_evec() : nullptr;
+   a.evperm = r->evperm;
    a.overwrite = f.overwrite ? 1 : 0;
    a.mask_in = f.mask_in;
    a.ess_out = f.ess_out;
@@ -380,10 +381,10 @@ void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, do
    const int elem_major = pa->elem_major() ? 1 : 0;
    if (pa->dim == 2)
       diag_kernel<2><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->npos, pa->ne_pad,
-                                                 pa->qdata, r->gmap, elem_major, evec, diag);
+                                                 pa->qdata, r->gmap, elem_major, r->evperm, evec, diag);
    else
       diag_kernel<3><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->npos, pa->ne_pad,
-                                                 pa->qdata, r->gmap, elem_major, evec, diag);
+                                                 pa->qdata, r->gmap, elem_major, r->evperm, evec, diag);
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
    if (r->n_shared > 0)

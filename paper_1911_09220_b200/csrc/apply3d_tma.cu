@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                      dot = fma(__ldg(a.x + d), r, dot);
                   }
                } else {
-                  a.evec[ev_em(ND, a.ne_pad, e, i)] = r;
+                  a.evec[ev_em_p(a.evperm, ND, e, i)] = r;
                }
             }
          }

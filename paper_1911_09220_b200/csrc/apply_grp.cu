@@ -327,7 +327,7 @@ __global__ void apply3d_kernel(const ApplyArgs a)
                a.y[d] = r;
                if (a.dot && !(a.notown && bit_set(a.notown, d))) dot = fma(__ldg(a.x + d), r, dot);
             } else {
-               a.evec[ev_em(ND, a.ne_pad, e, i)] = r;
+               a.evec[ev_em_p(a.evperm, ND, e, i)] = r;
             }
          }
       }

@@ -71,6 +71,14 @@ __host__ __device__ constexpr int64_t ev_em(int nd, int64_t /*ne_pad*/, int64_t 
    return e * nd + i;
 }
 
+// With a slot order (tfem_restriction::evperm: 3D, p >= 3) the E-vector keeps
+// each face's and edge's interior slots of an element contiguous, so the
+// scatter's reads of a face's DOFs share 32-byte sectors.
+__device__ __forceinline__ int64_t ev_em_p(const uint16_t *perm, int nd, int64_t e, int i)
+{
+   return e * nd + (perm ? static_cast<int>(__ldg(perm + i)) : i);
+}
+
 __host__ __device__ constexpr bool is_exclusive(uint32_t g) { return (g & kFlagMask) == kExclusive; }
 
 // Device element order (positions of the element map / qdata / E-vector).
@@ -197,6 +205,7 @@ struct tfem_restriction {
    // E-vector scratch (lazy) in the map's layout: slot-major [i][ne_pad],
    // element-major [e][nd] (ev_em); a slot indexes both
    double *evec = nullptr;
+   uint16_t *evperm = nullptr; // element-major 3D p >= 3: E-vector slot order (ev_em_p)
    bool cartesian = false;
    int n[3] = {0, 0, 0};
    double *ensure_evec();

@@ -20,6 +20,7 @@ struct ApplyArgs {
    const double *x;
    double *y;
    double *evec;
+   const uint16_t *evperm; // E-vector slot order of element-major 3D maps (or null)
    int overwrite;
    const uint32_t *mask_in;
    const uint32_t *ess_out;

@@ -248,13 +248,55 @@ __global__ void exclusive_add_kernel(const uint32_t *gmap, Layout L,
 }
 
 // API E-vector [e][i] -> internal gmap layout.
-__global__ void to_internal_kernel(Layout L, const double *api, double *evec)
+__global__ void to_internal_kernel(Layout L, const uint16_t *perm, const double *api, double *evec)
 {
    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
    if (t >= L.ne * L.nd) return;
    const int i = static_cast<int>(t % L.nd);
    const int64_t pos = L.order.pos_of(t / L.nd);
-   evec[L.elem_major ? ev_em(L.nd, L.ne_pad, pos, i) : (int64_t)i * L.ne_pad + pos] = api[t];
+   evec[L.elem_major ? ev_em_p(perm, L.nd, pos, i) : (int64_t)i * L.ne_pad + pos] = api[t];
+}
+
+// Bucket slots (map indices e nd + i) -> E-vector indices e nd + perm[i].
+__global__ void remap_slots_kernel(uint32_t *slots, int64_t n, int nd, const uint16_t *perm)
+{
+   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (k >= n) return;
+   const uint32_t s = slots[k];
+   slots[k] = (s / nd) * nd + perm[s % nd];
+}
+
+// TFEM_EVPERM=0 keeps the natural slot order (A/B).
+bool evperm_on()
+{
+   static const bool on = [] {
+      const char *v = std::getenv("TFEM_EVPERM");
+      return !(v && std::string(v) == "0");
+   }();
+   return on;
+}
+
+// 3D E-vector slot order inside an element: the (p-1)^3 interior slots, then
+// each face's (p-1)^2, each edge's p-1, the vertices -- sub-entities in
+// (c, b, a) class order (0 / interior / p), slots in natural order inside.
+std::vector<uint16_t> ev_perm_3d(int p)
+{
+   const int D1 = p + 1;
+   auto cls = [p](int x) { return x == 0 ? 0 : (x == p ? 2 : 1); };
+   std::vector<uint16_t> perm(D1 * D1 * D1);
+   int next = 0;
+   for (int m = 3; m >= 0; m--) // interior coordinates of the sub-entity
+      for (int kc = 0; kc < 3; kc++)
+         for (int kb = 0; kb < 3; kb++)
+            for (int ka = 0; ka < 3; ka++) {
+               if ((ka == 1) + (kb == 1) + (kc == 1) != m) continue;
+               for (int c = 0; c < D1; c++)
+                  for (int b = 0; b < D1; b++)
+                     for (int a = 0; a < D1; a++)
+                        if (cls(a) == ka && cls(b) == kb && cls(c) == kc)
+                           perm[a + D1 * (b + D1 * c)] = static_cast<uint16_t>(next++);
+            }
+   return perm;
 }
 
 
@@ -522,6 +564,11 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
       invalid("restriction: a DOF is shared by more than 8 elements");
    }
    TFEM_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * ndofs, s));
+   if (elem_major && r->dim == 3 && r->p >= 3 && evperm_on()) {
+      const std::vector<uint16_t> perm = ev_perm_3d(r->p);
+      r->evperm = dalloc<uint16_t>(r->nd);
+      h2d(s, r->evperm, perm.data(), sizeof(uint16_t) * perm.size());
+   }
    if (r->n_buckets > 0) {
       fill_slots_kernel<<<blocks_for(nslots), kThreads, 0, s>>>(gmap, L, bucket_of, rank, counts,
                                                                bp);
@@ -530,6 +577,12 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
          sort_rows_kernel<<<blocks_for(r->buckets[b].n), kThreads, 0, s>>>(
             r->buckets[b].slots, r->buckets[b].n, r->buckets[b].c, L);
          ctx->launched();
+         if (r->evperm) {
+            const int64_t m = r->buckets[b].n * r->buckets[b].c;
+            remap_slots_kernel<<<blocks_for(m), kThreads, 0, s>>>(r->buckets[b].slots, m, r->nd,
+                                                                  r->evperm);
+            ctx->launched();
+         }
          // element-major E-vector: rows in first-slot (element) order, so the
          // scatter's threads read neighbouring slots of the same elements
          if (elem_major) sort_rows_by_first_slot(ctx, r->buckets[b]);
@@ -555,7 +608,7 @@ void restriction_mult_transpose(tfem_ctx *ctx, const tfem_restriction *r, const 
    ctx->launched();
    if (r->n_shared > 0) {
       double *ev = const_cast<tfem_restriction *>(r)->ensure_evec();
-      to_internal_kernel<<<blocks_for(nslots), kThreads, 0, ctx->stream>>>(L, e, ev);
+      to_internal_kernel<<<blocks_for(nslots), kThreads, 0, ctx->stream>>>(L, r->evperm, e, ev);
       ctx->launched();
       scatter_shared(ctx, r, ev, nullptr, l, false, nullptr, nullptr, nullptr, false);
    }
@@ -647,6 +700,7 @@ void restriction_destroy(tfem_restriction *r)
 {
    if (!r) return;
    cudaFree(r->gmap);
+   cudaFree(r->evperm);
    for (int b = 0; b < r->n_buckets; b++) {
       cudaFree(r->buckets[b].dofs);
       cudaFree(r->buckets[b].slots);
@@ -710,7 +764,7 @@ void restriction_assign_last(tfem_ctx *ctx, const tfem_restriction *r, const dou
    ctx->launched();
    if (r->n_shared > 0) {
       double *ev = const_cast<tfem_restriction *>(r)->ensure_evec();
-      to_internal_kernel<<<blocks_for(nslots), kThreads, 0, ctx->stream>>>(L, e, ev);
+      to_internal_kernel<<<blocks_for(nslots), kThreads, 0, ctx->stream>>>(L, r->evperm, e, ev);
       ctx->launched();
       for (int b = 0; b < r->n_buckets; b++) {
          const auto &bk = r->buckets[b];
