@@ -30,6 +30,20 @@ namespace {
 template <int Q>
 constexpr int epw() { return 32 / (Q * Q) > 0 ? 32 / (Q * Q) : 1; }
 
+// Row strides of TB / TG ([e][c][b][qx], row = Q + kPadT) and of the P
+// planes ([e][c][qy][qx], plane = Q^2 + kPadP), padded against shared-memory
+// bank conflicts of the row-wise stages (exhaustive search of the access
+// patterns, 64-bit accesses in half-warp phases; measured slower at p = 5,
+// q = 6, where the larger rows cost a warp of occupancy).
+constexpr int pad_t3(int P, int Q)
+{
+   return (P == 2 && Q == 4) ? 3 : (P == 3 && Q == 4) ? 1 : (P == 4 && Q == 6) ? 1 : 0;
+}
+constexpr int pad_p3(int P, int Q)
+{
+   return (P == 2 && Q == 4) ? 4 : (P == 3 && Q == 4) ? 4 : (P == 4 && Q == 6) ? 2 : 0;
+}
+
 template <int P, int Q, int KIND>
 struct alignas(16) Warp3 {
    static constexpr int D1 = P + 1, ND = D1 * D1 * D1, NQD = Q * Q * Q;
@@ -38,8 +52,10 @@ struct alignas(16) Warp3 {
    static constexpr int kSlots = 2;
    double q[kSlots][EPW * NC * NQD];                  // the group's point factors
    double V[2][EPW * ND];                             // x of the open / next group
-   double TB[EPW * D1 * D1 * Q], TG[EPW * D1 * D1 * Q]; // [e][c][b][qx]
-   double Px[EPW * D1 * Q * Q], Py[EPW * D1 * Q * Q], Pz[EPW * D1 * Q * Q]; // [e][c][qy][qx]
+   static constexpr int kSt = Q + pad_t3(P, Q), kSp = Q * Q + pad_p3(P, Q); // padded strides
+   static constexpr int kEt = D1 * D1 * kSt, kEp = D1 * kSp;                   // per element
+   double TB[EPW * kEt], TG[EPW * kEt];                  // [e][c][b][qx]
+   double Px[EPW * kEp], Py[EPW * kEp], Pz[EPW * kEp];   // [e][c][qy][qx]
    uint64_t full[kSlots], empty[kSlots];
    uint32_t gm[EPW * ND]; // the open group's map entries and essential flags
    uint8_t es[EPW * ND];  // (read by the epilogue)
@@ -62,6 +78,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    constexpr int kW = Cfg3<P, Q, KIND>::kW, kBlock = Cfg3<P, Q, KIND>::kBlock;
    constexpr int kSlots = W::kSlots;
    constexpr int NT = D1 * D1 * Q;         // contraction outputs per element
+   constexpr int kSt = W::kSt, kSp = W::kSp, kEt = W::kEt, kEp = W::kEp;
    constexpr int GPL = (EPW * ND + 31) / 32; // map entries per lane
    // row-wise contractions (basis operands compile-time) when a warp covers
    // the rows in one pass, or two at q <= 6 (BP5 p=5 +7 %); measured slower
@@ -189,8 +206,8 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                   sb = fma(sB[jx][kk], v, sb);
                   if (KIND == TFEM_DIFFUSION) sg = fma(sG[jx][kk], v, sg);
                }
-               sm.TB[jj] = sb;
-               sm.TG[jj] = sg;
+               sm.TB[j * kEt + cb * kSt + jx] = sb;
+               sm.TG[j * kEt + cb * kSt + jx] = sg;
             }
          } else
          for (int it = lane; it < EPW * D1 * D1; it += 32) {
@@ -198,7 +215,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             double v[D1];
 #pragma unroll
             for (int kk = 0; kk < D1; kk++) v[kk] = V[j * ND + cb * D1 + kk];
-            double *TBo = sm.TB + j * NT + cb * Q, *TGo = sm.TG + j * NT + cb * Q;
+            double *TBo = sm.TB + j * kEt + cb * kSt, *TGo = sm.TG + j * kEt + cb * kSt;
 #pragma unroll
             for (int jx = 0; jx < Q; jx++) {
                double sb = 0.0, sg = 0.0;
@@ -221,17 +238,17 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             const int ej = cl / (Q * Q), col = cl % (Q * Q);
             const int qx = col % Q, qy = col / Q;
             const bool live = ej < cnt;
-            const double *TB = sm.TB + ej * NT, *TG = sm.TG + ej * NT;
+            const double *TB = sm.TB + ej * kEt, *TG = sm.TG + ej * kEt;
             double UBB[D1], UBG[D1], UGB[D1];
 #pragma unroll
             for (int c = 0; c < D1; c++) { // contract b
                double bb = 0.0, bg = 0.0, gb = 0.0;
 #pragma unroll
                for (int b = 0; b < D1; b++) {
-                  const double tb = TB[(c * D1 + b) * Q + qx];
+                  const double tb = TB[(c * D1 + b) * kSt + qx];
                   bb = fma(sB[qy][b], tb, bb);
                   if (KIND == TFEM_DIFFUSION) {
-                     const double tg = TG[(c * D1 + b) * Q + qx];
+                     const double tg = TG[(c * D1 + b) * kSt + qx];
                      bg = fma(sG[qy][b], tb, bg);
                      gb = fma(sB[qy][b], tg, gb);
                   }
@@ -279,13 +296,13 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                   }
                }
             }
-            const int po = ej * D1 * Q * Q;
+            const int po = ej * kEp;
 #pragma unroll
             for (int c = 0; c < D1; c++) {
-               sm.Px[po + (c * Q + qy) * Q + qx] = Px[c];
+               sm.Px[po + c * kSp + qy * Q + qx] = Px[c];
                if (KIND == TFEM_DIFFUSION) {
-                  sm.Py[po + (c * Q + qy) * Q + qx] = Py[c];
-                  sm.Pz[po + (c * Q + qy) * Q + qx] = Pz[c];
+                  sm.Py[po + c * kSp + qy * Q + qx] = Py[c];
+                  sm.Pz[po + c * kSp + qy * Q + qx] = Pz[c];
                }
             }
          }
@@ -296,24 +313,24 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          if constexpr (!kRows3) {
             for (int jj = lane; jj < EPW * NT; jj += 32) {
                const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q, b = cb % D1, c = cb / D1;
-               const int po = j * D1 * Q * Q;
+               const int po = j * kEp;
                double sx = 0.0, syz = 0.0;
 #pragma unroll
                for (int y = 0; y < Q; y++) {
-                  const int o = po + (c * Q + y) * Q + jx;
+                  const int o = po + c * kSp + y * Q + jx;
                   sx = fma(sB[y][b], sm.Px[o], sx);
                   if (KIND == TFEM_DIFFUSION) {
                      syz = fma(sG[y][b], sm.Py[o], syz);
                      syz = fma(sB[y][b], sm.Pz[o], syz);
                   }
                }
-               sm.TB[jj] = sx;
-               sm.TG[jj] = syz;
+               sm.TB[j * kEt + cb * kSt + jx] = sx;
+               sm.TG[j * kEt + cb * kSt + jx] = syz;
             }
          } else
          for (int it = lane; it < EPW * Q * D1; it += 32) {
             const int j = it / (Q * D1), r = it % (Q * D1), jx = r % Q, c = r / Q;
-            const int po = j * D1 * Q * Q + c * Q * Q + jx;
+            const int po = j * kEp + c * kSp + jx;
             double px[Q], py[Q], pz[Q];
 #pragma unroll
             for (int y = 0; y < Q; y++) {
@@ -334,7 +351,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                      syz = fma(a.t.B[y][b], pz[y], syz);
                   }
                }
-               const int o = j * NT + (c * D1 + b) * Q + jx;
+               const int o = j * kEt + (c * D1 + b) * kSt + jx;
                sm.TB[o] = sx;
                if (KIND == TFEM_DIFFUSION) sm.TG[o] = syz;
             }
@@ -348,8 +365,8 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             double tb[Q], tg[Q];
 #pragma unroll
             for (int x = 0; x < Q; x++) {
-               tb[x] = sm.TB[j * NT + cb * Q + x];
-               if (KIND == TFEM_DIFFUSION) tg[x] = sm.TG[j * NT + cb * Q + x];
+               tb[x] = sm.TB[j * kEt + cb * kSt + x];
+               if (KIND == TFEM_DIFFUSION) tg[x] = sm.TG[j * kEt + cb * kSt + x];
             }
             const int64_t e = g * EPW + j;
 #pragma unroll
