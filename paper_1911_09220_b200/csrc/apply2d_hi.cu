@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel
                         dot = mac<EXACT>(dot, __ldg(a.x + d), rr);
                      }
                   } else {
-                     a.evec[ev_em(ND, a.ne_pad, e, t)] = rr;
+                     a.evec[ev_em_p(a.evperm, ND, e, t)] = rr;
                   }
                }
             }

@@ -134,7 +134,7 @@ __global__ void apply2d_grp_kernel(const ApplyArgs a)
          a.y[d] = r;
          if (a.dot && !(a.notown && bit_set(a.notown, d))) dot = mul<EXACT>(__ldg(a.x + d), r);
       } else {
-         a.evec[ev_em(ND, a.ne_pad, e, t)] = r;
+         a.evec[ev_em_p(a.evperm, ND, e, t)] = r;
       }
    }
    if (a.dot) {

@@ -63,17 +63,12 @@ constexpr uint32_t kWarpOwner = 0xc0000000u;
 constexpr uint32_t kDofMask = 0x3fffffffu;
 
 // E-vector index of slot (element position e, local i) of an element-major
-// map ([e][nd], the map's own layout); slot-major maps use i * ne_pad + e.
+// map: [e][nd] like the map, with the slots of an element in the order
+// tfem_restriction::evperm (interior, then each face's and edge's interior
+// slots contiguous, so the scatter's reads of one face / edge share 32-byte
+// sectors; null = natural order).  Slot-major maps use i * ne_pad + e.
 // (A [i][ne_pad] E-vector for element-major maps was measured: +3 % at 3D
 // p <= 2, -3 % at p = 3 and BP5 p = 4.)
-__host__ __device__ constexpr int64_t ev_em(int nd, int64_t /*ne_pad*/, int64_t e, int i)
-{
-   return e * nd + i;
-}
-
-// With a slot order (tfem_restriction::evperm: 3D, p >= 3) the E-vector keeps
-// each face's and edge's interior slots of an element contiguous, so the
-// scatter's reads of a face's DOFs share 32-byte sectors.
 __device__ __forceinline__ int64_t ev_em_p(const uint16_t *perm, int nd, int64_t e, int i)
 {
    return e * nd + (perm ? static_cast<int>(__ldg(perm + i)) : i);
@@ -189,7 +184,7 @@ struct tfem_restriction {
       int c = 0;
       int64_t n = 0;
       int32_t *dofs = nullptr;
-      uint32_t *slots = nullptr; // gmap / E-vector slots
+      uint32_t *slots = nullptr; // E-vector slots (= gmap slots unless evperm)
    };
    static constexpr int kMaxBuckets = 7; // c = 2..8
    int n_buckets = 0;
@@ -203,9 +198,9 @@ struct tfem_restriction {
    Bucket gbuckets[kMaxBuckets];
    int64_t n_gshared = 0;
    // E-vector scratch (lazy) in the map's layout: slot-major [i][ne_pad],
-   // element-major [e][nd] (ev_em); a slot indexes both
+   // element-major [e][nd] with the element's slots in evperm order (ev_em_p)
    double *evec = nullptr;
-   uint16_t *evperm = nullptr; // element-major 3D p >= 3: E-vector slot order (ev_em_p)
+   uint16_t *evperm = nullptr; // element-major maps: E-vector slot order (ev_em_p)
    bool cartesian = false;
    int n[3] = {0, 0, 0};
    double *ensure_evec();
