@@ -349,6 +349,7 @@ def run_tfem(args):
     xprof = tf.Vector(dev, N)
     tf.abi.check(lib.tfem_cg_profile(dev.h, op.h, xin.h, min(args.iters, 100),
                                      pc.h if pc is not None else None, xprof.h, seg))
+    del xin, yout, xprof
     t_op = seg[0] * 1e-6
     peak, peak_kind = peaks()
     achieved = b_op / t_op / 1e9
@@ -376,6 +377,9 @@ def run_tfem(args):
         bh, dh, xh = bp.numpy(), dp.numpy(), xp.numpy()
         if pc is None:
             dh = None
+        # the device-resident legs are done: their vectors make room for the
+        # API's own device copies of b / diag / x (1B DOFs fill the GPU)
+        del res, b, x, diag, pc
         tf.cg_solve_host(op, bh, 0.0, args.iters, dh, out=xh)
         dev.sync()
         w0 = time.perf_counter()
