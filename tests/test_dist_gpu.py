@@ -120,7 +120,7 @@ def _rank(rank, world, port, n, p, q):
             pass
 
 
-@pytest.mark.parametrize("n,p", [((24, 18), 3), ((6, 5, 8), 2)])
+@pytest.mark.parametrize("n,p", [((24, 18), 3), ((24, 18), 4), ((6, 5, 8), 2), ((5, 4, 6), 3)])
 def test_two_ranks_share_one_gpu_gloo(dev, n, p):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
