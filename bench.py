@@ -140,6 +140,26 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def op_flops_per_element(dim, p, nq, kind):
+    """Algorithmic FP64 flops of one element's sum-factorised PA action
+    (tensor_kernels.cpp:67-110 in 2D, its 3D analogue): the forward
+    contractions, the pointwise qdata product and the transposed
+    contractions, a multiply-add counted as 2 flops."""
+    D1, Q = p + 1, nq
+    if dim == 2:
+        if kind == "mass":
+            return 2 * (2 * Q * D1 ** 2 + 2 * Q ** 2 * D1) + Q ** 2
+        # T (2 chains), W (2), point (4 mul + 2 add), S (2), r (2) + final add
+        return 2 * (4 * Q * D1 ** 2 + 4 * Q ** 2 * D1) + 6 * Q ** 2 + D1 ** 2
+    fwd_m = Q * D1 ** 3 + Q ** 2 * D1 ** 2 + Q ** 3 * D1
+    if kind == "mass":
+        return 2 * 2 * fwd_m + Q ** 3
+    # forward: (B, G) in x, three products in y, three gradients in z;
+    # pointwise symmetric 3x3 (9 mul + 6 add); the transpose mirrors it
+    fwd_d = 2 * Q * D1 ** 3 + 3 * Q ** 2 * D1 ** 2 + 3 * Q ** 3 * D1
+    return 2 * 2 * fwd_d + 15 * Q ** 3 + 2 * D1 ** 3
+
+
 def traffic_from_profile(key):
     f = ROOT / "profiles" / "traffic.json"
     if f.exists():
@@ -351,6 +371,15 @@ def run_tfem(args):
                                      pc.h if pc is not None else None, xprof.h, seg))
     del xin, yout, xprof
     t_op = seg[0] * 1e-6
+    # FP64 side of the same launch: algorithmic flops against the measured
+    # CUDA-core DFMA peak (probe.cu; the element kernels use no tensor cores)
+    fpeak = C.c_double(0.0)
+    tf.abi.check(lib.tfem_fp64_peak(dev.h, C.byref(fpeak)))
+    f_op = E * op_flops_per_element(args.dim, p, nq, "mass" if args.bp == 1 else "diffusion")
+    fp64 = {"achieved": f_op / t_op / 1e12, "peak": fpeak.value, "unit": "TFLOP/s",
+            "frac": f_op / t_op / 1e12 / fpeak.value if fpeak.value > 0 else None,
+            "flops_per_launch": f_op, "flops_per_dof": f_op / N,
+            "peak_source": "measured (tfem_fp64_peak: DFMA chains on every SM)"}
     peak, peak_kind = peaks()
     achieved = b_op / t_op / 1e9
     b_it = b_op + (80 if args.bp == 1 else 96) * N
@@ -418,7 +447,7 @@ def run_tfem(args):
                      "frac": achieved / peak, "traffic": traffic_from_profile("operator"),
                      "kernel": "PA operator (element kernel + shared-DOF scatter)",
                      "bytes_per_launch": b_op, "ms_per_launch": 1e3 * t_op,
-                     "peak_source": peak_kind},
+                     "peak_source": peak_kind, "fp64": fp64},
         "cg_roofline": {"achieved": cg_achieved, "frac": cg_achieved / peak, "unit": "GB/s",
                         "bytes_per_dof_iteration": b_it / N, "kernels": cg_kernels},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,

@@ -337,6 +337,11 @@ int tfem_cg_profile(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *b,
                     int iters, const tfem_vec *jacobi_diag, tfem_vec *x,
                     double *seg_us);
 
+/* Diagnostics (no reference counterpart): the measured CUDA-core FP64 (DFMA)
+ * peak of the context's device in TFLOP/s -- the FP64 roofline bench.py
+ * reports the element kernels against. */
+int tfem_fp64_peak(tfem_ctx *ctx, double *tflops);
+
 #ifdef __cplusplus
 }
 #endif

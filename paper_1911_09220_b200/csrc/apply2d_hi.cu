@@ -57,9 +57,18 @@ struct alignas(16) Warp2 {
    static constexpr int kT = Q * D1 + pad_t(P, Q), kW2 = Q * Q + pad_w(P, Q), kS = D1 * Q + pad_s(P, Q);
    double q[kSlots][GRP * kQe];
    double V[2][GRP * ND];           // [e][a * D1 + b]
-   double T1[GRP][kT], T2[GRP][kT]; // [e][qx][b]
+#ifndef TFEM_HI_NO_ALIAS
+   // T is dead once W is formed, so S (written from W) reuses its storage:
+   // the smaller per-warp footprint fits more computing warps per SM
+   union {
+      struct { double T1[GRP][kT], T2[GRP][kT]; }; // [e][qx][b]
+      struct { double S1[GRP][kS], S2[GRP][kS]; }; // [e][a][qy]
+   };
+#else
+   double T1[GRP][kT], T2[GRP][kT];
+   double S1[GRP][kS], S2[GRP][kS];
+#endif
    double W1[GRP][kW2], W2[GRP][kW2]; // [e][qx][qy]
-   double S1[GRP][kS], S2[GRP][kS];   // [e][a][qy]
    uint32_t gm[GRP * ND];                   // the slot's map entries, for the epilogue
    uint8_t es[GRP * ND];                    // ... and their essential flags (ess_out)
    uint64_t full[kSlots], empty[kSlots];
@@ -68,8 +77,19 @@ struct alignas(16) Warp2 {
 template <int P, int Q, int KIND>
 struct Cfg2 {
    static constexpr size_t kWarpBytes = sizeof(Warp2<P, Q, KIND>);
-   static constexpr int kW0 = static_cast<int>((200 * 1024) / kWarpBytes);
-   static constexpr int kW = kW0 > 11 ? 11 : (kW0 < 1 ? 1 : kW0);
+   // Latency-bound (ncu at p = 6: 2 warps per scheduler, 0.34 eligible):
+   // as many computing warps as shared memory holds (224 KB: +2-7 % over
+   // 200 KB at p = 5, 6, 8), up to what the registers allow -- 11 (170
+   // registers), or 15 (128) where ptxas needs no more (q = 6, p = 4, 5).
+#ifndef TFEM_HI_SMEM_KB
+#define TFEM_HI_SMEM_KB 224
+#endif
+#ifndef TFEM_HI_WIDE
+#define TFEM_HI_WIDE 15
+#endif
+   static constexpr int kMaxW = (Q == 6 && (P == 4 || P == 5) && KIND == TFEM_DIFFUSION) ? TFEM_HI_WIDE : 11;
+   static constexpr int kW0 = static_cast<int>((TFEM_HI_SMEM_KB * 1024) / kWarpBytes);
+   static constexpr int kW = kW0 > kMaxW ? kMaxW : (kW0 < 1 ? 1 : kW0);
    static constexpr int kBlock = 32 * (kW + 1);
    static constexpr size_t kSmem = kWarpBytes * kW;
 };

@@ -797,6 +797,15 @@ int tfem_cg_profile(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *b, i
    });
 }
 
+int tfem_fp64_peak(tfem_ctx *ctx, double *tflops)
+{
+   return guard([&] {
+      need(ctx, "fp64_peak");
+      need(tflops, "fp64_peak");
+      *tflops = fp64_peak_tflops(ctx);
+   });
+}
+
 int tfem_cg_solve_host(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
                        int max_iters, const double *jacobi_diag, double *x, tfem_cg_result *res)
 {

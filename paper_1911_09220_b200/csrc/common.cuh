@@ -380,6 +380,9 @@ int64_t prolongation_grid(const tfem_prolongation *P);
 // With dot sinks set, the last integrator's launches emit x . y partials.
 void operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, double *y,
                    const DotSink *dot_elem, const DotSink *dot_scatter, const int *done);
+// Measured CUDA-core FP64 (DFMA) peak in TFLOP/s (probe.cu; diagnostics).
+double fp64_peak_tflops(tfem_ctx *ctx);
+
 void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
               int max_iters, const double *diag, double *x, tfem_cg_result *res,
               tfem_cg_callback cb, void *user, double *seg_us = nullptr);

@@ -443,3 +443,12 @@ def test_full_size_properties(dev):
     m.assemble()
     m.mult_true(tf.Vector(dev, sp.n_dofs, 1.0), y)
     assert y.numpy().sum() == pytest.approx(1.0, rel=1e-12)
+
+
+def test_fp64_peak_probe(dev):
+    # diagnostics behind bench.py's FP64 roofline: the DFMA peak of a B200 is
+    # ~37 TFLOP/s nominal; the probe must land in a physically sensible range
+    import ctypes as C
+    v = C.c_double(0.0)
+    tf.abi.check(tf.lib().tfem_fp64_peak(dev.h, C.byref(v)))
+    assert 5.0 < v.value < 100.0, v.value
