@@ -70,7 +70,14 @@ struct Cfg3 {
 #define TFEM_3D_SMEM_KB 224
 #endif
    static constexpr int kW0 = static_cast<int>((TFEM_3D_SMEM_KB * 1024) / kWarpBytes);
-   static constexpr int kW = kW0 > 11 ? 11 : (kW0 < 1 ? 1 : kW0); // compute warps
+   // warp cap from the registers ptxas needs: 11 (170 each) by default, 15
+   // (128) at p <= 2 with q <= p + 2 except p = 2, q = 4, 13 (146) at p = 3, q = 5
+#ifndef TFEM_3D_WIDE
+#define TFEM_3D_WIDE 1
+#endif
+   static constexpr int kMaxW = !TFEM_3D_WIDE || KIND != TFEM_DIFFUSION ? 11
+                              : (Q <= 3) ? 15 : (P == 3 && Q == 5) ? 13 : 11;
+   static constexpr int kW = kW0 > kMaxW ? kMaxW : (kW0 < 1 ? 1 : kW0); // compute warps
    static constexpr int kBlock = 32 * (kW + 1);
    static constexpr size_t kSmem = kWarpBytes * kW;
 };
