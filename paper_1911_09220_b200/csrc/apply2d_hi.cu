@@ -74,20 +74,26 @@ struct alignas(16) Warp2 {
    uint64_t full[kSlots], empty[kSlots];
 };
 
-template <int P, int Q, int KIND>
+template <int P, int Q, int KIND, bool EXACT>
 struct Cfg2 {
    static constexpr size_t kWarpBytes = sizeof(Warp2<P, Q, KIND>);
    // Latency-bound (ncu at p = 6: 2 warps per scheduler, 0.34 eligible):
    // as many computing warps as shared memory holds (224 KB: +2-7 % over
    // 200 KB at p = 5, 6, 8), up to what the registers allow -- 11 (170
-   // registers), or 15 (128) where ptxas needs no more (q = 6, p = 4, 5).
+   // registers), 15 (128) where ptxas needs no more (q = 6, p = 4, 5), and
+   // in FMA numerics 13 (144) at p = 7, q = 9 (+2.6 %; the bit-exact variant
+   // needs 168).  12 warps at q = 7, p = 5 measured -2.3 %, at q = 9, p = 8
+   // +-1 %: kept at 11 (tools/ab_wide.sh).
 #ifndef TFEM_HI_SMEM_KB
 #define TFEM_HI_SMEM_KB 224
 #endif
 #ifndef TFEM_HI_WIDE
 #define TFEM_HI_WIDE 15
 #endif
-   static constexpr int kMaxW = (Q == 6 && (P == 4 || P == 5) && KIND == TFEM_DIFFUSION) ? TFEM_HI_WIDE : 11;
+   static constexpr bool kDiff = KIND == TFEM_DIFFUSION;
+   static constexpr int kMaxW = (kDiff && Q == 6 && (P == 4 || P == 5)) ? TFEM_HI_WIDE
+                              : (kDiff && !EXACT && TFEM_HI_WIDE > 11 && P == 7 && Q == 9) ? 13
+                              : 11;
    static constexpr int kW0 = static_cast<int>((TFEM_HI_SMEM_KB * 1024) / kWarpBytes);
    static constexpr int kW = kW0 > kMaxW ? kMaxW : (kW0 < 1 ? 1 : kW0);
    static constexpr int kBlock = 32 * (kW + 1);
@@ -95,11 +101,11 @@ struct Cfg2 {
 };
 
 template <int P, int Q, int KIND, bool EXACT, bool EDOT>
-__global__ void __launch_bounds__(Cfg2<P, Q, KIND>::kBlock, 1) apply2d_hi_kernel(const ApplyArgs a)
+__global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi_kernel(const ApplyArgs a)
 {
    using W = Warp2<P, Q, KIND>;
    constexpr int D1 = W::D1, ND = W::ND, NQD = W::NQD, NC = W::NC, GRP = W::GRP;
-   constexpr int kW = Cfg2<P, Q, KIND>::kW, kBlock = Cfg2<P, Q, KIND>::kBlock;
+   constexpr int kW = Cfg2<P, Q, KIND, EXACT>::kW, kBlock = Cfg2<P, Q, KIND, EXACT>::kBlock;
    constexpr int kSlots = W::kSlots;
    constexpr int GPL = (GRP * ND + 31) / 32;
    constexpr unsigned kQBytes = NC * NQD * 8;
@@ -377,7 +383,7 @@ int g_sm2 = 0;
 template <int P, int Q, int KIND, bool EXACT>
 void launch(const ApplyArgs &a, cudaStream_t s, unsigned /*blocks*/)
 {
-   using C = Cfg2<P, Q, KIND>;
+   using C = Cfg2<P, Q, KIND, EXACT>;
    static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
    static const bool once = [] {
       cudaFuncSetAttribute(apply2d_hi_kernel<P, Q, KIND, EXACT, false>,
@@ -402,8 +408,8 @@ KernelPick make(bool exact)
 {
    KernelPick k;
    k.launch = exact ? launch<P, Q, KIND, true> : launch<P, Q, KIND, false>;
-   k.elems_per_block = Cfg2<P, Q, KIND>::kW * Warp2<P, Q, KIND>::GRP;
-   k.threads = Cfg2<P, Q, KIND>::kBlock;
+   k.elems_per_block = (exact ? Cfg2<P, Q, KIND, true>::kW : Cfg2<P, Q, KIND, false>::kW) * Warp2<P, Q, KIND>::GRP;
+   k.threads = exact ? Cfg2<P, Q, KIND, true>::kBlock : Cfg2<P, Q, KIND, false>::kBlock;
    k.persistent_blocks = g_sm2;
    k.energy_dot = true;
    return k;

@@ -129,10 +129,25 @@ def test_two_ranks_share_one_gpu_gloo(dev, n, p):
     procs = [ctx.Process(target=_rank, args=(r, 2, port, n, p, q)) for r in range(2)]
     for pr in procs:
         pr.start()
-    res = [q.get(timeout=240) for _ in range(2)]
+    # a rank that fails leaves its peer blocked in a collective: report the
+    # first failure (or a dead rank) instead of waiting for both results
+    import queue
+    import time
+    res, deadline = [], time.monotonic() + 240
+    while len(res) < 2 and time.monotonic() < deadline:
+        try:
+            res.append(q.get(timeout=2))
+        except queue.Empty:
+            dead = [(i, pr.exitcode) for i, pr in enumerate(procs)
+                    if pr.exitcode not in (None, 0)]
+            if dead:
+                break
+        if res and res[-1][1] != "ok":
+            break
     for pr in procs:
-        pr.join(timeout=60)
+        pr.join(timeout=5 if len(res) < 2 else 60)
         if pr.is_alive():
             pr.kill()
     bad = [r for r in res if r[1] != "ok"]
     assert not bad, bad[0][2]
+    assert len(res) == 2, ("rank(s) died or hung", res, [pr.exitcode for pr in procs])
