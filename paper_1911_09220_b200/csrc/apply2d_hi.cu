@@ -90,9 +90,12 @@ struct Cfg2 {
 #ifndef TFEM_HI_WIDE
 #define TFEM_HI_WIDE 15
 #endif
+#ifndef TFEM_HI_W13_P6
+#define TFEM_HI_W13_P6 0
+#endif
    static constexpr bool kDiff = KIND == TFEM_DIFFUSION;
    static constexpr int kMaxW = (kDiff && Q == 6 && (P == 4 || P == 5)) ? TFEM_HI_WIDE
-                              : (kDiff && !EXACT && TFEM_HI_WIDE > 11 && P == 7 && Q == 9) ? 13
+                              : (kDiff && !EXACT && TFEM_HI_WIDE > 11 && ((P == 7 && Q == 9) || (TFEM_HI_W13_P6 && P == 6 && Q == 7))) ? 13
                               : 11;
    static constexpr int kW0 = static_cast<int>((TFEM_HI_SMEM_KB * 1024) / kWarpBytes);
    static constexpr int kW = kW0 > kMaxW ? kMaxW : (kW0 < 1 ? 1 : kW0);
