@@ -81,7 +81,8 @@ struct Cfg2 {
    // as many computing warps as shared memory holds (224 KB: +2-7 % over
    // 200 KB at p = 5, 6, 8), up to what the registers allow -- 11 (170
    // registers), 15 (128) where ptxas needs no more (q = 6, p = 4, 5), and
-   // in FMA numerics 13 (144) at p = 7, q = 9 (+2.6 %; the bit-exact variant
+   // in FMA numerics 13 at p = 7, q = 9 (+2.6 %; 126 registers -- 12 to 15
+   // warps put four on one SMSP, so ptxas caps at 128; the bit-exact variant
    // needs 168).  12 warps at q = 7, p = 5 measured -2.3 %, at q = 9, p = 8
    // +-1 %: kept at 11 (tools/ab_wide.sh).
 #ifndef TFEM_HI_SMEM_KB
@@ -93,9 +94,13 @@ struct Cfg2 {
 #ifndef TFEM_HI_W13_P6
 #define TFEM_HI_W13_P6 0
 #endif
+#ifndef TFEM_HI_W15_P4
+#define TFEM_HI_W15_P4 0
+#endif
    static constexpr bool kDiff = KIND == TFEM_DIFFUSION;
    static constexpr int kMaxW = (kDiff && Q == 6 && (P == 4 || P == 5)) ? TFEM_HI_WIDE
                               : (kDiff && !EXACT && TFEM_HI_WIDE > 11 && ((P == 7 && Q == 9) || (TFEM_HI_W13_P6 && P == 6 && Q == 7))) ? 13
+                              : (kDiff && !EXACT && TFEM_HI_W15_P4 && P == 4 && Q == 5) ? 15
                               : 11;
    static constexpr int kW0 = static_cast<int>((TFEM_HI_SMEM_KB * 1024) / kWarpBytes);
    static constexpr int kW = kW0 > kMaxW ? kMaxW : (kW0 < 1 ? 1 : kW0);
