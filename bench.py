@@ -160,14 +160,19 @@ def op_flops_per_element(dim, p, nq, kind):
     return 2 * 2 * fwd_d + 15 * Q ** 3 + 2 * D1 ** 3
 
 
-def traffic_from_profile(key):
+def config_key(args, n):
+    return f"{args.dim}d_bp{args.bp}_p{args.order}_n{n}_{args.numerics}"
+
+
+def traffic_from_profile(args, n):
+    """ncu-measured DRAM bytes per operator application for THIS workload
+    (profiles/traffic.json, keyed by config_key), or None when no capture of
+    this exact configuration exists -- never another config's number."""
     f = ROOT / "profiles" / "traffic.json"
-    if f.exists():
-        try:
-            return json.loads(f.read_text()).get(key)
-        except Exception:
-            return None
-    return None
+    try:
+        return json.loads(f.read_text())["configs"][config_key(args, n)]["operator"]
+    except Exception:
+        return None
 
 
 # ------------------------------------------------------------ reference arm
@@ -234,7 +239,7 @@ def run_reference_arm(args):
     value = ndofs * args.cpu_iters * args.steps / t / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "GDOF/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_of(args, n, p, ndofs, per_step_iters=args.cpu_iters),
@@ -265,6 +270,27 @@ def config_of(args, n, p, ndofs, per_step_iters=None, world=1):
 
 
 # ---------------------------------------------------------------- our arm
+def result_check(tf, dev, op, b_host, res, iters):
+    """After the timed region: the last solve's x against its own claim.
+    The true residual ||b - A x|| (one more device operator application,
+    differences on the host) must equal the recursive residual the device CG
+    tracked for the returned iterate (res.x_norm) up to the round-off drift of
+    `iters` iterations; the iteration count must be the requested one."""
+    N = b_host.size
+    ax = tf.Vector(dev, N)
+    op.mult(res.x, ax)
+    r = b_host - ax.numpy()
+    true_rel = float(np.linalg.norm(r) / np.linalg.norm(b_host))
+    rec_rel = res.x_norm / res.initial_norm
+    drift = abs(true_rel - rec_rel) / rec_rel
+    ok = res.iterations == iters and drift <= 1e-6
+    if not ok:
+        raise SystemExit(f"bench: result check failed: iterations {res.iterations}/{iters}, "
+                         f"true residual {true_rel:.6e} vs recursive {rec_rel:.6e}")
+    return {"iterations": res.iterations, "true_rel_residual": true_rel,
+            "recursive_rel_residual": rec_rel, "drift": drift, "ok": ok}
+
+
 def run_tfem(args):
     import torch
     import paper_1911_09220_b200 as tf
@@ -318,13 +344,14 @@ def run_tfem(args):
     with Clocks(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            res = step()
         ev1.record(stream)
         ev1.synchronize()
     t_value = ev0.elapsed_time(ev1) / 1e3
     launches = dev.launch_count() - launches0
     clocks = clk.summary()
     value = N * args.iters * args.steps / t_value / 1e9
+    check = result_check(tf, dev, op, b_host, res, args.iters)
 
     # ---- the bit-exact numerics (reference operation order), same workload
     exact = None
@@ -444,20 +471,45 @@ def run_tfem(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_of(args, n, p, N),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_from_profile("operator"),
+                     "frac": achieved / peak, "traffic": traffic_from_profile(args, n),
                      "kernel": "PA operator (element kernel + shared-DOF scatter)",
                      "bytes_per_launch": b_op, "ms_per_launch": 1e3 * t_op,
                      "peak_source": peak_kind, "fp64": fp64},
         "cg_roofline": {"achieved": cg_achieved, "frac": cg_achieved / peak, "unit": "GB/s",
                         "bytes_per_dof_iteration": b_it / N, "kernels": cg_kernels},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
-        "bit_exact_numerics": exact, "setup_s": setup_s,
+        "bit_exact_numerics": exact, "setup_s": setup_s, "result_check": check,
     }
     print(json.dumps(line))
 
 
+def self_launch(args):
+    """--gpus N without torchrun: re-launch this command as N ranks (one per
+    GPU, torchrun, 127.0.0.1); a box with fewer GPUs is an error."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but this box has "
+                                                     f"{have} CUDA device(s)"}))
+        sys.exit(2)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
 def main():
     args = parse()
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None and int(world) != args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
+        sys.exit(2)
+    if world is None and args.gpus > 1 and args.impl != "reference":
+        self_launch(args)
     if args.impl == "reference":
         run_reference_arm(args)
     else:

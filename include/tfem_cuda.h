@@ -84,6 +84,11 @@ void *tfem_ctx_stream(tfem_ctx *ctx);
 int tfem_ctx_set_numerics(tfem_ctx *ctx, int mode);
 /* Kernel launches issued through this context since creation. */
 int64_t tfem_ctx_launch_count(const tfem_ctx *ctx);
+/* Test hook (no reference counterpart): cap the persistent element kernels'
+ * grids at max_blocks blocks (0 = one per SM, the default), so a small mesh
+ * runs many laps of every block's pipeline ring -- the steady state the
+ * parity tests must reach without the CPU oracle timing out. */
+int tfem_ctx_set_max_blocks(tfem_ctx *ctx, int max_blocks);
 
 /* -------------------------------------------- 1D rules and basis tables */
 /* gauss_legendre / gauss_lobatto on [0,1] (quadrature.cpp:64-125). */
@@ -304,6 +309,8 @@ typedef struct {
    int converged;       /* CgResult::converged */
    double final_norm;   /* ||r|| of the recursive residual at exit */
    double initial_norm; /* ||b|| */
+   double x_norm;       /* recursive ||r|| of the returned x (the best iterate
+                           when not converged, solvers.cpp:89-96) */
 } tfem_cg_result;
 
 /* on_iterate(it, x_host, user) after every iteration (solvers.cpp:82);

@@ -9,12 +9,10 @@ fallback: if the shared library is missing, importing fails.
 from __future__ import annotations
 
 import ctypes as C
-import os
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
-# TFEM_LIB: an out-of-tree variant build (tools/variants.sh), for A/B timing
-SO_PATH = Path(os.environ.get("TFEM_LIB") or HERE / "libtfem_cuda.so")
+SO_PATH = HERE / "libtfem_cuda.so"
 
 
 class TfemError(Exception):
@@ -58,7 +56,8 @@ i64p = C.POINTER(C.c_int64)
 
 class CgResult(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int),
-                ("final_norm", C.c_double), ("initial_norm", C.c_double)]
+                ("final_norm", C.c_double), ("initial_norm", C.c_double),
+                ("x_norm", C.c_double)]
 
 
 CG_CALLBACK = C.CFUNCTYPE(None, C.c_int, dp, i64, vp)
@@ -88,6 +87,7 @@ _PROTOS = {
     "tfem_ctx_stream": (vp, [vp]),
     "tfem_ctx_set_numerics": (C.c_int, [vp, C.c_int]),
     "tfem_ctx_launch_count": (i64, [vp]),
+    "tfem_ctx_set_max_blocks": (C.c_int, [vp, C.c_int]),
     "tfem_quadrature": (C.c_int, [C.c_int, C.c_int, dp, dp]),
     "tfem_eval_matrices": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp]),
     "tfem_vec_create": (C.c_int, [vp, i64, C.POINTER(vp)]),

@@ -242,24 +242,13 @@ Tables tables_of(const tfem_pa *pa)
 
 KernelPick pick(const tfem_ctx *ctx, const tfem_pa *pa)
 {
-   // TFEM_APPLY2D=reg selects the plain one-thread-per-element kernel (A/B).
-   static const bool use_tma = [] {
-      const char *v = std::getenv("TFEM_APPLY2D");
-      return !(v && std::string(v) == "reg");
-   }();
    const bool exact = pa->dim == 2 && ctx->numerics == TFEM_NUMERICS_REFERENCE;
    KernelPick k;
-   // TFEM_APPLY3D=grp selects the thread-group kernel for 3D and 2D p >= 4 (A/B).
-   static const bool use_tma3 = [] {
-      const char *v = std::getenv("TFEM_APPLY3D");
-      return !(v && std::string(v) == "grp");
-   }();
    if (pa->dim == 2 && pa->p <= 3)
-      k = use_tma ? pick_apply2d_tma(pa->p, pa->nq, pa->kind, exact, ctx->sm_count)
-                  : pick_apply2d_reg(pa->p, pa->nq, pa->kind, exact);
-   else if (pa->dim == 3 && use_tma3 && (k = pick_apply3d_tma(pa->p, pa->nq, pa->kind, ctx->sm_count)).launch)
+      k = pick_apply2d_tma(pa->p, pa->nq, pa->kind, exact, ctx->sm_count);
+   else if (pa->dim == 3 && (k = pick_apply3d_tma(pa->p, pa->nq, pa->kind, ctx->sm_count)).launch)
       ;
-   else if (pa->dim == 2 && use_tma3 &&
+   else if (pa->dim == 2 &&
             (k = pick_apply2d_hi(pa->p, pa->nq, pa->kind, exact, ctx->sm_count)).launch)
       ;
    else
@@ -268,11 +257,17 @@ KernelPick pick(const tfem_ctx *ctx, const tfem_pa *pa)
    return k;
 }
 
-unsigned elem_blocks(const KernelPick &k, int64_t ne)
+// Persistent kernels: min(work, one block per SM); ctx->max_blocks (a test
+// hook, tfem_ctx_set_max_blocks) caps them further so small meshes run many
+// laps of every block's pipeline ring.
+unsigned elem_blocks(const tfem_ctx *ctx, const KernelPick &k, int64_t ne)
 {
-   const int64_t b = blocks_for(ne, k.elems_per_block);
-   return static_cast<unsigned>(k.persistent_blocks > 0 ? std::min<int64_t>(b, k.persistent_blocks)
-                                                        : b);
+   int64_t b = blocks_for(ne, k.elems_per_block);
+   if (k.persistent_blocks > 0) {
+      b = std::min<int64_t>(b, k.persistent_blocks);
+      if (ctx->max_blocks > 0) b = std::min<int64_t>(b, ctx->max_blocks);
+   }
+   return static_cast<unsigned>(b > 0 ? b : 1);
 }
 
 } // namespace
@@ -303,18 +298,8 @@ int64_t scatter_shared(tfem_ctx *ctx, const tfem_restriction *r, const double *e
    return grid;
 }
 
-// The tile kernel sums tile-local DOFs itself when the space has records.
-// A/B switches (TFEM_WARP_LOCAL, TFEM_EDOT = 0 disables; default on).
-bool env_on(const char *name)
-{
-   const char *v = std::getenv(name);
-   return !(v && std::string(v) == "0");
-}
-bool tiled(const KernelPick &k, const tfem_restriction *r)
-{
-   static const bool on = env_on("TFEM_WARP_LOCAL");
-   return on && k.warp_reduce && r->warp_local;
-}
+// The bulk-copy kernel sums warp-local DOFs itself on ordered spaces.
+bool tiled(const KernelPick &k, const tfem_restriction *r) { return k.warp_reduce && r->warp_local; }
 
 void check_pair(const tfem_pa *pa, const tfem_restriction *r)
 {
@@ -329,7 +314,7 @@ void pa_apply_grids(const tfem_pa *pa, const tfem_restriction *r, int64_t *g_ele
                     int64_t *g_scatter)
 {
    const KernelPick k = pick(pa->ctx, pa);
-   *g_elem = elem_blocks(k, pa->npos);
+   *g_elem = elem_blocks(pa->ctx, k, pa->npos);
    *g_scatter = scatter_grid(r, tiled(k, r));
 }
 
@@ -357,13 +342,12 @@ void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const
    a.elem_ess = f.mask_in ? f.elem_ess : nullptr;
    a.notown = f.notown;
    a.warp_local = tl ? 1 : 0;
-   static const bool edot_on = env_on("TFEM_EDOT");
-   const bool edot = edot_on && k.energy_dot && static_cast<bool>(f.dot) && f.overwrite &&
+   const bool edot = k.energy_dot && static_cast<bool>(f.dot) && f.overwrite &&
                      f.mask_in == f.ess_out && !f.notown;
    a.energy_dot = edot ? 1 : 0;
    a.dot = f.dot;
    a.done = f.done;
-   k.launch(a, ctx->stream, elem_blocks(k, pa->npos));
+   k.launch(a, ctx->stream, elem_blocks(ctx, k, pa->npos));
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
    if (r->n_shared > 0)

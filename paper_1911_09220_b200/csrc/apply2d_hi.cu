@@ -57,17 +57,12 @@ struct alignas(16) Warp2 {
    static constexpr int kT = Q * D1 + pad_t(P, Q), kW2 = Q * Q + pad_w(P, Q), kS = D1 * Q + pad_s(P, Q);
    double q[kSlots][GRP * kQe];
    double V[2][GRP * ND];           // [e][a * D1 + b]
-#ifndef TFEM_HI_NO_ALIAS
    // T is dead once W is formed, so S (written from W) reuses its storage:
    // the smaller per-warp footprint fits more computing warps per SM
    union {
       struct { double T1[GRP][kT], T2[GRP][kT]; }; // [e][qx][b]
       struct { double S1[GRP][kS], S2[GRP][kS]; }; // [e][a][qy]
    };
-#else
-   double T1[GRP][kT], T2[GRP][kT];
-   double S1[GRP][kS], S2[GRP][kS];
-#endif
    double W1[GRP][kW2], W2[GRP][kW2]; // [e][qx][qy]
    uint32_t gm[GRP * ND];                   // the slot's map entries, for the epilogue
    uint8_t es[GRP * ND];                    // ... and their essential flags (ess_out)
@@ -85,24 +80,11 @@ struct Cfg2 {
    // warps put four on one SMSP, so ptxas caps at 128; the bit-exact variant
    // needs 168).  12 warps at q = 7, p = 5 measured -2.3 %, at q = 9, p = 8
    // +-1 %: kept at 11 (tools/ab_wide.sh).
-#ifndef TFEM_HI_SMEM_KB
-#define TFEM_HI_SMEM_KB 224
-#endif
-#ifndef TFEM_HI_WIDE
-#define TFEM_HI_WIDE 15
-#endif
-#ifndef TFEM_HI_W13_P6
-#define TFEM_HI_W13_P6 0
-#endif
-#ifndef TFEM_HI_W15_P4
-#define TFEM_HI_W15_P4 0
-#endif
    static constexpr bool kDiff = KIND == TFEM_DIFFUSION;
-   static constexpr int kMaxW = (kDiff && Q == 6 && (P == 4 || P == 5)) ? TFEM_HI_WIDE
-                              : (kDiff && !EXACT && TFEM_HI_WIDE > 11 && ((P == 7 && Q == 9) || (TFEM_HI_W13_P6 && P == 6 && Q == 7))) ? 13
-                              : (kDiff && !EXACT && TFEM_HI_W15_P4 && P == 4 && Q == 5) ? 15
+   static constexpr int kMaxW = (kDiff && Q == 6 && (P == 4 || P == 5)) ? 15
+                              : (kDiff && !EXACT && P == 7 && Q == 9) ? 13
                               : 11;
-   static constexpr int kW0 = static_cast<int>((TFEM_HI_SMEM_KB * 1024) / kWarpBytes);
+   static constexpr int kW0 = static_cast<int>((224 * 1024) / kWarpBytes);
    static constexpr int kW = kW0 > kMaxW ? kMaxW : (kW0 < 1 ? 1 : kW0);
    static constexpr int kBlock = 32 * (kW + 1);
    static constexpr size_t kSmem = kWarpBytes * kW;
@@ -386,60 +368,50 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi
    }
 }
 
-int g_sm2 = 0;
-
+// grid: min(blocks of kW groups, persistent blocks) -- elem_blocks (apply.cu)
 template <int P, int Q, int KIND, bool EXACT>
-void launch(const ApplyArgs &a, cudaStream_t s, unsigned /*blocks*/)
+void launch(const ApplyArgs &a, cudaStream_t s, unsigned grid)
 {
    using C = Cfg2<P, Q, KIND, EXACT>;
    static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
-   static const bool once = [] {
-      cudaFuncSetAttribute(apply2d_hi_kernel<P, Q, KIND, EXACT, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
-      cudaFuncSetAttribute(apply2d_hi_kernel<P, Q, KIND, EXACT, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
-      return true;
-   }();
-   (void)once;
-   constexpr int GRP = Warp2<P, Q, KIND>::GRP;
-   const int64_t groups = (a.ne + GRP - 1) / GRP;
-   const int64_t nblk = (groups + C::kW - 1) / C::kW;
-   const unsigned grid = static_cast<unsigned>(nblk < g_sm2 ? nblk : g_sm2);
-   if (a.energy_dot)
+   if (a.energy_dot) {
+      max_dynamic_smem((const void *)apply2d_hi_kernel<P, Q, KIND, EXACT, true>, C::kSmem);
       apply2d_hi_kernel<P, Q, KIND, EXACT, true><<<grid, C::kBlock, C::kSmem, s>>>(a);
-   else
+   } else {
+      max_dynamic_smem((const void *)apply2d_hi_kernel<P, Q, KIND, EXACT, false>, C::kSmem);
       apply2d_hi_kernel<P, Q, KIND, EXACT, false><<<grid, C::kBlock, C::kSmem, s>>>(a);
+   }
 }
 
 template <int P, int Q, int KIND>
-KernelPick make(bool exact)
+KernelPick make(bool exact, int sm_count)
 {
    KernelPick k;
    k.launch = exact ? launch<P, Q, KIND, true> : launch<P, Q, KIND, false>;
    k.elems_per_block = (exact ? Cfg2<P, Q, KIND, true>::kW : Cfg2<P, Q, KIND, false>::kW) * Warp2<P, Q, KIND>::GRP;
    k.threads = exact ? Cfg2<P, Q, KIND, true>::kBlock : Cfg2<P, Q, KIND, false>::kBlock;
-   k.persistent_blocks = g_sm2;
+   k.persistent_blocks = sm_count;
    k.energy_dot = true;
    return k;
 }
 
 template <int P, int KIND>
-KernelPick pick_q(int nq, bool exact)
+KernelPick pick_q(int nq, bool exact, int sm)
 {
-   if (nq == P + 2) return make<P, P + 2, KIND>(exact);
-   if (nq == P + 1) return make<P, P + 1, KIND>(exact);
+   if (nq == P + 2) return make<P, P + 2, KIND>(exact, sm);
+   if (nq == P + 1) return make<P, P + 1, KIND>(exact, sm);
    return {};
 }
 
 template <int KIND>
-KernelPick pick_p(int p, int nq, bool exact)
+KernelPick pick_p(int p, int nq, bool exact, int sm)
 {
    switch (p) {
-   case 4: return pick_q<4, KIND>(nq, exact);
-   case 5: return pick_q<5, KIND>(nq, exact);
-   case 6: return pick_q<6, KIND>(nq, exact);
-   case 7: return pick_q<7, KIND>(nq, exact);
-   case 8: return pick_q<8, KIND>(nq, exact);
+   case 4: return pick_q<4, KIND>(nq, exact, sm);
+   case 5: return pick_q<5, KIND>(nq, exact, sm);
+   case 6: return pick_q<6, KIND>(nq, exact, sm);
+   case 7: return pick_q<7, KIND>(nq, exact, sm);
+   case 8: return pick_q<8, KIND>(nq, exact, sm);
    }
    return {};
 }
@@ -448,8 +420,8 @@ KernelPick pick_p(int p, int nq, bool exact)
 
 KernelPick pick_apply2d_hi(int p, int nq, int kind, bool exact, int sm_count)
 {
-   g_sm2 = sm_count;
-   return kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact) : pick_p<TFEM_DIFFUSION>(p, nq, exact);
+   return kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact, sm_count)
+                            : pick_p<TFEM_DIFFUSION>(p, nq, exact, sm_count);
 }
 
 } // namespace tfem

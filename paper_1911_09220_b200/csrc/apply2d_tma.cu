@@ -494,27 +494,19 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
    }
 }
 
-int g_sm_count = 0;
-
+// grid: min(tiles, persistent blocks) -- elem_blocks (apply.cu)
 template <int P, int Q, int KIND, bool EXACT>
-void launch(const ApplyArgs &a, cudaStream_t s, unsigned /*blocks*/)
+void launch(const ApplyArgs &a, cudaStream_t s, unsigned grid)
 {
    const size_t smem = sizeof(TileSmem<P, Q, KIND, EXACT>);
    static_assert(sizeof(TileSmem<P, Q, KIND, EXACT>) <= 227 * 1024, "shared memory budget");
-   static const bool once = [&] {
-      cudaFuncSetAttribute(apply2d_tma_kernel<P, Q, KIND, EXACT, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(apply2d_tma_kernel<P, Q, KIND, EXACT, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      return true;
-   }();
-   (void)once;
-   const int64_t nblk = (a.ne + kTile - 1) / kTile;
-   const unsigned grid = static_cast<unsigned>(nblk < g_sm_count ? nblk : g_sm_count);
-   if (a.energy_dot)
+   if (a.energy_dot) {
+      max_dynamic_smem((const void *)apply2d_tma_kernel<P, Q, KIND, EXACT, true>, smem);
       apply2d_tma_kernel<P, Q, KIND, EXACT, true><<<grid, kBlock, smem, s>>>(a);
-   else
+   } else {
+      max_dynamic_smem((const void *)apply2d_tma_kernel<P, Q, KIND, EXACT, false>, smem);
       apply2d_tma_kernel<P, Q, KIND, EXACT, false><<<grid, kBlock, smem, s>>>(a);
+   }
 }
 
 template <int P, int KIND>
@@ -538,11 +530,9 @@ Launch pick_p(int p, int nq, bool exact)
 
 } // namespace
 
-// Grid: min(tiles, 2 per SM) persistent blocks; the dot sink is sized by
-// elem_blocks_tma().
+// Grid: min(tiles, one block per SM) persistent blocks.
 KernelPick pick_apply2d_tma(int p, int nq, int kind, bool exact, int sm_count)
 {
-   g_sm_count = sm_count;
    KernelPick k;
    k.launch = kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact)
                                 : pick_p<TFEM_DIFFUSION>(p, nq, exact);

@@ -429,33 +429,23 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    }
 }
 
-int g_sm3 = 0;
-
+// grid: min(blocks of kW warps, persistent blocks) -- elem_blocks (apply.cu)
 template <int P, int Q, int KIND>
-void launch(const ApplyArgs &a, cudaStream_t s, unsigned /*blocks*/)
+void launch(const ApplyArgs &a, cudaStream_t s, unsigned grid)
 {
    using C = Cfg3<P, Q, KIND>;
    static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
-   static const bool once = [] {
-      cudaFuncSetAttribute(apply3d_tma_kernel<P, Q, KIND, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
-      cudaFuncSetAttribute(apply3d_tma_kernel<P, Q, KIND, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
-      return true;
-   }();
-   (void)once;
-   constexpr int EPW = Warp3<P, Q, KIND>::EPW;
-   const int64_t groups = (a.ne + EPW - 1) / EPW;
-   const int64_t nblk = (groups + C::kW - 1) / C::kW;
-   const unsigned grid = static_cast<unsigned>(nblk < g_sm3 ? nblk : g_sm3);
-   if (a.energy_dot)
+   if (a.energy_dot) {
+      max_dynamic_smem((const void *)apply3d_tma_kernel<P, Q, KIND, true>, C::kSmem);
       apply3d_tma_kernel<P, Q, KIND, true><<<grid, C::kBlock, C::kSmem, s>>>(a);
-   else
+   } else {
+      max_dynamic_smem((const void *)apply3d_tma_kernel<P, Q, KIND, false>, C::kSmem);
       apply3d_tma_kernel<P, Q, KIND, false><<<grid, C::kBlock, C::kSmem, s>>>(a);
+   }
 }
 
 template <int P, int Q, int KIND>
-KernelPick make()
+KernelPick make(int sm_count)
 {
    KernelPick k;
    // bulk copies need 16-byte sizes and element strides
@@ -463,22 +453,22 @@ KernelPick make()
       k.launch = launch<P, Q, KIND>;
       k.elems_per_block = Cfg3<P, Q, KIND>::kW * Warp3<P, Q, KIND>::EPW;
       k.threads = Cfg3<P, Q, KIND>::kBlock;
-      k.persistent_blocks = g_sm3;
+      k.persistent_blocks = sm_count;
       k.energy_dot = true;
    }
    return k;
 }
 
 template <int KIND>
-KernelPick pick_kind(int p, int nq)
+KernelPick pick_kind(int p, int nq, int sm)
 {
    // up to Q = 7; larger Q leaves too few warps per SM (the group kernel)
    switch (p) {
-   case 1: return nq == 3 ? make<1, 3, KIND>() : nq == 2 ? make<1, 2, KIND>() : KernelPick{};
-   case 2: return nq == 4 ? make<2, 4, KIND>() : nq == 3 ? make<2, 3, KIND>() : KernelPick{};
-   case 3: return nq == 5 ? make<3, 5, KIND>() : nq == 4 ? make<3, 4, KIND>() : KernelPick{};
-   case 4: return nq == 5 ? make<4, 5, KIND>() : nq == 6 ? make<4, 6, KIND>() : KernelPick{};
-   case 5: return nq == 6 ? make<5, 6, KIND>() : nq == 7 ? make<5, 7, KIND>() : KernelPick{};
+   case 1: return nq == 3 ? make<1, 3, KIND>(sm) : nq == 2 ? make<1, 2, KIND>(sm) : KernelPick{};
+   case 2: return nq == 4 ? make<2, 4, KIND>(sm) : nq == 3 ? make<2, 3, KIND>(sm) : KernelPick{};
+   case 3: return nq == 5 ? make<3, 5, KIND>(sm) : nq == 4 ? make<3, 4, KIND>(sm) : KernelPick{};
+   case 4: return nq == 5 ? make<4, 5, KIND>(sm) : nq == 6 ? make<4, 6, KIND>(sm) : KernelPick{};
+   case 5: return nq == 6 ? make<5, 6, KIND>(sm) : nq == 7 ? make<5, 7, KIND>(sm) : KernelPick{};
    }
    return {};
 }
@@ -487,8 +477,8 @@ KernelPick pick_kind(int p, int nq)
 
 KernelPick pick_apply3d_tma(int p, int nq, int kind, int sm_count)
 {
-   g_sm3 = sm_count;
-   return kind == TFEM_MASS ? pick_kind<TFEM_MASS>(p, nq) : pick_kind<TFEM_DIFFUSION>(p, nq);
+   return kind == TFEM_MASS ? pick_kind<TFEM_MASS>(p, nq, sm_count)
+                            : pick_kind<TFEM_DIFFUSION>(p, nq, sm_count);
 }
 
 } // namespace tfem

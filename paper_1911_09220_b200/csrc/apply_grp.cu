@@ -339,20 +339,12 @@ __global__ void apply3d_kernel(const ApplyArgs a)
 }
 
 
-template <typename K>
-void set_smem(K kernel, size_t bytes)
-{
-   if (bytes > 48 * 1024)
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
-
 template <int P, int Q, int KIND, bool EXACT>
 void launch2d(const ApplyArgs &a, cudaStream_t s, unsigned blocks)
 {
    constexpr int NT = round32(Q * Q), GR = groups_for(NT);
    const size_t smem = sizeof(Smem2D<P, Q>) * GR;
-   static bool once = (set_smem(apply2d_grp_kernel<P, Q, KIND, EXACT>, smem), true);
-   (void)once;
+   if (smem > 48 * 1024) max_dynamic_smem((const void *)apply2d_grp_kernel<P, Q, KIND, EXACT>, smem);
    apply2d_grp_kernel<P, Q, KIND, EXACT><<<blocks, NT * GR, smem, s>>>(a);
 }
 
@@ -361,8 +353,7 @@ void launch3d(const ApplyArgs &a, cudaStream_t s, unsigned blocks)
 {
    constexpr int NT = round32(Q * Q), GR = groups_for(NT);
    const size_t smem = sizeof(Smem3D<P, Q>) * GR;
-   static bool once = (set_smem(apply3d_kernel<P, Q, KIND>, smem), true);
-   (void)once;
+   if (smem > 48 * 1024) max_dynamic_smem((const void *)apply3d_kernel<P, Q, KIND>, smem);
    apply3d_kernel<P, Q, KIND><<<blocks, NT * GR, smem, s>>>(a);
 }
 

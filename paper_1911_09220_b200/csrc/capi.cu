@@ -5,6 +5,8 @@
 
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <string>
 
 namespace tfem {
@@ -58,13 +60,51 @@ void need(const void *p, const char *what)
    if (!p) invalid(std::string(what) + ": null argument");
 }
 
+// Every entry point runs on its context's device, whatever the calling
+// thread's current device is (one thread may drive several contexts).
+void bind(const tfem_ctx *ctx)
+{
+   int cur = -1;
+   TFEM_CUDA(cudaGetDevice(&cur));
+   if (cur != ctx->device) TFEM_CUDA(cudaSetDevice(ctx->device));
+}
+
+void need(const tfem_ctx *ctx, const char *what)
+{
+   if (!ctx) invalid(std::string(what) + ": null argument");
+   bind(ctx);
+}
+
+// Objects created through a context carry it.
+template <typename T>
+void need_obj(const T *o, const char *what)
+{
+   if (!o) invalid(std::string(what) + ": null argument");
+   bind(o->ctx);
+}
+
 void check_vec(const tfem_vec *v, int64_t n, const char *what)
 {
-   need(v, what);
+   need_obj(v, what);
    if (v->n != n) invalid(std::string(what) + ": size mismatch");
 }
 
 } // namespace
+
+namespace tfem {
+void max_dynamic_smem(const void *kernel, size_t bytes)
+{
+   static std::mutex mu;
+   static std::set<std::pair<const void *, int>> done;
+   int dev = 0;
+   TFEM_CUDA(cudaGetDevice(&dev));
+   std::lock_guard<std::mutex> lock(mu);
+   if (done.count({kernel, dev})) return;
+   TFEM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bytes)));
+   done.insert({kernel, dev});
+}
+} // namespace tfem
 
 void tfem_ctx::ensure_partials(int64_t n)
 {
@@ -102,7 +142,14 @@ int tfem_ctx_destroy(tfem_ctx *ctx)
 {
    return guard([&] {
       if (!ctx) return;
+      bind(ctx);
       cudaStreamSynchronize(ctx->stream);
+      for (auto &d : ctx->dot_sinks) {
+         cudaFree(d.second.partials);
+         cudaFree(d.second.chunks);
+         cudaFree(d.second.tickets);
+      }
+      for (double *b : ctx->stage) cudaFree(b);
       cudaFree(ctx->red.partials);
       cudaFree(ctx->scalars);
       cudaFreeHost(ctx->host_scalars);
@@ -132,6 +179,15 @@ int tfem_ctx_set_numerics(tfem_ctx *ctx, int mode)
 }
 
 int64_t tfem_ctx_launch_count(const tfem_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int tfem_ctx_set_max_blocks(tfem_ctx *ctx, int max_blocks)
+{
+   return guard([&] {
+      need(ctx, "tfem_ctx_set_max_blocks");
+      if (max_blocks < 0) invalid("tfem_ctx_set_max_blocks: negative cap");
+      ctx->max_blocks = max_blocks;
+   });
+}
 
 // ------------------------------------------------------------------ tables
 int tfem_quadrature(int rule, int n, double *points, double *weights)
@@ -194,6 +250,7 @@ int tfem_vec_destroy(tfem_vec *v)
 {
    return guard([&] {
       if (!v) return;
+      bind(v->ctx);
       if (v->owns) cudaFree(v->d);
       delete v;
    });
@@ -225,7 +282,7 @@ int tfem_vec_download(const tfem_vec *v, double *host, int64_t n)
 int tfem_vec_fill(tfem_vec *v, double value)
 {
    return guard([&] {
-      need(v, "tfem_vec_fill");
+      need_obj(v, "tfem_vec_fill");
       vec_fill(v->ctx, v->d, v->n, value);
       TFEM_CUDA(cudaStreamSynchronize(v->ctx->stream));
    });
@@ -277,7 +334,11 @@ int tfem_restriction_cartesian(tfem_ctx *ctx, int dim, const int *n, int p,
 
 int tfem_restriction_destroy(tfem_restriction *r)
 {
-   return guard([&] { restriction_destroy(r); });
+   return guard([&] {
+      if (!r) return;
+      bind(r->ctx);
+      restriction_destroy(r);
+   });
 }
 
 int64_t tfem_restriction_n_dofs(const tfem_restriction *r) { return r ? r->ndofs : 0; }
@@ -286,7 +347,7 @@ int64_t tfem_restriction_n_elem(const tfem_restriction *r) { return r ? r->ne : 
 int tfem_restriction_elem_dofs(const tfem_restriction *r, int32_t *host)
 {
    return guard([&] {
-      need(r, "tfem_restriction_elem_dofs");
+      need_obj(r, "tfem_restriction_elem_dofs");
       need(host, "tfem_restriction_elem_dofs");
       restriction_elem_dofs(r, host);
    });
@@ -295,7 +356,7 @@ int tfem_restriction_elem_dofs(const tfem_restriction *r, int32_t *host)
 int tfem_restriction_boundary_dofs(const tfem_restriction *r, int32_t *host, int64_t *count)
 {
    return guard([&] {
-      need(r, "tfem_restriction_boundary_dofs");
+      need_obj(r, "tfem_restriction_boundary_dofs");
       need(count, "tfem_restriction_boundary_dofs");
       *count = restriction_boundary_dofs(r, host);
    });
@@ -392,6 +453,7 @@ int tfem_geometry_destroy(tfem_geometry *g)
 {
    return guard([&] {
       if (!g) return;
+      bind(g->ctx);
       cudaFree(g->ctrl);
       delete g;
    });
@@ -424,6 +486,7 @@ int tfem_pa_destroy(tfem_pa *pa)
 {
    return guard([&] {
       if (!pa) return;
+      bind(pa->ctx);
       cudaFree(pa->qdata);
       delete pa;
    });
@@ -464,7 +527,7 @@ uint64_t tfem_pa_multiply_count(const tfem_pa *pa)
 int tfem_pa_qdata(const tfem_pa *pa, double *host)
 {
    return guard([&] {
-      need(pa, "PaData::d");
+      need_obj(pa, "PaData::d");
       need(host, "PaData::d");
       const size_t n = static_cast<size_t>(pa->ncomp) * pa->nqd * pa->ne_pad;
       std::vector<double> dev(n);
@@ -634,7 +697,11 @@ int tfem_prolongation_create(tfem_ctx *ctx, int64_t n_local, int64_t n_true, con
 
 int tfem_prolongation_destroy(tfem_prolongation *P)
 {
-   return guard([&] { prolongation_destroy(P); });
+   return guard([&] {
+      if (!P) return;
+      bind(P->ctx);
+      prolongation_destroy(P);
+   });
 }
 
 int tfem_prolongation_mult(tfem_ctx *ctx, const tfem_prolongation *P, const tfem_vec *x_true,
@@ -694,7 +761,7 @@ int tfem_operator_set_comm(tfem_operator *op, const tfem_comm *comm, const tfem_
                            int64_t n_not_owned, const int32_t *not_owned)
 {
    return guard([&] {
-      need(op, "tfem_operator_set_comm");
+      need_obj(op, "tfem_operator_set_comm");
       need(comm, "tfem_operator_set_comm");
       need(halo, "tfem_operator_set_comm");
       if (!comm->exchange || !comm->allreduce) invalid("tfem_operator_set_comm: null hook");
@@ -716,7 +783,9 @@ int tfem_operator_create_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, co
 int tfem_operator_destroy(tfem_operator *op)
 {
    return guard([&] {
-      if (op) operator_release(op);
+      if (!op) return;
+      bind(op->ctx);
+      operator_release(op);
    });
 }
 
@@ -816,16 +885,17 @@ int tfem_cg_solve_host(tfem_ctx *ctx, const tfem_operator *op, const double *b, 
       need(x, "cg_solve");
       need(res, "cg_solve");
       const int64_t n = op->n;
-      // Device staging buffers cached per (context, size).
-      static thread_local std::vector<std::pair<int64_t, double *>> cache;
+      // Device staging buffers cached per context (and size).
       auto buf = [&](int slot) -> double * {
-         if (cache.size() < 3) cache.resize(3, {0, nullptr});
-         if (cache[slot].first != n) {
-            cudaFree(cache[slot].second);
-            TFEM_CUDA(cudaMalloc(&cache[slot].second, sizeof(double) * n));
-            cache[slot].first = n;
+         if (ctx->stage_n[slot] != n) {
+            TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+            cudaFree(ctx->stage[slot]);
+            ctx->stage[slot] = nullptr;
+            ctx->stage_n[slot] = 0;
+            TFEM_CUDA(cudaMalloc(&ctx->stage[slot], sizeof(double) * n));
+            ctx->stage_n[slot] = n;
          }
-         return cache[slot].second;
+         return ctx->stage[slot];
       };
       double *db = buf(0), *dx = buf(1), *dd = jacobi_diag ? buf(2) : nullptr;
       TFEM_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <memory>
+#include <mutex>
 #include <unordered_map>
 
 namespace tfem {
@@ -34,13 +35,10 @@ inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n +
 
 // Fixed grid for vector kernels: deterministic partial count for a given n.
 // 4 blocks of 256 per SM (measured against 2-32: +2 % CG at 10M DOFs over 8,
-// same at 100M; TFEM_VEC_BLOCKS_PER_SM overrides for A/B runs).
+// same at 100M).
 inline unsigned vec_blocks(const tfem_ctx *ctx, int64_t n)
 {
-   static const int64_t per_sm = [] {
-      const char *v = std::getenv("TFEM_VEC_BLOCKS_PER_SM");
-      return v && std::atoll(v) > 0 ? std::atoll(v) : 4;
-   }();
+   constexpr int64_t per_sm = 4;
    const int64_t cap = static_cast<int64_t>(ctx->sm_count) * per_sm;
    const int64_t need = (n + kVecThreads - 1) / kVecThreads;
    return static_cast<unsigned>(need < cap ? (need > 0 ? need : 1) : cap);
@@ -357,6 +355,7 @@ struct SinkStore {
       cudaFree(s.chunks);
       cudaFree(s.tickets);
       s = DotSink{};
+      grid = nch = 0;
    }
 };
 
@@ -372,6 +371,7 @@ struct Workspace {
    const double *g_diag = nullptr, *g_x = nullptr;
    int g_batch = 0, g_numerics = -1;
    int64_t g_launches = 0;
+   int64_t ge = -1, gs = -1; // element / scatter grids the PA sinks are sized for
    ~Workspace()
    {
       cudaFree(r);
@@ -394,12 +394,43 @@ std::unordered_map<const tfem_operator *, std::unique_ptr<Workspace>> &workspace
    static std::unordered_map<const tfem_operator *, std::unique_ptr<Workspace>> w;
    return w;
 }
+std::mutex &workspaces_mu()
+{
+   static std::mutex mu;
+   return mu;
+}
+
+// The element kernel's grid depends on the context's numerics (kernel
+// variants differ in warps per block) and on its grid cap: the PA dot sinks
+// follow it, and the captured graph is dropped when it changes.
+void fit_pa_sinks(tfem_ctx *ctx, const tfem_operator *op, Workspace &w)
+{
+   if (op->csr || op->P) return;
+   int64_t ge = 0, gs = 0;
+   pa_apply_grids(op->pa.back(), op->r, &ge, &gs);
+   if (ge == w.ge && gs == w.gs) return;
+   TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   w.s_elem.release();
+   w.s_scatter.release();
+   w.s_elem.alloc(ctx->stream, ge, 1);
+   if (gs > 0) w.s_scatter.alloc(ctx->stream, gs, 1);
+   w.ge = ge;
+   w.gs = gs;
+   if (w.graph) {
+      cudaGraphExecDestroy(w.graph);
+      w.graph = nullptr;
+   }
+}
 
 Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
 {
+   std::lock_guard<std::mutex> lock(workspaces_mu());
    auto &m = workspaces();
    auto it = m.find(op);
-   if (it != m.end()) return *it->second;
+   if (it != m.end()) {
+      fit_pa_sinks(ctx, op, *it->second);
+      return *it->second;
+   }
    auto w = std::make_unique<Workspace>();
    w->n = op->n;
    w->r = dalloc<double>(op->n);
@@ -415,10 +446,7 @@ Workspace &workspace_for(tfem_ctx *ctx, const tfem_operator *op)
    } else {
       // everything the iteration touches must exist before graph capture
       if (op->r->needs_evec()) const_cast<tfem_restriction *>(op->r)->ensure_evec();
-      int64_t ge = 0, gs = 0;
-      pa_apply_grids(op->pa.back(), op->r, &ge, &gs);
-      w->s_elem.alloc(ctx->stream, ge, 1);
-      if (gs > 0) w->s_scatter.alloc(ctx->stream, gs, 1);
+      fit_pa_sinks(ctx, op, *w);
    }
    w->s_vec.alloc(ctx->stream, vec_blocks(ctx, op->n), 2);
    w->st = dalloc<CgState>(1);
@@ -487,17 +515,24 @@ double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n,
                const tfem_operator *dist)
 {
    const uint32_t *notown = dist ? dist->notown : nullptr;
-   static thread_local std::unordered_map<int64_t, SinkStore> sinks;
+   // dot sinks cached on the context, by grid size
    const unsigned nb = vec_blocks(ctx, n);
-   auto it = sinks.find(nb);
-   if (it == sinks.end()) {
+   DotSink sink;
+   for (auto &d : ctx->dot_sinks)
+      if (d.first == nb) {
+         sink.partials = d.second.partials;
+         sink.chunks = d.second.chunks;
+         sink.tickets = d.second.tickets;
+      }
+   if (!sink) {
       SinkStore st;
       st.alloc(ctx->stream, nb, 1);
-      it = sinks.emplace(nb, st).first;
+      sink = st.s;
+      ctx->dot_sinks.push_back({nb, {sink.partials, sink.chunks, sink.tickets}});
    }
-   const SinkStore &s = it->second;
-   dot_kernel<<<nb, kVecThreads, 0, ctx->stream>>>(a, b, n, s.s, notown);
-   fold_kernel<<<1, kVecThreads, 0, ctx->stream>>>(s.s.chunks, s.nch, ctx->scalars);
+   const int64_t nch = n_chunks(nb);
+   dot_kernel<<<nb, kVecThreads, 0, ctx->stream>>>(a, b, n, sink, notown);
+   fold_kernel<<<1, kVecThreads, 0, ctx->stream>>>(sink.chunks, nch, ctx->scalars);
    ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
    if (dist) {
@@ -635,7 +670,10 @@ tfem_operator *operator_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, con
 
 void operator_release(tfem_operator *op)
 {
-   workspaces().erase(op);
+   {
+      std::lock_guard<std::mutex> lock(workspaces_mu());
+      workspaces().erase(op);
+   }
    cudaFree(op->ess);
    cudaFree(op->ess_mask);
    cudaFree(op->elem_ess);
@@ -732,6 +770,7 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
    res->converged = 0;
    res->final_norm = 0.0;
    res->initial_norm = 0.0;
+   res->x_norm = 0.0;
    if (diag) { // solvers.cpp:19-29
       int *bad = dalloc<int>(1);
       TFEM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
@@ -808,7 +847,7 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
    if (max_iters <= 0 && !hs.done) {
       // for-loop never runs (solvers.cpp:60, 89-96): x = best = 0
       res->iterations = max_iters;
-      res->final_norm = hs.rnorm;
+      res->final_norm = res->x_norm = hs.rnorm;
       return;
    }
    if (cb) {
@@ -887,6 +926,7 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
    res->iterations = hs.iterations;
    res->converged = hs.converged;
    res->final_norm = hs.rnorm;
+   res->x_norm = hs.converged ? hs.rnorm : hs.best_rnorm;
    const int pick = hs.converged ? hs.cur : hs.best; // solvers.cpp:89-96
    if (xb.x[pick] != x) {
       TFEM_CUDA(cudaMemcpyAsync(x, xb.x[pick], sizeof(double) * n, cudaMemcpyDeviceToDevice,

@@ -31,6 +31,11 @@ inline void cuda_check(cudaError_t e, const char *what)
 }
 #define TFEM_CUDA(call) ::tfem::cuda_check((call), #call)
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) holds per device: the
+// launch helpers call this before each launch; (kernel, device) pairs already
+// set are remembered (capi.cu).
+void max_dynamic_smem(const void *kernel, size_t bytes);
+
 // Copies / fills ordered on a context's (non-blocking) stream.  Never use the
 // legacy-stream cudaMemcpy / cudaMemset next to kernels on ctx->stream: the
 // non-blocking stream does not wait for the legacy one.
@@ -113,9 +118,6 @@ struct ElemOrder {
 inline ElemOrder elem_order_for(int dim, int p, bool cartesian, const int *n)
 {
    ElemOrder o;
-#ifdef TFEM_NO_ORDER
-   cartesian = false; // A/B: reference element order
-#endif
    if (dim == 2 && p <= 3 && cartesian) {
       o.pw = 8;
       o.ph = 4;
@@ -154,10 +156,21 @@ struct tfem_ctx {
    cudaStream_t stream = nullptr;
    int numerics = TFEM_NUMERICS_FMA;
    int sm_count = 148;
+   int max_blocks = 0; // test hook: cap on persistent grids (0 = none)
    int64_t launches = 0;
    tfem::Reducer red;
    double *scalars = nullptr;      // device scratch for small results
    double *host_scalars = nullptr; // pinned mirror
+   // Device-side state cached per context (never per thread or process, so
+   // contexts on different devices never share memory): the dot sinks of
+   // vec_dot by grid size, the staging buffers of tfem_cg_solve_host.
+   struct DotStore {
+      double *partials = nullptr, *chunks = nullptr;
+      unsigned *tickets = nullptr;
+   };
+   std::vector<std::pair<int64_t, DotStore>> dot_sinks;
+   double *stage[3] = {nullptr, nullptr, nullptr};
+   int64_t stage_n[3] = {0, 0, 0};
    void ensure_partials(int64_t n);
    void launched(int64_t n = 1) { launches += n; }
 };

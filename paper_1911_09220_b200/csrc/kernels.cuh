@@ -47,8 +47,6 @@ struct KernelPick {
 
 constexpr int kElemThreads2D = 128;
 
-// Register-resident thread-per-element kernels: 2D, p <= 3.
-KernelPick pick_apply2d_reg(int p, int nq, int kind, bool exact);
 // The same arithmetic fed by a cp.async.bulk / mbarrier qdata pipeline
 // (persistent blocks): 2D, p <= 3.
 KernelPick pick_apply2d_tma(int p, int nq, int kind, bool exact, int sm_count);

@@ -266,16 +266,6 @@ __global__ void remap_slots_kernel(uint32_t *slots, int64_t n, int nd, const uin
    slots[k] = (s / nd) * nd + perm[s % nd];
 }
 
-// TFEM_EVPERM=0 keeps the natural slot order (A/B).
-bool evperm_on()
-{
-   static const bool on = [] {
-      const char *v = std::getenv("TFEM_EVPERM");
-      return !(v && std::string(v) == "0");
-   }();
-   return on;
-}
-
 // E-vector slot order inside an element: the interior slots, then (3D) each
 // face's (p-1)^2, each edge's p-1, the vertices -- sub-entities in (c, b, a)
 // class order (0 / interior / p), slots in natural order inside.
@@ -567,7 +557,7 @@ tfem_restriction *restriction_from_map(tfem_ctx *ctx, int dim, int p, int64_t ne
    TFEM_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * ndofs, s));
    // 3D only: in 2D (p >= 4) the element kernel's scattered stores cost
    // more than the scatter gains (measured -3 to -5 %)
-   if (elem_major && r->dim == 3 && r->p >= 3 && evperm_on()) {
+   if (elem_major && r->dim == 3 && r->p >= 3) {
       const std::vector<uint16_t> perm = ev_perm(r->dim, r->p);
       r->evperm = dalloc<uint16_t>(r->nd);
       h2d(s, r->evperm, perm.data(), sizeof(uint16_t) * perm.size());

@@ -92,6 +92,11 @@ class Device:
     def launch_count(self) -> int:
         return lib().tfem_ctx_launch_count(self.h)
 
+    def set_max_blocks(self, n: int):
+        """Test hook: cap the persistent element kernels at n blocks (0: one
+        per SM) so small meshes run many laps of each block's pipeline."""
+        check(lib().tfem_ctx_set_max_blocks(self.h, n))
+
     def close(self):
         if getattr(self, "h", None):
             lib().tfem_ctx_destroy(self.h)
@@ -703,6 +708,8 @@ class CgResult:
     iterations: int
     converged: bool
     final_norm: float = 0.0
+    initial_norm: float = 0.0
+    x_norm: float = 0.0  # recursive residual norm of the returned x
 
 
 def cg_solve(op: LinearOperator, b, rel_tol: float, max_iters: int,
@@ -722,7 +729,8 @@ def cg_solve(op: LinearOperator, b, rel_tol: float, max_iters: int,
     check(lib().tfem_cg_solve(dev.h, op.h, bv.h, rel_tol, max_iters,
                               None if dv is None else dv.h, xv.h, C.byref(res), cb, None))
     op._count_iters = res.iterations
-    return CgResult(xv, res.iterations, bool(res.converged), res.final_norm)
+    return CgResult(xv, res.iterations, bool(res.converged), res.final_norm, res.initial_norm,
+                    res.x_norm)
 
 
 def cg_solve_host(op: LinearOperator, b: np.ndarray, rel_tol: float, max_iters: int,

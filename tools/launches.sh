@@ -1,11 +1,11 @@
 #!/bin/bash
-# tools/launches.sh VARIANT... -- on the GPU box: ncu kernel-duration list of
-# a short fma bench per variant ("main" = in-tree build), summarised.
-for v in "$@"; do
-  if [ "$v" = main ]; then L=""; else L="build/$v/libtfem_cuda.so"; fi
-  TFEM_LIB=$L timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none ${NCU_EXTRA} --csv \
+# tools/launches.sh TAG [bench args] -- on the GPU box: ncu kernel-duration
+# list of a short fma bench, summarised (the top kernels by total time).
+v=$1; shift
+for _ in 1; do
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none ${NCU_EXTRA} --csv \
     --log-file gpurun_out/launch_$v.csv python bench.py --steps 1 --warmup 1 --iters 20 \
-    --no-cpu-baseline --no-e2e --no-bitexact > /dev/null 2>&1
+    --no-cpu-baseline --no-e2e --no-bitexact "$@" > /dev/null 2>&1
   python - "$v" <<'PY'
 import csv, sys, collections
 v = sys.argv[1]
