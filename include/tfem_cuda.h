@@ -69,6 +69,7 @@ typedef struct tfem_geometry tfem_geometry;
 typedef struct tfem_pa tfem_pa;
 typedef struct tfem_operator tfem_operator;
 typedef struct tfem_prolongation tfem_prolongation;
+typedef struct tfem_nccl tfem_nccl;
 
 /* ------------------------------------------------------------- errors */
 const char *tfem_last_error(void);
@@ -89,6 +90,21 @@ int64_t tfem_ctx_launch_count(const tfem_ctx *ctx);
  * runs many laps of every block's pipeline ring -- the steady state the
  * parity tests must reach without the CPU oracle timing out. */
 int tfem_ctx_set_max_blocks(tfem_ctx *ctx, int max_blocks);
+
+/* -------------------------------------------------------------- memory */
+/* Caching allocators behind the device-resident Vector of the reference-side
+ * binding (the Memory / Read-Write mirror of PAPER.md:1664-1689; vector.hpp:
+ * 14-48 is host-only).  Device blocks are per context and reused in stream
+ * order; host blocks are pinned (cudaHostAllocPortable) and cached, with a
+ * pageable fallback when no device exists.  Sizes are rounded to 512 B
+ * below 1 MiB and 2 MiB above. */
+int tfem_mem_alloc(tfem_ctx *ctx, size_t bytes, void **out);
+int tfem_mem_free(tfem_ctx *ctx, void *p);
+int tfem_mem_trim(tfem_ctx *ctx); /* cudaFree the cached device blocks */
+int tfem_host_alloc(size_t bytes, void **out);
+int tfem_host_free(void *p);
+/* Any-direction copy (cudaMemcpyDefault) on the context stream, synchronous. */
+int tfem_copy(tfem_ctx *ctx, void *dst, const void *src, size_t bytes);
 
 /* -------------------------------------------- 1D rules and basis tables */
 /* gauss_legendre / gauss_lobatto on [0,1] (quadrature.cpp:64-125). */
@@ -188,6 +204,10 @@ uint64_t tfem_pa_multiply_count(const tfem_pa *pa);
 int tfem_pa_qdata(const tfem_pa *pa, double *host);
 /* PaData::b1d / g1d (forms.hpp:36-37), nq x (p+1). */
 int tfem_pa_basis(const tfem_pa *pa, double *B, double *G);
+/* Replace the 1D tables with the caller's (nq x (p+1), row-major): PaData::
+ * b1d / g1d of a basis other than the H1 Gauss-Lobatto one tfem_pa_setup
+ * tabulates (an L2 space's Gauss-Legendre nodes, forms.cpp:213). */
+int tfem_pa_set_basis(tfem_pa *pa, const double *B, const double *G);
 /* pa_apply_local: y += G^T B^T D B G x on L-vectors (forms.cpp:231-296). */
 int tfem_pa_apply_local(tfem_ctx *ctx, const tfem_pa *pa,
                         const tfem_restriction *r, const tfem_vec *x,
@@ -301,6 +321,27 @@ typedef struct {
 } tfem_halo;
 
 int tfem_operator_set_comm(tfem_operator *op, const tfem_comm *comm, const tfem_halo *halo,
+                           int64_t n_not_owned, const int32_t *not_owned);
+
+/* The same plan with the communication inside the library over NCCL
+ * (NVLink / NVSwitch): the halo update is one ncclSend / ncclRecv group per
+ * iteration and the dots ncclAllReduce, all on the context's stream, so the
+ * distributed CG iteration is captured into the same CUDA graphs as the
+ * single-device one and no host code runs per iteration.  One communicator
+ * per rank (one process -- or one context -- per GPU): rank 0 makes the id,
+ * the caller ships it to the other ranks (any channel), every rank creates
+ * its communicator.  peer[k] is the rank the k-th send / receive list pairs
+ * with; send / receive buffers are allocated by the library. */
+#define TFEM_NCCL_ID_BYTES 128
+int tfem_nccl_unique_id(unsigned char id[TFEM_NCCL_ID_BYTES]);
+int tfem_nccl_create(tfem_ctx *ctx, int nranks, int rank,
+                     const unsigned char id[TFEM_NCCL_ID_BYTES], tfem_nccl **out);
+int tfem_nccl_destroy(tfem_nccl *comm);
+/* Sum k doubles of device memory over the ranks, in place (synchronous). */
+int tfem_nccl_allreduce(tfem_ctx *ctx, tfem_nccl *comm, double *device_buf, int64_t k);
+int tfem_operator_set_nccl(tfem_operator *op, tfem_nccl *comm, int n_peers, const int *peer,
+                           const int64_t *n_send, const int32_t *const *send_idx,
+                           const int64_t *n_recv, const int32_t *const *recv_idx,
                            int64_t n_not_owned, const int32_t *not_owned);
 
 /* ------------------------------------------------------------------- CG */

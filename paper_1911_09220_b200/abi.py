@@ -63,6 +63,7 @@ class CgResult(C.Structure):
 CG_CALLBACK = C.CFUNCTYPE(None, C.c_int, dp, i64, vp)
 
 MAX_PEERS = 8
+NCCL_ID_BYTES = 128
 EXCHANGE_HOOK = C.CFUNCTYPE(None, vp)
 ALLREDUCE_HOOK = C.CFUNCTYPE(None, C.c_int, vp)
 
@@ -88,6 +89,12 @@ _PROTOS = {
     "tfem_ctx_set_numerics": (C.c_int, [vp, C.c_int]),
     "tfem_ctx_launch_count": (i64, [vp]),
     "tfem_ctx_set_max_blocks": (C.c_int, [vp, C.c_int]),
+    "tfem_mem_alloc": (C.c_int, [vp, C.c_size_t, C.POINTER(vp)]),
+    "tfem_mem_free": (C.c_int, [vp, vp]),
+    "tfem_mem_trim": (C.c_int, [vp]),
+    "tfem_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
+    "tfem_host_free": (C.c_int, [vp]),
+    "tfem_copy": (C.c_int, [vp, vp, vp, C.c_size_t]),
     "tfem_quadrature": (C.c_int, [C.c_int, C.c_int, dp, dp]),
     "tfem_eval_matrices": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp]),
     "tfem_vec_create": (C.c_int, [vp, i64, C.POINTER(vp)]),
@@ -122,6 +129,7 @@ _PROTOS = {
     "tfem_pa_multiply_count": (C.c_uint64, [vp]),
     "tfem_pa_qdata": (C.c_int, [vp, dp]),
     "tfem_pa_basis": (C.c_int, [vp, dp, dp]),
+    "tfem_pa_set_basis": (C.c_int, [vp, dp, dp]),
     "tfem_pa_apply_local": (C.c_int, [vp, vp, vp, vp, vp]),
     "tfem_pa_diagonal": (C.c_int, [vp, vp, vp, vp]),
     "tfem_linear_form": (C.c_int, [vp, vp, vp, C.c_int, dp, vp]),
@@ -139,6 +147,12 @@ _PROTOS = {
     "tfem_operator_create": (C.c_int, [vp, C.c_int, C.POINTER(vp), vp, i64, i32p,
                                        C.POINTER(vp)]),
     "tfem_operator_set_comm": (C.c_int, [vp, C.POINTER(Comm), C.POINTER(Halo), i64, i32p]),
+    "tfem_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "tfem_nccl_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]),
+    "tfem_nccl_destroy": (C.c_int, [vp]),
+    "tfem_nccl_allreduce": (C.c_int, [vp, vp, vp, i64]),
+    "tfem_operator_set_nccl": (C.c_int, [vp, vp, C.c_int, ip, i64p, C.POINTER(i32p), i64p,
+                                         C.POINTER(i32p), i64, i32p]),
     "tfem_operator_create_csr": (C.c_int, [vp, i64, i32p, i32p, dp, C.POINTER(vp)]),
     "tfem_operator_destroy": (C.c_int, [vp]),
     "tfem_operator_size": (i64, [vp]),

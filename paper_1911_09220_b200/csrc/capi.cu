@@ -3,6 +3,7 @@
 // reference's exception class with the message in tfem_last_error().
 #include "common.cuh"
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -29,6 +30,10 @@ tfem_prolongation *prolongation_create(tfem_ctx *ctx, int64_t n_local, int64_t n
                                        const double *vals, const int32_t *true_index);
 void prolongation_destroy(tfem_prolongation *P);
 void operator_diagonal(tfem_ctx *ctx, const tfem_operator *op, double *diag);
+void operator_set_nccl(tfem_ctx *ctx, tfem_operator *op, tfem_nccl *comm, int n_peers,
+                       const int *peer, const int64_t *n_send, const int32_t *const *send_idx,
+                       const int64_t *n_recv, const int32_t *const *recv_idx,
+                       int64_t n_not_owned, const int32_t *not_owned);
 } // namespace tfem
 
 using namespace tfem;
@@ -45,6 +50,7 @@ int guard(F &&f)
       return TFEM_OK;
    } catch (const Error &e) {
       g_last_error = e.what();
+      if (e.code == TFEM_CUDA_ERROR) (void)cudaGetLastError(); // don't leak into later calls
       return e.code;
    } catch (const std::bad_alloc &) {
       g_last_error = "out of host memory";
@@ -114,6 +120,47 @@ void tfem_ctx::ensure_partials(int64_t n)
    red.cap = n;
 }
 
+namespace tfem {
+namespace {
+std::mutex &refs_mu()
+{
+   static std::mutex mu;
+   return mu;
+}
+} // namespace
+
+void ctx_retain(tfem_ctx *ctx)
+{
+   std::lock_guard<std::mutex> lock(refs_mu());
+   ctx->refs++;
+}
+
+void ctx_release(tfem_ctx *ctx)
+{
+   {
+      std::lock_guard<std::mutex> lock(refs_mu());
+      if (--ctx->refs > 0) return;
+   }
+   int cur = -1;
+   cudaGetDevice(&cur);
+   if (cur != ctx->device) cudaSetDevice(ctx->device);
+   cudaStreamSynchronize(ctx->stream);
+   for (auto &d : ctx->dot_sinks) {
+      cudaFree(d.second.partials);
+      cudaFree(d.second.chunks);
+      cudaFree(d.second.tickets);
+   }
+   for (double *b : ctx->stage) cudaFree(b);
+   for (auto &f : ctx->pool_free) cudaFree(f.second);
+   for (auto &l : ctx->pool_live) cudaFree(l.first);
+   cudaFree(ctx->red.partials);
+   cudaFree(ctx->scalars);
+   cudaFreeHost(ctx->host_scalars);
+   cudaStreamDestroy(ctx->stream);
+   delete ctx;
+}
+} // namespace tfem
+
 extern "C" {
 
 const char *tfem_last_error(void) { return g_last_error.c_str(); }
@@ -138,23 +185,14 @@ int tfem_ctx_create(int device, tfem_ctx **out)
    });
 }
 
+// The handle goes; the context itself lives until its last object does.
 int tfem_ctx_destroy(tfem_ctx *ctx)
 {
    return guard([&] {
       if (!ctx) return;
       bind(ctx);
-      cudaStreamSynchronize(ctx->stream);
-      for (auto &d : ctx->dot_sinks) {
-         cudaFree(d.second.partials);
-         cudaFree(d.second.chunks);
-         cudaFree(d.second.tickets);
-      }
-      for (double *b : ctx->stage) cudaFree(b);
-      cudaFree(ctx->red.partials);
-      cudaFree(ctx->scalars);
-      cudaFreeHost(ctx->host_scalars);
-      cudaStreamDestroy(ctx->stream);
-      delete ctx;
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+      ctx_release(ctx);
    });
 }
 
@@ -186,6 +224,132 @@ int tfem_ctx_set_max_blocks(tfem_ctx *ctx, int max_blocks)
       need(ctx, "tfem_ctx_set_max_blocks");
       if (max_blocks < 0) invalid("tfem_ctx_set_max_blocks: negative cap");
       ctx->max_blocks = max_blocks;
+   });
+}
+
+// ------------------------------------------------------------------ memory
+namespace {
+// Pool granularity: 512 B below 1 MiB, 2 MiB above (a vector of a given
+// length always maps to the same class, so solves reuse their blocks).
+size_t pool_class(size_t bytes)
+{
+   constexpr size_t kSmall = 512, kLarge = size_t(2) << 20;
+   if (bytes == 0) bytes = 1;
+   return bytes < (size_t(1) << 20) ? (bytes + kSmall - 1) / kSmall * kSmall
+                                     : (bytes + kLarge - 1) / kLarge * kLarge;
+}
+
+struct HostPool {
+   std::mutex mu;
+   std::multimap<size_t, void *> free;
+   std::unordered_map<void *, std::pair<size_t, bool>> live; // class, pinned
+};
+HostPool &host_pool()
+{
+   static HostPool *p = new HostPool; // never destroyed: frees may come late
+   return *p;
+}
+} // namespace
+
+int tfem_mem_alloc(tfem_ctx *ctx, size_t bytes, void **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_mem_alloc");
+      need(out, "tfem_mem_alloc");
+      const size_t cls = pool_class(bytes);
+      std::lock_guard<std::mutex> lock(ctx->pool_mu);
+      void *p = nullptr;
+      auto it = ctx->pool_free.find(cls);
+      if (it != ctx->pool_free.end()) {
+         p = it->second;
+         ctx->pool_free.erase(it);
+      } else {
+         cudaError_t e = cudaMalloc(&p, cls);
+         if (e != cudaSuccess) {
+            // release the cache and retry once before failing
+            (void)cudaGetLastError();
+            TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+            for (auto &f : ctx->pool_free) cudaFree(f.second);
+            ctx->pool_free.clear();
+            TFEM_CUDA(cudaMalloc(&p, cls));
+         }
+      }
+      ctx->pool_live[p] = cls;
+      *out = p;
+   });
+}
+
+int tfem_mem_free(tfem_ctx *ctx, void *p)
+{
+   return guard([&] {
+      need(ctx, "tfem_mem_free");
+      if (!p) return;
+      std::lock_guard<std::mutex> lock(ctx->pool_mu);
+      auto it = ctx->pool_live.find(p);
+      if (it == ctx->pool_live.end()) invalid("tfem_mem_free: not a pool block of this context");
+      ctx->pool_free.emplace(it->second, p);
+      ctx->pool_live.erase(it);
+   });
+}
+
+int tfem_mem_trim(tfem_ctx *ctx)
+{
+   return guard([&] {
+      need(ctx, "tfem_mem_trim");
+      std::lock_guard<std::mutex> lock(ctx->pool_mu);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (auto &f : ctx->pool_free) cudaFree(f.second);
+      ctx->pool_free.clear();
+   });
+}
+
+int tfem_host_alloc(size_t bytes, void **out)
+{
+   return guard([&] {
+      need(out, "tfem_host_alloc");
+      const size_t cls = pool_class(bytes);
+      HostPool &hp = host_pool();
+      std::lock_guard<std::mutex> lock(hp.mu);
+      void *p = nullptr;
+      bool pinned = true;
+      auto it = hp.free.find(cls); // cached blocks are all pinned
+      if (it != hp.free.end()) {
+         p = it->second;
+         hp.free.erase(it);
+      } else if (cudaHostAlloc(&p, cls, cudaHostAllocPortable) != cudaSuccess) {
+         (void)cudaGetLastError(); // no device: pageable memory still works
+         p = std::malloc(cls);
+         pinned = false;
+         if (!p) throw std::bad_alloc();
+      }
+      hp.live[p] = {cls, pinned};
+      *out = p;
+   });
+}
+
+int tfem_host_free(void *p)
+{
+   return guard([&] {
+      if (!p) return;
+      HostPool &hp = host_pool();
+      std::lock_guard<std::mutex> lock(hp.mu);
+      auto it = hp.live.find(p);
+      if (it == hp.live.end()) invalid("tfem_host_free: not a pool block");
+      if (it->second.second) hp.free.emplace(it->second.first, p);
+      else std::free(p);
+      hp.live.erase(it);
+   });
+}
+
+int tfem_copy(tfem_ctx *ctx, void *dst, const void *src, size_t bytes)
+{
+   return guard([&] {
+      need(ctx, "tfem_copy");
+      if (!bytes) return;
+      need(dst, "tfem_copy");
+      need(src, "tfem_copy");
+      TFEM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
    });
 }
 
@@ -229,6 +393,7 @@ int tfem_vec_create(tfem_ctx *ctx, int64_t n, tfem_vec **out)
       TFEM_CUDA(cudaMemsetAsync(v->d, 0, sizeof(double) * n, ctx->stream));
       TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
       *out = v;
+      ctx_retain(ctx);
    });
 }
 
@@ -243,6 +408,7 @@ int tfem_vec_wrap(tfem_ctx *ctx, double *device_ptr, int64_t n, tfem_vec **out)
       v->n = n;
       v->owns = false;
       *out = v;
+      ctx_retain(ctx);
    });
 }
 
@@ -251,8 +417,10 @@ int tfem_vec_destroy(tfem_vec *v)
    return guard([&] {
       if (!v) return;
       bind(v->ctx);
+      tfem_ctx *ctx = v->ctx;
       if (v->owns) cudaFree(v->d);
       delete v;
+      ctx_release(ctx);
    });
 }
 
@@ -318,6 +486,7 @@ int tfem_restriction_create(tfem_ctx *ctx, int dim, int p, int64_t n_elem, int64
       need(elem_dofs, "tfem_restriction_create");
       need(out, "tfem_restriction_create");
       *out = restriction_create(ctx, dim, p, n_elem, n_dofs, elem_dofs);
+      ctx_retain(ctx);
    });
 }
 
@@ -329,6 +498,7 @@ int tfem_restriction_cartesian(tfem_ctx *ctx, int dim, const int *n, int p,
       need(n, "tfem_restriction_cartesian");
       need(out, "tfem_restriction_cartesian");
       *out = restriction_cartesian(ctx, dim, n, p);
+      ctx_retain(ctx);
    });
 }
 
@@ -337,7 +507,9 @@ int tfem_restriction_destroy(tfem_restriction *r)
    return guard([&] {
       if (!r) return;
       bind(r->ctx);
+      tfem_ctx *ctx = r->ctx;
       restriction_destroy(r);
+      ctx_release(ctx);
    });
 }
 
@@ -410,6 +582,7 @@ int tfem_geometry_create(tfem_ctx *ctx, int dim, int order, int64_t n_elem, cons
       TFEM_CUDA(cudaMalloc(&g->ctrl, bytes));
       h2d(ctx->stream, g->ctrl, ctrl, bytes);
       *out = g;
+      ctx_retain(ctx);
    });
 }
 
@@ -440,6 +613,7 @@ int tfem_geometry_cartesian_box(tfem_ctx *ctx, int dim, const int *n_local, cons
          g->ne *= n_local[d];
       }
       *out = g.release();
+      ctx_retain(ctx);
    });
 }
 
@@ -454,8 +628,10 @@ int tfem_geometry_destroy(tfem_geometry *g)
    return guard([&] {
       if (!g) return;
       bind(g->ctx);
+      tfem_ctx *ctx = g->ctx;
       cudaFree(g->ctrl);
       delete g;
+      ctx_release(ctx);
    });
 }
 
@@ -479,6 +655,7 @@ int tfem_pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
       need(g, "pa_setup");
       need(out, "pa_setup");
       *out = pa_setup(ctx, kind, g, p, nq, rule, coeff, coeff_const, bad_elem);
+      ctx_retain(ctx);
    });
 }
 
@@ -487,8 +664,10 @@ int tfem_pa_destroy(tfem_pa *pa)
    return guard([&] {
       if (!pa) return;
       bind(pa->ctx);
+      tfem_ctx *ctx = pa->ctx;
       cudaFree(pa->qdata);
       delete pa;
+      ctx_release(ctx);
    });
 }
 
@@ -551,6 +730,17 @@ int tfem_pa_basis(const tfem_pa *pa, double *B, double *G)
       need(pa, "tfem_pa_basis");
       if (B) std::memcpy(B, pa->B.data(), sizeof(double) * pa->B.size());
       if (G) std::memcpy(G, pa->G.data(), sizeof(double) * pa->G.size());
+   });
+}
+
+int tfem_pa_set_basis(tfem_pa *pa, const double *B, const double *G)
+{
+   return guard([&] {
+      need_obj(pa, "tfem_pa_set_basis");
+      need(B, "tfem_pa_set_basis");
+      need(G, "tfem_pa_set_basis");
+      std::memcpy(pa->B.data(), B, sizeof(double) * pa->B.size());
+      std::memcpy(pa->G.data(), G, sizeof(double) * pa->G.size());
    });
 }
 
@@ -623,6 +813,7 @@ int tfem_operator_create_p(tfem_ctx *ctx, int n_pa, tfem_pa *const *pa,
          throw;
       }
       *out = op;
+      ctx_retain(ctx);
    });
 }
 
@@ -692,6 +883,7 @@ int tfem_prolongation_create(tfem_ctx *ctx, int64_t n_local, int64_t n_true, con
       need(out, "tfem_prolongation_create");
       if (rowptr[n_local] > 0 && (!cols || !vals)) invalid("tfem_prolongation_create: null CSR");
       *out = prolongation_create(ctx, n_local, n_true, rowptr, cols, vals, true_index);
+      ctx_retain(ctx);
    });
 }
 
@@ -700,7 +892,9 @@ int tfem_prolongation_destroy(tfem_prolongation *P)
    return guard([&] {
       if (!P) return;
       bind(P->ctx);
+      tfem_ctx *ctx = P->ctx;
       prolongation_destroy(P);
+      ctx_release(ctx);
    });
 }
 
@@ -769,6 +963,64 @@ int tfem_operator_set_comm(tfem_operator *op, const tfem_comm *comm, const tfem_
    });
 }
 
+int tfem_nccl_unique_id(unsigned char id[TFEM_NCCL_ID_BYTES])
+{
+   return guard([&] {
+      need(id, "tfem_nccl_unique_id");
+      nccl_unique_id(id);
+   });
+}
+
+int tfem_nccl_create(tfem_ctx *ctx, int nranks, int rank, const unsigned char id[TFEM_NCCL_ID_BYTES],
+                     tfem_nccl **out)
+{
+   return guard([&] {
+      need(ctx, "tfem_nccl_create");
+      need(id, "tfem_nccl_create");
+      need(out, "tfem_nccl_create");
+      *out = nccl_create(ctx, nranks, rank, id);
+      ctx_retain(ctx);
+   });
+}
+
+int tfem_nccl_destroy(tfem_nccl *comm)
+{
+   return guard([&] {
+      if (!comm) return;
+      bind(comm->ctx);
+      tfem_ctx *ctx = comm->ctx;
+      nccl_destroy(comm);
+      ctx_release(ctx);
+   });
+}
+
+int tfem_nccl_allreduce(tfem_ctx *ctx, tfem_nccl *comm, double *device_buf, int64_t k)
+{
+   return guard([&] {
+      need(ctx, "tfem_nccl_allreduce");
+      need(comm, "tfem_nccl_allreduce");
+      if (k > 0) need(device_buf, "tfem_nccl_allreduce");
+      if (k > 0) nccl_allreduce(ctx, comm, device_buf, k);
+      TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   });
+}
+
+int tfem_operator_set_nccl(tfem_operator *op, tfem_nccl *comm, int n_peers, const int *peer,
+                           const int64_t *n_send, const int32_t *const *send_idx,
+                           const int64_t *n_recv, const int32_t *const *recv_idx,
+                           int64_t n_not_owned, const int32_t *not_owned)
+{
+   return guard([&] {
+      need_obj(op, "tfem_operator_set_nccl");
+      need(comm, "tfem_operator_set_nccl");
+      if (comm->ctx != op->ctx) invalid("tfem_operator_set_nccl: communicator of another context");
+      if (n_peers > 0 && (!peer || !n_send || !send_idx || !n_recv || !recv_idx))
+         invalid("tfem_operator_set_nccl: null halo list");
+      operator_set_nccl(op->ctx, op, comm, n_peers, peer, n_send, send_idx, n_recv, recv_idx,
+                        n_not_owned, not_owned);
+   });
+}
+
 int tfem_operator_create_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, const int32_t *cols,
                              const double *vals, tfem_operator **out)
 {
@@ -777,6 +1029,7 @@ int tfem_operator_create_csr(tfem_ctx *ctx, int64_t n, const int32_t *rowptr, co
       need(rowptr, "tfem_operator_create_csr");
       need(out, "tfem_operator_create_csr");
       *out = operator_csr(ctx, n, rowptr, cols, vals);
+      ctx_retain(ctx);
    });
 }
 
@@ -785,7 +1038,9 @@ int tfem_operator_destroy(tfem_operator *op)
    return guard([&] {
       if (!op) return;
       bind(op->ctx);
+      tfem_ctx *ctx = op->ctx;
       operator_release(op);
+      ctx_release(ctx);
    });
 }
 

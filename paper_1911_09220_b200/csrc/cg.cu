@@ -26,6 +26,7 @@
 namespace tfem {
 
 void vec_axpy(tfem_ctx *ctx, double a, const double *x, double *y, int64_t n);
+void comm_allreduce(tfem_ctx *ctx, const tfem_operator *op, int k);
 
 namespace {
 
@@ -537,7 +538,7 @@ double vec_dot(tfem_ctx *ctx, const double *a, const double *b, int64_t n,
    TFEM_CUDA(cudaGetLastError());
    if (dist) {
       copy_scalar_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scalars, dist->red);
-      dist->comm.allreduce(1, dist->comm.user);
+      comm_allreduce(ctx, dist, 1);
       copy_scalar_kernel<<<1, 1, 0, ctx->stream>>>(dist->red, ctx->scalars);
       ctx->launched(2);
    }
@@ -584,14 +585,30 @@ void operator_set_ess(tfem_ctx *ctx, tfem_operator *op, int64_t n_ess, const int
    TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
-void operator_set_comm(tfem_ctx *ctx, tfem_operator *op, const tfem_comm &comm,
-                       const tfem_halo &halo, int64_t n_not_owned, const int32_t *not_owned)
+namespace {
+// The owned halo buffers of an NCCL operator (and its reduction slots).
+void free_nccl_buffers(tfem_operator *op)
+{
+   if (!op->nccl) return;
+   for (int k = 0; k < op->n_peers; k++) {
+      cudaFree(op->send_buf[k]);
+      cudaFree(op->recv_buf[k]);
+      op->send_buf[k] = op->recv_buf[k] = nullptr;
+   }
+   cudaFree(op->red);
+   op->red = nullptr;
+   op->nccl = nullptr;
+}
+
+// Halo lists, ownership bitmap and buffers of a distributed operator
+// (DESIGN.md 6), shared by the hook (set_comm) and NCCL (set_nccl) paths.
+void set_plan(tfem_ctx *ctx, tfem_operator *op, int n_peers, const int64_t *n_send,
+              const int32_t *const *send_idx, const int64_t *n_recv,
+              const int32_t *const *recv_idx, int64_t n_not_owned, const int32_t *not_owned)
 {
    if (op->csr) invalid("tfem_operator_set_comm: needs a PA operator");
    if (op->P) invalid("tfem_operator_set_comm: prolongated (non-conforming) operators run on one device");
-   if (halo.n_peers < 0 || halo.n_peers > TFEM_MAX_PEERS)
-      invalid("tfem_operator_set_comm: bad peer count");
-   if (!halo.red) invalid("tfem_operator_set_comm: null reduction buffer");
+   if (n_peers < 0 || n_peers > TFEM_MAX_PEERS) invalid("tfem_operator_set_comm: bad peer count");
    auto upload = [&](const int32_t *idx, int64_t n) -> int32_t * {
       for (int64_t i = 0; i < n; i++)
          if (idx[i] < 0 || idx[i] >= op->n) invalid("tfem_operator_set_comm: DOF out of range");
@@ -599,20 +616,18 @@ void operator_set_comm(tfem_ctx *ctx, tfem_operator *op, const tfem_comm &comm,
       h2d(ctx->stream, d, idx, sizeof(int32_t) * n);
       return d;
    };
+   free_nccl_buffers(op);
    for (int k = 0; k < op->n_peers; k++) {
       cudaFree(op->send_idx[k]);
       cudaFree(op->recv_idx[k]);
    }
-   op->n_peers = halo.n_peers;
-   for (int k = 0; k < halo.n_peers; k++) {
-      op->n_send[k] = halo.n_send[k];
-      op->n_recv[k] = halo.n_recv[k];
-      op->send_idx[k] = upload(halo.send_idx[k], halo.n_send[k]);
-      op->recv_idx[k] = upload(halo.recv_idx[k], halo.n_recv[k]);
-      op->send_buf[k] = halo.send_buf[k];
-      op->recv_buf[k] = halo.recv_buf[k];
+   op->n_peers = n_peers;
+   for (int k = 0; k < n_peers; k++) {
+      op->n_send[k] = n_send[k];
+      op->n_recv[k] = n_recv[k];
+      op->send_idx[k] = upload(send_idx[k], n_send[k]);
+      op->recv_idx[k] = upload(recv_idx[k], n_recv[k]);
    }
-   op->red = halo.red;
    cudaFree(op->notown);
    op->notown = nullptr;
    if (n_not_owned > 0) {
@@ -627,11 +642,51 @@ void operator_set_comm(tfem_ctx *ctx, tfem_operator *op, const tfem_comm &comm,
       TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
       cudaFree(d);
    }
-   op->comm = comm;
    op->has_comm = true;
 }
+} // namespace
 
-// Halo update of a device vector: pack, hook, unpack (all on the stream).
+void operator_set_comm(tfem_ctx *ctx, tfem_operator *op, const tfem_comm &comm,
+                       const tfem_halo &halo, int64_t n_not_owned, const int32_t *not_owned)
+{
+   if (!halo.red) invalid("tfem_operator_set_comm: null reduction buffer");
+   set_plan(ctx, op, halo.n_peers, halo.n_send, halo.send_idx, halo.n_recv, halo.recv_idx,
+            n_not_owned, not_owned);
+   for (int k = 0; k < halo.n_peers; k++) {
+      op->send_buf[k] = halo.send_buf[k];
+      op->recv_buf[k] = halo.recv_buf[k];
+   }
+   op->red = halo.red;
+   op->comm = comm;
+}
+
+void operator_set_nccl(tfem_ctx *ctx, tfem_operator *op, tfem_nccl *comm, int n_peers,
+                       const int *peer, const int64_t *n_send, const int32_t *const *send_idx,
+                       const int64_t *n_recv, const int32_t *const *recv_idx,
+                       int64_t n_not_owned, const int32_t *not_owned)
+{
+   for (int k = 0; k < n_peers; k++)
+      if (peer[k] < 0 || peer[k] >= comm->nranks || peer[k] == comm->rank)
+         invalid("tfem_operator_set_nccl: bad peer rank");
+   set_plan(ctx, op, n_peers, n_send, send_idx, n_recv, recv_idx, n_not_owned, not_owned);
+   for (int k = 0; k < n_peers; k++) {
+      op->peer_rank[k] = peer[k];
+      op->send_buf[k] = dalloc<double>(n_send[k]);
+      op->recv_buf[k] = dalloc<double>(n_recv[k]);
+   }
+   op->red = dalloc<double>(4);
+   op->comm = tfem_comm{};
+   op->nccl = comm;
+}
+
+// Sum red[0..k) over the ranks, in stream order.
+void comm_allreduce(tfem_ctx *ctx, const tfem_operator *op, int k)
+{
+   if (op->nccl) nccl_allreduce(ctx, op->nccl, op->red, k);
+   else op->comm.allreduce(k, op->comm.user);
+}
+
+// Halo update of a device vector: pack, transfer, unpack (all on the stream).
 void halo_exchange(tfem_ctx *ctx, const tfem_operator *op, double *v)
 {
    for (int k = 0; k < op->n_peers; k++)
@@ -640,7 +695,8 @@ void halo_exchange(tfem_ctx *ctx, const tfem_operator *op, double *v)
             v, op->send_idx[k], op->n_send[k], op->send_buf[k]);
          ctx->launched();
       }
-   op->comm.exchange(op->comm.user);
+   if (op->nccl) nccl_exchange(ctx, op);
+   else op->comm.exchange(op->comm.user);
    for (int k = 0; k < op->n_peers; k++)
       if (op->n_recv[k] > 0) {
          scatter_idx_kernel<<<blocks_for(op->n_recv[k], 256), 256, 0, ctx->stream>>>(
@@ -673,6 +729,11 @@ void operator_release(tfem_operator *op)
    {
       std::lock_guard<std::mutex> lock(workspaces_mu());
       workspaces().erase(op);
+   }
+   free_nccl_buffers(op);
+   for (int k = 0; k < op->n_peers; k++) {
+      cudaFree(op->send_idx[k]);
+      cudaFree(op->recv_idx[k]);
    }
    cudaFree(op->ess);
    cudaFree(op->ess_mask);
@@ -783,7 +844,7 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
       if (hb) invalid("cg_solve: Jacobi diagonal must be strictly positive");
    }
    Workspace &w = workspace_for(ctx, op);
-   const tfem_comm *comm = op->has_comm ? &op->comm : nullptr;
+   const bool comm = op->has_comm;
    const double bnorm = std::sqrt(vec_dot(ctx, b, b, n, comm ? op : nullptr));
    res->initial_norm = bnorm;
    if (!std::isfinite(bnorm)) runtime("cg_solve: right-hand side is not finite");
@@ -803,7 +864,7 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
    if (comm) {
       fold_to_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, nullptr,
                                                          0, 2, op->red);
-      comm->allreduce(2, comm->user);
+      comm_allreduce(ctx, op, 2);
       red_init_kernel<<<1, 1, 0, ctx->stream>>>(op->red, w.st);
    } else {
       cg_init_finish_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch,
@@ -822,13 +883,13 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
       fold_to_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_elem.s.chunks, w.s_elem.nch,
                                                          w.s_scatter.s.chunks, w.s_scatter.nch,
                                                          1, op->red);
-      comm->allreduce(1, comm->user);
+      comm_allreduce(ctx, op, 1);
       red_alpha_kernel<<<1, 1, 0, ctx->stream>>>(op->red, w.st);
       cg_update_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, w.q, w.r, diag, n, w.s_vec.s,
                                                             op->notown);
       fold_to_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_vec.s.chunks, w.s_vec.nch, nullptr,
                                                          0, 2, op->red);
-      comm->allreduce(2, comm->user);
+      comm_allreduce(ctx, op, 2);
       red_beta_kernel<<<1, 1, 0, ctx->stream>>>(op->red, w.st);
       cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.r, diag, w.p, n,
                                                             w.dir_ticket);
@@ -861,9 +922,10 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
             cb(hs.it, hx.data(), n, user);
          }
       }
-   } else if (comm) {
-      // Eager: the hooks enqueue communication on the stream.  All ranks see
-      // the same scalars, hence the same stop decision at the same batch.
+   } else if (comm && !op->nccl) {
+      // Host hooks (e.g. gloo tests): eager, the hooks enqueue communication
+      // on the stream.  All ranks see the same scalars, hence the same stop
+      // decision at the same batch.
       while (!hs.done) {
          for (int k = 0; k < 8; k++) dist_iteration();
          hs = read_state();
@@ -893,8 +955,20 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
       for (auto &e : ev) cudaEventDestroy(e);
    } else {
       // Batches of iterations as one graph; the batch length keeps the
-      // per-batch host round trip small against the work it covers.
+      // per-batch host round trip small against the work it covers.  A
+      // distributed (NCCL) iteration is captured the same way -- its
+      // collectives are stream-ordered NCCL calls; its first batch runs
+      // eagerly so NCCL's lazy connection setup never happens under capture.
+      // Every rank reads the same scalars, so all replay the same batches.
       const int batch = 16;
+      auto iteration = [&]() {
+         if (comm) dist_iteration();
+         else enqueue_iteration(ctx, op, w, xb, diag);
+      };
+      if (comm && !w.graph && !hs.done) {
+         for (int k = 0; k < batch; k++) iteration();
+         hs = read_state();
+      }
       if (!w.graph || w.g_diag != diag || w.g_x != x || w.g_batch != batch ||
           w.g_numerics != ctx->numerics) {
          if (w.graph) {
@@ -904,7 +978,7 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
          cudaGraph_t g;
          const int64_t before = ctx->launches;
          TFEM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-         for (int k = 0; k < batch; k++) enqueue_iteration(ctx, op, w, xb, diag);
+         for (int k = 0; k < batch; k++) iteration();
          TFEM_CUDA(cudaStreamEndCapture(ctx->stream, &g));
          w.g_launches = ctx->launches - before;
          ctx->launches = before;

@@ -6,8 +6,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 namespace tfem {
@@ -152,6 +155,10 @@ struct Reducer {
 } // namespace tfem
 
 struct tfem_ctx {
+   // Reference count: the context handle plus every object created through
+   // it (vectors, restrictions, geometries, PaData, operators, prolongations);
+   // tfem_ctx_destroy drops the handle's count, the last object frees it.
+   int refs = 1;
    int device = 0;
    cudaStream_t stream = nullptr;
    int numerics = TFEM_NUMERICS_FMA;
@@ -171,8 +178,21 @@ struct tfem_ctx {
    std::vector<std::pair<int64_t, DotStore>> dot_sinks;
    double *stage[3] = {nullptr, nullptr, nullptr};
    int64_t stage_n[3] = {0, 0, 0};
+   // Caching device allocator (tfem_mem_alloc / tfem_mem_free): freed blocks
+   // return to a size-keyed free list and are reused in stream order (the
+   // context has one stream), so host-side objects that come and go -- the
+   // device mirrors of the reference's Vector -- never cudaMalloc per call.
+   std::mutex pool_mu;
+   std::multimap<size_t, void *> pool_free;
+   std::unordered_map<void *, size_t> pool_live;
    void ensure_partials(int64_t n);
    void launched(int64_t n = 1) { launches += n; }
+};
+
+struct tfem_nccl {
+   tfem_ctx *ctx = nullptr;
+   void *comm = nullptr; // ncclComm_t
+   int rank = 0, nranks = 1;
 };
 
 struct tfem_vec {
@@ -272,8 +292,10 @@ struct tfem_operator {
    // bitmap load per slot)
    uint32_t *elem_ess = nullptr;
    uint32_t *notown = nullptr;   // bitmap: DOFs owned by another rank (dist)
-   bool has_comm = false;        // distributed: CG calls the hooks below
+   bool has_comm = false;        // distributed: NCCL (nccl) or the host hooks (comm)
    tfem_comm comm{};
+   tfem_nccl *nccl = nullptr;    // library-side NCCL: buffers below owned here
+   int peer_rank[TFEM_MAX_PEERS] = {};
    int n_peers = 0;
    int64_t n_send[TFEM_MAX_PEERS] = {}, n_recv[TFEM_MAX_PEERS] = {};
    int32_t *send_idx[TFEM_MAX_PEERS] = {}, *recv_idx[TFEM_MAX_PEERS] = {}; // device
@@ -284,6 +306,16 @@ struct tfem_operator {
 };
 
 namespace tfem {
+
+void ctx_retain(tfem_ctx *ctx);
+void ctx_release(tfem_ctx *ctx);
+
+// NCCL (comm.cu)
+void nccl_unique_id(unsigned char *id);
+tfem_nccl *nccl_create(tfem_ctx *ctx, int nranks, int rank, const unsigned char *id);
+void nccl_destroy(tfem_nccl *c);
+void nccl_allreduce(tfem_ctx *ctx, const tfem_nccl *c, double *d, int64_t k);
+void nccl_exchange(tfem_ctx *ctx, const tfem_operator *op);
 
 constexpr int kChunk = 32;
 

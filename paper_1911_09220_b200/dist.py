@@ -11,12 +11,17 @@ Ownership: rank r owns the DOF lattice planes J in [1 if r > 0 else 0, top]
 of its slab (top = its upper interface plane); the bottom interface plane
 belongs to rank r-1, the planes above `top` to rank r+1.
 
-Per CG iteration (inside the library's loop, tfem_operator_set_comm):
+Per CG iteration (inside the library's loop):
   halo update of p      owner -> ghost copies: send my planes J in [1, p] down,
                         my plane J = top up; receive J = 0 from below and
                         J in (top, top+p] from above
   allreduce(p.q), allreduce(r.r, r.z)   dots over owned DOFs only
-Communication runs through torch.distributed (NCCL) on the library's stream.
+Transport: "nccl" (default) -- the library's own NCCL communicator
+(tfem_nccl_create / tfem_operator_set_nccl): ncclSend/ncclRecv and
+ncclAllReduce on the library stream, captured into the CG's CUDA graphs, no
+Python per iteration; torch.distributed only ships the NCCL id and times the
+run.  "hooks" -- host callbacks through torch.distributed (gloo test path:
+several ranks sharing one GPU, which NCCL refuses).
 
 The plan (partition, lattice coordinates, halo lists, ownership, essential
 DOFs) is plain numpy shared by the GPU driver and the CPU test backend
@@ -26,7 +31,6 @@ from __future__ import annotations
 
 import ctypes as C
 import json
-import os
 import time
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
@@ -149,7 +153,7 @@ class DistOperator:
     """One rank's constrained PA diffusion operator with the halo / allreduce
     hooks wired to torch.distributed on the library stream."""
 
-    def __init__(self, dev, slab: Slab, ext=None, kind="diffusion"):
+    def __init__(self, dev, slab: Slab, ext=None, kind="diffusion", transport=None):
         import torch
         import torch.distributed as tdist
         from . import abi
@@ -168,6 +172,14 @@ class DistOperator:
         self.op = ConstrainedOperator(self.form, self.plan.ess)
         gpu = torch.device("cuda", torch.cuda.current_device())
         self.stream = torch.cuda.ExternalStream(dev.stream)
+        if transport is None:
+            transport = "nccl" if tdist.get_backend() == "nccl" else "hooks"
+        self.transport = transport
+        self.nccl = None
+        if transport == "nccl":
+            self._init_nccl(abi, tdist)
+            self.diag = self.op.diagonal()
+            return
         self.red = torch.zeros(4, dtype=torch.float64, device=gpu)
         self.bufs = []
         halo = abi.Halo()
@@ -226,6 +238,40 @@ class DistOperator:
         self._halo = halo
         self.diag = self.op.diagonal()
 
+    def _init_nccl(self, abi, tdist):
+        """The library's own communicator: rank 0's NCCL id over
+        torch.distributed, then the halo plan with library-owned buffers."""
+        rank, world = self.slab.rank, self.slab.world
+        idbuf = C.create_string_buffer(abi.NCCL_ID_BYTES)
+        if rank == 0:
+            abi.check(abi.lib().tfem_nccl_unique_id(idbuf))
+        obj = [idbuf.raw if rank == 0 else None]
+        tdist.broadcast_object_list(obj, src=0)
+        idbuf = C.create_string_buffer(obj[0], abi.NCCL_ID_BYTES)
+        h = abi.vp()
+        abi.check(abi.lib().tfem_nccl_create(self.dev.h, world, rank, idbuf, C.byref(h)))
+        self.nccl = h
+        peers = self.plan.peers
+        k = len(peers)
+        peer = (C.c_int * max(k, 1))(*[pr for pr, _, _ in peers])
+        n_send = (C.c_int64 * max(k, 1))(*[len(s) for _, s, _ in peers])
+        n_recv = (C.c_int64 * max(k, 1))(*[len(r) for _, _, r in peers])
+        self._keep = [x for _, s, r in peers for x in (s, r)]
+        s_idx = (abi.i32p * max(k, 1))(*[s.ctypes.data_as(abi.i32p) for _, s, _ in peers])
+        r_idx = (abi.i32p * max(k, 1))(*[r.ctypes.data_as(abi.i32p) for _, _, r in peers])
+        no = self.plan.not_owned
+        abi.check(abi.lib().tfem_operator_set_nccl(
+            self.op.h, h, k, peer, n_send, s_idx, n_recv, r_idx, len(no),
+            no.ctypes.data_as(abi.i32p) if len(no) else None))
+
+    def close(self):
+        from . import abi
+        if getattr(self, "op", None) is not None:
+            self.op = None  # the operator references the communicator
+        if getattr(self, "nccl", None):
+            abi.lib().tfem_nccl_destroy(self.nccl)
+            self.nccl = None
+
     @property
     def n_owned(self) -> int:
         return len(self.plan.owned)
@@ -239,17 +285,12 @@ def bench_distributed(args, rank: int, world: int, local: int):
 
     if getattr(args, "bp", 3) != 3:
         raise SystemExit("bench: the distributed run is BP3 (diffusion, Jacobi) only")
-    # Test-only knobs (one-GPU boxes): all ranks on device 0 over gloo.  The
-    # production path is NCCL with one GPU per rank.
-    if os.environ.get("TFEM_DIST_SAME_DEVICE") == "1":
-        local = 0
-    backend = os.environ.get("TFEM_DIST_BACKEND", "nccl")
+    # one GPU per rank; the CG's halo / dots go through the library's own
+    # NCCL communicator (DistOperator, transport "nccl"); the process group
+    # ships its id, and times the run (barrier, max over ranks)
     torch.cuda.set_device(local)
-    if backend == "nccl":
-        tdist.init_process_group("nccl", rank=rank, world_size=world,
-                                 device_id=torch.device("cuda", local))
-    else:
-        tdist.init_process_group(backend, rank=rank, world_size=world)
+    tdist.init_process_group("nccl", rank=rank, world_size=world,
+                             device_id=torch.device("cuda", local))
     dev = tf.Device(local, numerics=args.numerics)
     n = args.cells or {2: round((10.0e6 ** 0.5 - 1) / args.order),
                    3: round((10.0e6 ** (1 / 3) - 1) / args.order)}[args.dim]
@@ -337,7 +378,10 @@ def bench_distributed(args, rank: int, world: int, local: int):
             "e2e": e2e, "cpu_baseline": None, "clocks": clk.summary(),
             "gpu_launches": launches, "setup_s": setup_s,
             "partition": f"{world} slabs of {slab.hi - slab.lo} cell layers + 1 ghost layer",
+            "transport": "library NCCL (ncclSend/ncclRecv halo + ncclAllReduce dots, "
+                         "captured in the CG graphs)",
         }
         print(json.dumps(line))
     tdist.barrier()
+    d.close()
     tdist.destroy_process_group()

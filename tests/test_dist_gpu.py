@@ -1,7 +1,9 @@
-"""GPU: the library's distributed CG loop (tfem_operator_set_comm hooks,
-owned-DOF dots, halo pack/unpack, rank-local folds + allreduce).
+"""GPU: the library's distributed CG loop (owned-DOF dots, halo pack/unpack,
+rank-local folds + allreduce).
 
-* 1 rank over NCCL: bit-identical iterates to the single-device solver.
+* 1 rank over the library's own NCCL communicator (tfem_nccl_create,
+  tfem_operator_set_nccl; ncclAllReduce inside the captured CG graphs):
+  bit-identical iterates to the single-device solver.
 * 2 ranks sharing the one GPU over gloo (host-staged hooks; no kernel waits
   on another process): same iteration count as the single-device solve of
   the global problem, same solution on owned DOFs.
@@ -48,6 +50,7 @@ def test_one_rank_nccl_matches_single_device(dev):
     try:
         n, p = (40, 30), 3
         d = DistOperator(dev, partition(2, n, p, 0, 1))
+        assert d.transport == "nccl" and d.nccl  # the library's own communicator
         sp, op, ess, _ = single_device_solution(dev, n, p, 1e-10, 2000, 0)
         assert (d.plan.ess == ess).all() and len(d.plan.not_owned) == 0
         b = np.random.default_rng(4).uniform(-1, 1, sp.n_dofs)
@@ -60,6 +63,7 @@ def test_one_rank_nccl_matches_single_device(dev):
         r4 = tf.cg_solve(op, b, 0.0, 37, op.diagonal())
         assert r3.iterations == r4.iterations == 37
         assert (r3.x.numpy() == r4.x.numpy()).all()
+        d.close()
     finally:
         tdist.destroy_process_group()
 
