@@ -452,6 +452,20 @@ def run_tfem(args):
                "ms_per_step": 1e3 * t_e / args.steps,
                "api": "tfem_cg_solve_host (pinned host b, diag -> x)"}
 
+    # ---- end to end through the reference's own C++ API (the drop-in build:
+    # form_linear_system + cg_solve on host Vectors, integration/bench_dropin)
+    dropin = None
+    exe = ROOT / "integration" / "_build" / "bin" / "bench_dropin"
+    if not args.no_e2e and args.dim == 2 and args.bp == 3 and exe.exists():
+        del op, a, sp
+        dev.sync()
+        out = subprocess.run([str(exe), str(n), str(p), str(args.iters), str(args.steps),
+                              str(args.warmup)], capture_output=True, text=True, timeout=900)
+        try:
+            dropin = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception:
+            dropin = {"error": (out.stdout + out.stderr)[-500:]}
+
     cpu = None
     if not args.no_cpu_baseline and args.dim == 2:
         try:
@@ -477,7 +491,7 @@ def run_tfem(args):
                      "peak_source": peak_kind, "fp64": fp64},
         "cg_roofline": {"achieved": cg_achieved, "frac": cg_achieved / peak, "unit": "GB/s",
                         "bytes_per_dof_iteration": b_it / N, "kernels": cg_kernels},
-        "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
+        "e2e": e2e, "e2e_dropin": dropin, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
         "bit_exact_numerics": exact, "setup_s": setup_s, "result_check": check,
     }
     print(json.dumps(line))

@@ -122,6 +122,20 @@ double *Mirror::device_readwrite(const double *host, std::size_t n)
    return d_;
 }
 
+void Mirror::init(double *host, std::size_t n, double value)
+{
+   if (value != 0.0 || n * sizeof(double) < kPinnedBytes) {
+      std::fill(host, host + n, value);
+      return;
+   }
+   double *d = device_write(n);
+   tfem_vec *v = nullptr;
+   check(tfem_vec_wrap(context(), d, static_cast<int64_t>(n), &v));
+   const int rc = tfem_vec_fill(v, 0.0);
+   tfem_vec_destroy(v);
+   check(rc);
+}
+
 Mirror::Mirror(const Mirror &o) { *this = o; }
 
 Mirror &Mirror::operator=(const Mirror &o)

@@ -24,6 +24,7 @@
 #include <cstddef>
 #include <cstdlib>
 #include <new>
+#include <utility>
 
 struct tfem_ctx;
 
@@ -48,6 +49,17 @@ struct HostAllocator {
    template <class U>
    HostAllocator(const HostAllocator<U> &) noexcept
    {
+   }
+   // default-initialize (no zero fill): Vector decides how to initialize
+   template <class U>
+   void construct(U *p) noexcept
+   {
+      ::new (static_cast<void *>(p)) U;
+   }
+   template <class U, class... A>
+   void construct(U *p, A &&...a)
+   {
+      ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
    }
    T *allocate(std::size_t n)
    {
@@ -85,6 +97,10 @@ public:
    Mirror &operator=(Mirror &&o) noexcept;
    ~Mirror();
 
+   /// Vector(n, value): fill the host copy -- or, for a zero vector of
+   /// pinned size, zero the device copy instead (the host copy then loads
+   /// on first host access, like any device-newer vector).
+   void init(double *host, std::size_t n, double value);
    /// Before any host read: downloads into `host` if the device is newer.
    void host_read(double *host, std::size_t n) const
    {
