@@ -389,6 +389,10 @@ int tfem_cg_profile(tfem_ctx *ctx, const tfem_operator *op, const tfem_vec *b,
  * peak of the context's device in TFLOP/s -- the FP64 roofline bench.py
  * reports the element kernels against. */
 int tfem_fp64_peak(tfem_ctx *ctx, double *tflops);
+/* Diagnostics: the measured FP64 tensor-core (DMMA, mma.sync m8n8k4) peak in
+ * TFLOP/s -- the ceiling a DMMA contraction would have (north_star: DMMA only
+ * where it beats CUDA-core DFMA). */
+int tfem_dmma_peak(tfem_ctx *ctx, double *tflops);
 
 #ifdef __cplusplus
 }

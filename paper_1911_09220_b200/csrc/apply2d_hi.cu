@@ -90,9 +90,15 @@ struct Cfg2 {
    static constexpr size_t kSmem = kWarpBytes * kW;
 };
 
-template <int P, int Q, int KIND, bool EXACT, bool EDOT>
+// CO (collocated, BP5): q = p + 1 Gauss-Lobatto points on the nodes, B1d = I
+// exactly: T2 = V, dx = T1, S2 = W2, vx = S1 (the B contractions are copies,
+// so the stages read the source in place).  In EXACT numerics the skipped
+// sums add only signed zeros, so results stay bit-identical up to the sign
+// of a zero.
+template <int P, int Q, int KIND, bool EXACT, bool EDOT, bool CO>
 __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi_kernel(const ApplyArgs a)
 {
+   static_assert(!CO || Q == P + 1, "collocation needs q = p + 1");
    using W = Warp2<P, Q, KIND>;
    constexpr int D1 = W::D1, ND = W::ND, NQD = W::NQD, NC = W::NC, GRP = W::GRP;
    constexpr int kW = Cfg2<P, Q, KIND, EXACT>::kW, kBlock = Cfg2<P, Q, KIND, EXACT>::kBlock;
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi
             // row once and runs the unrolled outputs along it with the basis
             // operands as compile-time constant-bank operands (the
             // per-output lane mapping was shared-memory bound).
-            if (lane < GRP * D1) { // contract x: T[qx][b], a lane per (e, b)
+            if (lane < GRP * D1 && !(CO && KIND == TFEM_MASS)) { // contract x: T[qx][b], a lane per (e, b)
                const int j = lane / D1, b = lane % D1;
                const double *V = sm.V[vb] + j * ND;
                double v[D1];
@@ -231,10 +237,10 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi
 #pragma unroll
                   for (int kk = 1; kk < D1; kk++) {
                      if (KIND == TFEM_DIFFUSION) s1 = mac<EXACT>(s1, a.t.G[qx][kk], v[kk]);
-                     s2 = mac<EXACT>(s2, a.t.B[qx][kk], v[kk]);
+                     if (!CO) s2 = mac<EXACT>(s2, a.t.B[qx][kk], v[kk]);
                   }
                   if (KIND == TFEM_DIFFUSION) sm.T1[j][qx * D1 + b] = s1;
-                  sm.T2[j][qx * D1 + b] = s2;
+                  if (!CO) sm.T2[j][qx * D1 + b] = s2; // CO: T2 = V in place
                }
             }
             prefetch_x(gn, gnext, vb ^ 1); // the other V buffer is free
@@ -245,20 +251,21 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi
                const double *qd = qs + j * W::kQe;
                const bool live = j < cnt;
                double t1[D1], t2[D1];
+               const double *T2s = CO ? sm.V[vb] + j * ND : sm.T2[j]; // CO: T2 = V ([a D1 + b])
 #pragma unroll
                for (int b = 0; b < D1; b++) {
                   if (KIND == TFEM_DIFFUSION) t1[b] = sm.T1[j][qx * D1 + b];
-                  t2[b] = sm.T2[j][qx * D1 + b];
+                  t2[b] = T2s[qx * D1 + b];
                }
 #pragma unroll
                for (int qy = 0; qy < Q; qy++) {
                   const int t = qy * Q + qx;
                   if (KIND == TFEM_DIFFUSION) {
-                     double dx = mul<EXACT>(t1[0], a.t.B[qy][0]);
+                     double dx = CO ? t1[qy] : mul<EXACT>(t1[0], a.t.B[qy][0]);
                      double dy = mul<EXACT>(t2[0], a.t.G[qy][0]);
 #pragma unroll
                      for (int b = 1; b < D1; b++) {
-                        dx = mac<EXACT>(dx, t1[b], a.t.B[qy][b]);
+                        if (!CO) dx = mac<EXACT>(dx, t1[b], a.t.B[qy][b]);
                         dy = mac<EXACT>(dy, t2[b], a.t.G[qy][b]);
                      }
                      const double d0 = qd[t], d1 = qd[NQD + t], d2 = qd[2 * NQD + t];
@@ -268,9 +275,10 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi
                      sm.W1[j][qx * Q + qy] = w1;
                      sm.W2[j][qx * Q + qy] = w2;
                   } else {
-                     double u = mul<EXACT>(t2[0], a.t.B[qy][0]);
+                     double u = CO ? t2[qy] : mul<EXACT>(t2[0], a.t.B[qy][0]);
 #pragma unroll
-                     for (int b = 1; b < D1; b++) u = mac<EXACT>(u, t2[b], a.t.B[qy][b]);
+                     for (int b = 1; b < D1; b++)
+                        if (!CO) u = mac<EXACT>(u, t2[b], a.t.B[qy][b]);
                      const double w = mul<EXACT>(u, qd[t]);
                      if (EDOT && live) dot = mac<EXACT>(dot, u, w);
                      sm.W2[j][qx * Q + qy] = w;
@@ -279,26 +287,26 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
-            if (lane < GRP * Q) { // contract qx: S[a][qy], a lane per (e, qy)
+            if (lane < GRP * Q && !(CO && KIND == TFEM_MASS)) { // contract qx: S[a][qy], a lane per (e, qy)
                const int j = lane / Q, qy = lane % Q;
                double w1[Q], w2[Q];
 #pragma unroll
                for (int qx = 0; qx < Q; qx++) {
                   if (KIND == TFEM_DIFFUSION) w1[qx] = sm.W1[j][qx * Q + qy];
-                  w2[qx] = sm.W2[j][qx * Q + qy];
+                  if (!CO) w2[qx] = sm.W2[j][qx * Q + qy];
                }
 #pragma unroll
                for (int i = 0; i < D1; i++) {
                   if (KIND == TFEM_DIFFUSION) {
                      double s1 = mul<EXACT>(a.t.G[0][i], w1[0]);
-                     double s2 = mul<EXACT>(a.t.B[0][i], w2[0]);
+                     double s2 = CO ? 0.0 : mul<EXACT>(a.t.B[0][i], w2[0]);
 #pragma unroll
                      for (int qx = 1; qx < Q; qx++) {
                         s1 = mac<EXACT>(s1, a.t.G[qx][i], w1[qx]);
-                        s2 = mac<EXACT>(s2, a.t.B[qx][i], w2[qx]);
+                        if (!CO) s2 = mac<EXACT>(s2, a.t.B[qx][i], w2[qx]);
                      }
                      sm.S1[j][i * Q + qy] = s1;
-                     sm.S2[j][i * Q + qy] = s2;
+                     if (!CO) sm.S2[j][i * Q + qy] = s2; // CO: S2 = W2 in place
                   } else {
                      double sv = mul<EXACT>(a.t.B[0][i], w2[0]);
 #pragma unroll
@@ -311,24 +319,28 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi
             if (lane < cnt * D1) { // contract qy: r(a, b), a lane per (e, a); epilogue
                const int j = lane / D1, ia = lane % D1;
                double s1[Q], s2[Q];
+               // CO: S2 = W2 ([qx = a][qy])
+               const double *S2s = CO ? sm.W2[j] : sm.S2[j];
 #pragma unroll
                for (int qy = 0; qy < Q; qy++) {
                   if (KIND == TFEM_DIFFUSION) s1[qy] = sm.S1[j][ia * Q + qy];
-                  s2[qy] = sm.S2[j][ia * Q + qy];
+                  s2[qy] = S2s[ia * Q + qy];
                }
                const int64_t e = g * GRP + j;
 #pragma unroll
                for (int b = 0; b < D1; b++) {
                   double rr;
                   if (KIND == TFEM_DIFFUSION) {
-                     double vx = mul<EXACT>(s1[0], a.t.B[0][b]);
+                     double vx = CO ? s1[b] : mul<EXACT>(s1[0], a.t.B[0][b]);
                      double vy = mul<EXACT>(s2[0], a.t.G[0][b]);
 #pragma unroll
                      for (int qy = 1; qy < Q; qy++) {
-                        vx = mac<EXACT>(vx, s1[qy], a.t.B[qy][b]);
+                        if (!CO) vx = mac<EXACT>(vx, s1[qy], a.t.B[qy][b]);
                         vy = mac<EXACT>(vy, s2[qy], a.t.G[qy][b]);
                      }
                      rr = add<EXACT>(vx, vy);
+                  } else if (CO) {
+                     rr = s2[b];
                   } else {
                      rr = mul<EXACT>(s2[0], a.t.B[0][b]);
 #pragma unroll
@@ -369,25 +381,33 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi
 }
 
 // grid: min(blocks of kW groups, persistent blocks) -- elem_blocks (apply.cu)
-template <int P, int Q, int KIND, bool EXACT>
+template <int P, int Q, int KIND, bool EXACT, bool CO>
 void launch(const ApplyArgs &a, cudaStream_t s, unsigned grid)
 {
    using C = Cfg2<P, Q, KIND, EXACT>;
    static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
    if (a.energy_dot) {
-      max_dynamic_smem((const void *)apply2d_hi_kernel<P, Q, KIND, EXACT, true>, C::kSmem);
-      apply2d_hi_kernel<P, Q, KIND, EXACT, true><<<grid, C::kBlock, C::kSmem, s>>>(a);
+      max_dynamic_smem((const void *)apply2d_hi_kernel<P, Q, KIND, EXACT, true, CO>, C::kSmem);
+      apply2d_hi_kernel<P, Q, KIND, EXACT, true, CO><<<grid, C::kBlock, C::kSmem, s>>>(a);
    } else {
-      max_dynamic_smem((const void *)apply2d_hi_kernel<P, Q, KIND, EXACT, false>, C::kSmem);
-      apply2d_hi_kernel<P, Q, KIND, EXACT, false><<<grid, C::kBlock, C::kSmem, s>>>(a);
+      max_dynamic_smem((const void *)apply2d_hi_kernel<P, Q, KIND, EXACT, false, CO>, C::kSmem);
+      apply2d_hi_kernel<P, Q, KIND, EXACT, false, CO><<<grid, C::kBlock, C::kSmem, s>>>(a);
    }
 }
 
+template <int P, int Q, int KIND, bool EXACT>
+Launch launcher(bool colloc)
+{
+   if constexpr (Q == P + 1)
+      if (colloc) return launch<P, Q, KIND, EXACT, true>;
+   return launch<P, Q, KIND, EXACT, false>;
+}
+
 template <int P, int Q, int KIND>
-KernelPick make(bool exact, int sm_count)
+KernelPick make(bool exact, int sm_count, bool colloc)
 {
    KernelPick k;
-   k.launch = exact ? launch<P, Q, KIND, true> : launch<P, Q, KIND, false>;
+   k.launch = exact ? launcher<P, Q, KIND, true>(colloc) : launcher<P, Q, KIND, false>(colloc);
    k.elems_per_block = (exact ? Cfg2<P, Q, KIND, true>::kW : Cfg2<P, Q, KIND, false>::kW) * Warp2<P, Q, KIND>::GRP;
    k.threads = exact ? Cfg2<P, Q, KIND, true>::kBlock : Cfg2<P, Q, KIND, false>::kBlock;
    k.persistent_blocks = sm_count;
@@ -396,32 +416,32 @@ KernelPick make(bool exact, int sm_count)
 }
 
 template <int P, int KIND>
-KernelPick pick_q(int nq, bool exact, int sm)
+KernelPick pick_q(int nq, bool exact, int sm, bool co)
 {
-   if (nq == P + 2) return make<P, P + 2, KIND>(exact, sm);
-   if (nq == P + 1) return make<P, P + 1, KIND>(exact, sm);
+   if (nq == P + 2) return make<P, P + 2, KIND>(exact, sm, false);
+   if (nq == P + 1) return make<P, P + 1, KIND>(exact, sm, co);
    return {};
 }
 
 template <int KIND>
-KernelPick pick_p(int p, int nq, bool exact, int sm)
+KernelPick pick_p(int p, int nq, bool exact, int sm, bool co)
 {
    switch (p) {
-   case 4: return pick_q<4, KIND>(nq, exact, sm);
-   case 5: return pick_q<5, KIND>(nq, exact, sm);
-   case 6: return pick_q<6, KIND>(nq, exact, sm);
-   case 7: return pick_q<7, KIND>(nq, exact, sm);
-   case 8: return pick_q<8, KIND>(nq, exact, sm);
+   case 4: return pick_q<4, KIND>(nq, exact, sm, co);
+   case 5: return pick_q<5, KIND>(nq, exact, sm, co);
+   case 6: return pick_q<6, KIND>(nq, exact, sm, co);
+   case 7: return pick_q<7, KIND>(nq, exact, sm, co);
+   case 8: return pick_q<8, KIND>(nq, exact, sm, co);
    }
    return {};
 }
 
 } // namespace
 
-KernelPick pick_apply2d_hi(int p, int nq, int kind, bool exact, int sm_count)
+KernelPick pick_apply2d_hi(int p, int nq, int kind, bool exact, int sm_count, bool colloc)
 {
-   return kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact, sm_count)
-                            : pick_p<TFEM_DIFFUSION>(p, nq, exact, sm_count);
+   return kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact, sm_count, colloc)
+                            : pick_p<TFEM_DIFFUSION>(p, nq, exact, sm_count, colloc);
 }
 
 } // namespace tfem

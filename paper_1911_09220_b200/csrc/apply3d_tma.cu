@@ -66,25 +66,23 @@ struct Cfg3 {
    static constexpr size_t kWarpBytes = sizeof(Warp3<P, Q, KIND>);
    // computing warps as shared memory allows: 224 KB (vs 200) is +9 % at
    // p = 4 (6 -> 7 warps), neutral where the 11-warp cap or the warp size binds
-#ifndef TFEM_3D_SMEM_KB
-#define TFEM_3D_SMEM_KB 224
-#endif
-   static constexpr int kW0 = static_cast<int>((TFEM_3D_SMEM_KB * 1024) / kWarpBytes);
+   static constexpr int kW0 = static_cast<int>((224 * 1024) / kWarpBytes);
    // warp cap from the registers ptxas needs: 11 (170 each) by default, 15
    // (128) at p <= 2 with q <= p + 2 except p = 2, q = 4, 13 (146) at p = 3, q = 5
-#ifndef TFEM_3D_WIDE
-#define TFEM_3D_WIDE 1
-#endif
-   static constexpr int kMaxW = !TFEM_3D_WIDE || KIND != TFEM_DIFFUSION ? 11
+   static constexpr int kMaxW = KIND != TFEM_DIFFUSION ? 11
                               : (Q <= 3) ? 15 : (P == 3 && Q == 5) ? 13 : 11;
    static constexpr int kW = kW0 > kMaxW ? kMaxW : (kW0 < 1 ? 1 : kW0); // compute warps
    static constexpr int kBlock = 32 * (kW + 1);
    static constexpr size_t kSmem = kWarpBytes * kW;
 };
 
-template <int P, int Q, int KIND, bool EDOT>
+// CO (collocated, BP5): q = p + 1 Gauss-Lobatto points on the Gauss-Lobatto
+// nodes, so B1d = I exactly (quadrature.cpp:91-125, basis.cpp:53-58): every
+// B contraction is a copy and is skipped -- half the FP64 work per element.
+template <int P, int Q, int KIND, bool EDOT, bool CO>
 __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kernel(const ApplyArgs a)
 {
+   static_assert(!CO || Q == P + 1, "collocation needs q = p + 1");
    using W = Warp3<P, Q, KIND>;
    constexpr int D1 = W::D1, ND = W::ND, NQD = W::NQD, NC = W::NC, EPW = W::EPW;
    constexpr int kW = Cfg3<P, Q, KIND>::kW, kBlock = Cfg3<P, Q, KIND>::kBlock;
@@ -207,8 +205,24 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          const double *V = sm.V[vb];
          // contract a -> TB / TG [e][c][b][qx]: a lane per (e, c, b) row, qx
          // unrolled (basis operands from the constant bank) when the rows
-         // fit one pass of the warp; else a lane per output
-         if constexpr (!kRows1) {
+         // fit one pass of the warp; else a lane per output.  CO: TB = V,
+         // only TG is formed.
+         if constexpr (CO) {
+            for (int it = lane; it < EPW * D1 * D1; it += 32) {
+               const int j = it / (D1 * D1), cb = it % (D1 * D1);
+               double v[D1];
+#pragma unroll
+               for (int kk = 0; kk < D1; kk++) v[kk] = V[j * ND + cb * D1 + kk];
+               double *TGo = sm.TG + j * kEt + cb * kSt;
+#pragma unroll
+               for (int jx = 0; jx < Q; jx++) {
+                  double sg = 0.0;
+#pragma unroll
+                  for (int kk = 0; kk < D1; kk++) sg = fma(a.t.G[jx][kk], v[kk], sg);
+                  TGo[jx] = sg;
+               }
+            }
+         } else if constexpr (!kRows1) {
             for (int jj = lane; jj < EPW * NT; jj += 32) {
                const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q;
                double sb = 0.0, sg = 0.0;
@@ -252,6 +266,21 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             const bool live = ej < cnt;
             const double *TB = sm.TB + ej * kEt, *TG = sm.TG + ej * kEt;
             double UBB[D1], UBG[D1], UGB[D1];
+            if constexpr (CO) {
+               // UBB = V[c][qy][qx], UGB = TG[c][qy][qx], UBG = G_y V
+               const double *Ve = V + ej * ND;
+#pragma unroll
+               for (int c = 0; c < D1; c++) {
+                  UBB[c] = Ve[(c * D1 + qy) * D1 + qx];
+                  if (KIND == TFEM_DIFFUSION) {
+                     UGB[c] = TG[(c * D1 + qy) * kSt + qx];
+                     double bg = 0.0;
+#pragma unroll
+                     for (int b = 0; b < D1; b++) bg = fma(sG[qy][b], Ve[(c * D1 + b) * D1 + qx], bg);
+                     UBG[c] = bg;
+                  }
+               }
+            } else
 #pragma unroll
             for (int c = 0; c < D1; c++) { // contract b
                double bb = 0.0, bg = 0.0, gb = 0.0;
@@ -280,19 +309,34 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                // constant bank, not shared memory
                if (KIND == TFEM_MASS) {
                   double u = 0.0;
+                  if constexpr (CO) {
+                     u = UBB[qz];
+                  } else {
 #pragma unroll
-                  for (int c = 0; c < D1; c++) u = fma(a.t.B[qz][c], UBB[c], u);
+                     for (int c = 0; c < D1; c++) u = fma(a.t.B[qz][c], UBB[c], u);
+                  }
                   const double w = u * qd[q];
                   if (EDOT && live) dot = fma(u, w, dot);
+                  if constexpr (CO) {
+                     Px[qz] = w;
+                  } else {
 #pragma unroll
-                  for (int c = 0; c < D1; c++) Px[c] = fma(a.t.B[qz][c], w, Px[c]);
+                     for (int c = 0; c < D1; c++) Px[c] = fma(a.t.B[qz][c], w, Px[c]);
+                  }
                } else {
                   double ux = 0.0, uy = 0.0, uz = 0.0;
+                  if constexpr (CO) {
+                     ux = UGB[qz];
+                     uy = UBG[qz];
 #pragma unroll
-                  for (int c = 0; c < D1; c++) {
-                     ux = fma(a.t.B[qz][c], UGB[c], ux);
-                     uy = fma(a.t.B[qz][c], UBG[c], uy);
-                     uz = fma(a.t.G[qz][c], UBB[c], uz);
+                     for (int c = 0; c < D1; c++) uz = fma(a.t.G[qz][c], UBB[c], uz);
+                  } else {
+#pragma unroll
+                     for (int c = 0; c < D1; c++) {
+                        ux = fma(a.t.B[qz][c], UGB[c], ux);
+                        uy = fma(a.t.B[qz][c], UBG[c], uy);
+                        uz = fma(a.t.G[qz][c], UBB[c], uz);
+                     }
                   }
                   const double D00 = qd[q], D01 = qd[NQD + q], D02 = qd[2 * NQD + q];
                   const double D11 = qd[3 * NQD + q], D12 = qd[4 * NQD + q], D22 = qd[5 * NQD + q];
@@ -300,11 +344,18 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                   const double wy = fma(D12, uz, fma(D11, uy, D01 * ux));
                   const double wz = fma(D22, uz, fma(D12, uy, D02 * ux));
                   if (EDOT && live) dot = fma(uz, wz, fma(uy, wy, fma(ux, wx, dot)));
+                  if constexpr (CO) {
+                     Px[qz] = wx;
+                     Py[qz] = wy;
 #pragma unroll
-                  for (int c = 0; c < D1; c++) {
-                     Px[c] = fma(a.t.B[qz][c], wx, Px[c]);
-                     Py[c] = fma(a.t.B[qz][c], wy, Py[c]);
-                     Pz[c] = fma(a.t.G[qz][c], wz, Pz[c]);
+                     for (int c = 0; c < D1; c++) Pz[c] = fma(a.t.G[qz][c], wz, Pz[c]);
+                  } else {
+#pragma unroll
+                     for (int c = 0; c < D1; c++) {
+                        Px[c] = fma(a.t.B[qz][c], wx, Px[c]);
+                        Py[c] = fma(a.t.B[qz][c], wy, Py[c]);
+                        Pz[c] = fma(a.t.G[qz][c], wz, Pz[c]);
+                     }
                   }
                }
             }
@@ -321,8 +372,26 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          __syncwarp();
          if (lane == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
          // contract qy -> [e][c][b][qx] (x-gradient part in TB, y + z in TG):
-         // a lane per (e, c, qx), b unrolled (or a lane per output)
-         if constexpr (!kRows3) {
+         // a lane per (e, c, qx), b unrolled (or a lane per output).  CO: TB
+         // is Px itself (read in place below), TG = G_y Py + Pz.
+         if constexpr (CO) {
+            for (int it = lane; it < EPW * Q * D1; it += 32) {
+               const int j = it / (Q * D1), r = it % (Q * D1), jx = r % Q, c = r / Q;
+               const int po = j * kEp + c * kSp + jx;
+               if (KIND == TFEM_DIFFUSION) {
+                  double py[Q];
+#pragma unroll
+                  for (int y = 0; y < Q; y++) py[y] = sm.Py[po + y * Q];
+#pragma unroll
+                  for (int b = 0; b < D1; b++) {
+                     double syz = sm.Pz[po + b * Q];
+#pragma unroll
+                     for (int y = 0; y < Q; y++) syz = fma(a.t.G[y][b], py[y], syz);
+                     sm.TG[j * kEt + (c * D1 + b) * kSt + jx] = syz;
+                  }
+               }
+            }
+         } else if constexpr (!kRows3) {
             for (int jj = lane; jj < EPW * NT; jj += 32) {
                const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q, b = cb % D1, c = cb / D1;
                const int po = j * kEp;
@@ -377,7 +446,9 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             double tb[Q], tg[Q];
 #pragma unroll
             for (int x = 0; x < Q; x++) {
-               tb[x] = sm.TB[j * kEt + cb * kSt + x];
+               // CO: TB[c][b][x] = Px[c][y = b][x]
+               tb[x] = CO ? sm.Px[j * kEp + (cb / D1) * kSp + (cb % D1) * Q + x]
+                          : sm.TB[j * kEt + cb * kSt + x];
                if (KIND == TFEM_DIFFUSION) tg[x] = sm.TG[j * kEt + cb * kSt + x];
             }
             const int64_t e = g * EPW + j;
@@ -385,15 +456,26 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             for (int ka = 0; ka < kA; ka++) {
                const int ia = kRows1 ? ka : it % D1;
                double r = 0.0;
-#pragma unroll
-               for (int x = 0; x < Q; x++) {
-                  const double gx = kRows1 ? a.t.G[x][ka] : sG[x][ia];
-                  const double bx = kRows1 ? a.t.B[x][ka] : sB[x][ia];
+               if constexpr (CO) {
+                  // r = G_x TB + TG[.., a] (B_x = I)
                   if (KIND == TFEM_MASS) {
-                     r = fma(bx, tb[x], r);
+                     r = kRows1 ? tb[ka] : tb[ia];
                   } else {
-                     r = fma(gx, tb[x], r);
-                     r = fma(bx, tg[x], r);
+#pragma unroll
+                     for (int x = 0; x < Q; x++) r = fma(kRows1 ? a.t.G[x][ka] : sG[x][ia], tb[x], r);
+                     r += kRows1 ? tg[ka] : tg[ia];
+                  }
+               } else {
+#pragma unroll
+                  for (int x = 0; x < Q; x++) {
+                     const double gx = kRows1 ? a.t.G[x][ka] : sG[x][ia];
+                     const double bx = kRows1 ? a.t.B[x][ka] : sB[x][ia];
+                     if (KIND == TFEM_MASS) {
+                        r = fma(bx, tb[x], r);
+                     } else {
+                        r = fma(gx, tb[x], r);
+                        r = fma(bx, tg[x], r);
+                     }
                   }
                }
                const int i = cb * D1 + ia;
@@ -430,27 +512,30 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
 }
 
 // grid: min(blocks of kW warps, persistent blocks) -- elem_blocks (apply.cu)
-template <int P, int Q, int KIND>
+template <int P, int Q, int KIND, bool CO>
 void launch(const ApplyArgs &a, cudaStream_t s, unsigned grid)
 {
    using C = Cfg3<P, Q, KIND>;
    static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
    if (a.energy_dot) {
-      max_dynamic_smem((const void *)apply3d_tma_kernel<P, Q, KIND, true>, C::kSmem);
-      apply3d_tma_kernel<P, Q, KIND, true><<<grid, C::kBlock, C::kSmem, s>>>(a);
+      max_dynamic_smem((const void *)apply3d_tma_kernel<P, Q, KIND, true, CO>, C::kSmem);
+      apply3d_tma_kernel<P, Q, KIND, true, CO><<<grid, C::kBlock, C::kSmem, s>>>(a);
    } else {
-      max_dynamic_smem((const void *)apply3d_tma_kernel<P, Q, KIND, false>, C::kSmem);
-      apply3d_tma_kernel<P, Q, KIND, false><<<grid, C::kBlock, C::kSmem, s>>>(a);
+      max_dynamic_smem((const void *)apply3d_tma_kernel<P, Q, KIND, false, CO>, C::kSmem);
+      apply3d_tma_kernel<P, Q, KIND, false, CO><<<grid, C::kBlock, C::kSmem, s>>>(a);
    }
 }
 
 template <int P, int Q, int KIND>
-KernelPick make(int sm_count)
+KernelPick make(int sm_count, bool colloc)
 {
    KernelPick k;
    // bulk copies need 16-byte sizes and element strides
    if constexpr ((Warp3<P, Q, KIND>::NC * Q * Q * Q) % 2 == 0) {
-      k.launch = launch<P, Q, KIND>;
+      if constexpr (Q == P + 1)
+         k.launch = colloc ? launch<P, Q, KIND, true> : launch<P, Q, KIND, false>;
+      else
+         k.launch = launch<P, Q, KIND, false>;
       k.elems_per_block = Cfg3<P, Q, KIND>::kW * Warp3<P, Q, KIND>::EPW;
       k.threads = Cfg3<P, Q, KIND>::kBlock;
       k.persistent_blocks = sm_count;
@@ -460,25 +545,25 @@ KernelPick make(int sm_count)
 }
 
 template <int KIND>
-KernelPick pick_kind(int p, int nq, int sm)
+KernelPick pick_kind(int p, int nq, int sm, bool co)
 {
    // up to Q = 7; larger Q leaves too few warps per SM (the group kernel)
    switch (p) {
-   case 1: return nq == 3 ? make<1, 3, KIND>(sm) : nq == 2 ? make<1, 2, KIND>(sm) : KernelPick{};
-   case 2: return nq == 4 ? make<2, 4, KIND>(sm) : nq == 3 ? make<2, 3, KIND>(sm) : KernelPick{};
-   case 3: return nq == 5 ? make<3, 5, KIND>(sm) : nq == 4 ? make<3, 4, KIND>(sm) : KernelPick{};
-   case 4: return nq == 5 ? make<4, 5, KIND>(sm) : nq == 6 ? make<4, 6, KIND>(sm) : KernelPick{};
-   case 5: return nq == 6 ? make<5, 6, KIND>(sm) : nq == 7 ? make<5, 7, KIND>(sm) : KernelPick{};
+   case 1: return nq == 3 ? make<1, 3, KIND>(sm, co) : nq == 2 ? make<1, 2, KIND>(sm, co) : KernelPick{};
+   case 2: return nq == 4 ? make<2, 4, KIND>(sm, co) : nq == 3 ? make<2, 3, KIND>(sm, co) : KernelPick{};
+   case 3: return nq == 5 ? make<3, 5, KIND>(sm, co) : nq == 4 ? make<3, 4, KIND>(sm, co) : KernelPick{};
+   case 4: return nq == 5 ? make<4, 5, KIND>(sm, co) : nq == 6 ? make<4, 6, KIND>(sm, co) : KernelPick{};
+   case 5: return nq == 6 ? make<5, 6, KIND>(sm, co) : nq == 7 ? make<5, 7, KIND>(sm, co) : KernelPick{};
    }
    return {};
 }
 
 } // namespace
 
-KernelPick pick_apply3d_tma(int p, int nq, int kind, int sm_count)
+KernelPick pick_apply3d_tma(int p, int nq, int kind, int sm_count, bool colloc)
 {
-   return kind == TFEM_MASS ? pick_kind<TFEM_MASS>(p, nq, sm_count)
-                            : pick_kind<TFEM_DIFFUSION>(p, nq, sm_count);
+   return kind == TFEM_MASS ? pick_kind<TFEM_MASS>(p, nq, sm_count, colloc)
+                            : pick_kind<TFEM_DIFFUSION>(p, nq, sm_count, colloc);
 }
 
 } // namespace tfem

@@ -385,7 +385,7 @@ KernelPick pick_q(int dim, int nq, bool exact)
          if (nq == P + 2) return make2d<P, P + 2, KIND>(exact);
          if (nq == P + 1) return make2d<P, P + 1, KIND>(exact);
       }
-   } else {
+   } else if constexpr (P <= kMaxP3D) {
       if (nq == P + 2) return make3d<P, P + 2, KIND>();
       if (nq == P + 1) return make3d<P, P + 1, KIND>();
    }
@@ -404,6 +404,15 @@ KernelPick pick_p(int dim, int p, int nq, bool exact)
    case 6: return pick_q<6, KIND>(dim, nq, exact);
    case 7: return pick_q<7, KIND>(dim, nq, exact);
    case 8: return pick_q<8, KIND>(dim, nq, exact);
+   // 2D p = 9..16: the generic shared-memory stages
+   case 9: return pick_q<9, KIND>(dim, nq, exact);
+   case 10: return pick_q<10, KIND>(dim, nq, exact);
+   case 11: return pick_q<11, KIND>(dim, nq, exact);
+   case 12: return pick_q<12, KIND>(dim, nq, exact);
+   case 13: return pick_q<13, KIND>(dim, nq, exact);
+   case 14: return pick_q<14, KIND>(dim, nq, exact);
+   case 15: return pick_q<15, KIND>(dim, nq, exact);
+   case 16: return pick_q<16, KIND>(dim, nq, exact);
    }
    return {};
 }

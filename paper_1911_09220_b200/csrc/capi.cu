@@ -741,6 +741,7 @@ int tfem_pa_set_basis(tfem_pa *pa, const double *B, const double *G)
       need(G, "tfem_pa_set_basis");
       std::memcpy(pa->B.data(), B, sizeof(double) * pa->B.size());
       std::memcpy(pa->G.data(), G, sizeof(double) * pa->G.size());
+      pa->colloc = false; // tables of another basis: the general kernels
    });
 }
 
@@ -1127,6 +1128,15 @@ int tfem_fp64_peak(tfem_ctx *ctx, double *tflops)
       need(ctx, "fp64_peak");
       need(tflops, "fp64_peak");
       *tflops = fp64_peak_tflops(ctx);
+   });
+}
+
+int tfem_dmma_peak(tfem_ctx *ctx, double *tflops)
+{
+   return guard([&] {
+      need(ctx, "dmma_peak");
+      need(tflops, "dmma_peak");
+      *tflops = dmma_peak_tflops(ctx);
    });
 }
 

@@ -132,8 +132,11 @@ inline ElemOrder elem_order_for(int dim, int p, bool cartesian, const int *n)
    return o;
 }
 
-constexpr int kMaxP = 8;
-constexpr int kMaxQ = 10;
+// Orders: 2D up to p = 16 (the reference's target range), with
+// up to q = p + 3 points (compute_l2_error's rule); 3D up to p = 8.
+constexpr int kMaxP = 16;
+constexpr int kMaxQ = 19;
+constexpr int kMaxP3D = 8;
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
@@ -230,6 +233,24 @@ struct tfem_restriction {
    int n_gbuckets = 0;
    Bucket gbuckets[kMaxBuckets];
    int64_t n_gshared = 0;
+   // Patch junctions (ordered 2D spaces, FMA numerics): the DOFs on the
+   // sides between warp patches, summed without the E-vector / scatter.
+   // Each warp writes one partial per side DOF (its own slots summed
+   // in-warp) to `side` ([patch][jside] doubles); the last of a junction's
+   // patches to arrive (counter) adds the partials in a fixed order and
+   // writes y.  Junctions: V (vertical side between patch columns cx-1, cx
+   // of patch row py; points Y = 1..4p-1), H (horizontal side between patch
+   // rows cy-1, cy of patch column px; points X = 1..8p-1) and corners
+   // (cx, cy).  Tables hold the DOF of every point (-1: none / not shared
+   // between patches) and the number of patches that arrive (0: inactive).
+   struct Junctions {
+      int px = 0, py = 0, jside = 0;
+      int32_t *v_dof = nullptr, *h_dof = nullptr, *c_dof = nullptr;
+      uint8_t *v_exp = nullptr, *h_exp = nullptr, *c_exp = nullptr;
+      unsigned *cnt = nullptr; // V, then H, then corner counters (zero between launches)
+      double *side = nullptr;
+   } junc;
+   bool has_junctions = false;
    // E-vector scratch (lazy) in the map's layout: slot-major [i][ne_pad],
    // element-major [e][nd] with the element's slots in evperm order (ev_em_p)
    double *evec = nullptr;
@@ -263,6 +284,9 @@ struct tfem_pa {
    tfem::ElemOrder order; // element positions of qdata (== the restriction's)
    bool elem_major() const { return tfem::elem_major_layout(dim, p); }
    std::vector<double> B, G; // nq x (p+1)
+   // B == I exactly (q = p+1 Gauss-Lobatto points on the basis nodes, BP5):
+   // the kernels skip the B contractions (collocated variants)
+   bool colloc = false;
 };
 
 struct tfem_prolongation {
@@ -427,6 +451,8 @@ void operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, doub
                    const DotSink *dot_elem, const DotSink *dot_scatter, const int *done);
 // Measured CUDA-core FP64 (DFMA) peak in TFLOP/s (probe.cu; diagnostics).
 double fp64_peak_tflops(tfem_ctx *ctx);
+// Measured FP64 tensor-core (DMMA m8n8k4) peak in TFLOP/s (probe.cu).
+double dmma_peak_tflops(tfem_ctx *ctx);
 
 void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
               int max_iters, const double *diag, double *x, tfem_cg_result *res,

@@ -32,6 +32,8 @@ struct ApplyArgs {
                     // scatter then adds only its essential DOFs' x^2)
    DotSink dot;     // fused x . y partials (CG's p . q)
    const int *done; // CG stop flag: skip the work once the solve has ended
+   int junction;    // patch-side DOFs through tfem_restriction::junc (no scatter)
+   tfem_restriction::Junctions junc;
 };
 
 using Launch = void (*)(const ApplyArgs &, cudaStream_t, unsigned);
@@ -51,9 +53,10 @@ constexpr int kElemThreads2D = 128;
 // (persistent blocks): 2D, p <= 3.
 KernelPick pick_apply2d_tma(int p, int nq, int kind, bool exact, int sm_count);
 // One element per warp with a bulk-copy qdata pipeline: 2D p >= 4.
-KernelPick pick_apply2d_hi(int p, int nq, int kind, bool exact, int sm_count);
+KernelPick pick_apply2d_hi(int p, int nq, int kind, bool exact, int sm_count, bool colloc);
 // One element per warp with a bulk-copy qdata pipeline: 3D, q^2 <= 32.
-KernelPick pick_apply3d_tma(int p, int nq, int kind, int sm_count);
+// colloc: B1d is exactly the identity (q = p+1 Gauss-Lobatto on the nodes).
+KernelPick pick_apply3d_tma(int p, int nq, int kind, int sm_count, bool colloc);
 // Thread-group-per-element kernels through shared memory: 2D p >= 4, 3D.
 KernelPick pick_apply_grp(int dim, int p, int nq, int kind, bool exact);
 

@@ -13,7 +13,7 @@ namespace tfem {
 
 namespace {
 
-constexpr int kMaxGeo = 4;          // geometry order m <= 3 on the device
+constexpr int kMaxGeo = 9;          // geometry order m <= 8 on the device
 constexpr int kMaxPts = kMaxQ + 2;  // rule points or m+2 check points
 
 struct GeoTables {
@@ -307,9 +307,10 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
                   const double *coeff_host, double coeff_const, int64_t *bad_elem)
 {
    if (kind != TFEM_DIFFUSION && kind != TFEM_MASS) invalid("pa_setup: unknown integrator kind");
-   if (p < 1 || p > kMaxP) invalid("pa_setup: order must be in [1, 8]");
-   if (nq < 1 || nq > kMaxQ) invalid("pa_setup: quadrature points per axis must be in [1, 10]");
-   if (g->order + 1 > kMaxGeo) invalid("pa_setup: geometry order must be <= 3 on the device");
+   if (p < 1 || p > (g->dim == 3 ? kMaxP3D : kMaxP))
+      invalid("pa_setup: order must be in [1, 16] (2D) / [1, 8] (3D) on the device");
+   if (nq < 1 || nq > kMaxQ) invalid("pa_setup: quadrature points per axis must be in [1, 19]");
+   if (g->order + 1 > kMaxGeo) invalid("pa_setup: geometry order must be <= 8 on the device");
    const int dim = g->dim;
    const int nqd = dim == 2 ? nq * nq : nq * nq * nq;
    auto *pa = new tfem_pa;
@@ -328,6 +329,10 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
    pa->B.resize(static_cast<size_t>(nq) * (p + 1));
    pa->G.resize(pa->B.size());
    eval_matrices(p, TFEM_NODES_GAUSS_LOBATTO, nq, rule, pa->B.data(), pa->G.data());
+   pa->colloc = nq == p + 1;
+   for (int q = 0; q < nq && pa->colloc; q++)
+      for (int i = 0; i <= p; i++)
+         if (pa->B[q * (p + 1) + i] != (q == i ? 1.0 : 0.0)) pa->colloc = false;
 
    std::vector<double> w;
    const std::vector<double> pts = gauss_points(rule, nq, &w);
@@ -386,7 +391,7 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
 
 void geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq, int rule, double *host_xyz)
 {
-   if (nq < 1 || nq > kMaxQ) invalid("geometry_points: points per axis must be in [1, 10]");
+   if (nq < 1 || nq > kMaxQ) invalid("geometry_points: points per axis must be in [1, 19]");
    const int dim = g->dim;
    const int nqd = dim == 2 ? nq * nq : nq * nq * nq;
    const GeoTables t = tables_at(g->order, gauss_points(rule, nq, nullptr), nullptr);
@@ -411,7 +416,7 @@ void linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *
 {
    if (g->dim != 2 || r->dim != 2) invalid("LinearForm: 2D spaces (forms.cpp:400-431)");
    if (r->p != p || r->ne != g->ne) invalid("LinearForm: geometry / space mismatch");
-   if (p < 1 || p > kMaxP || p + 2 > kMaxQ) invalid("LinearForm: order must be in [1, 8]");
+   if (p < 1 || p > kMaxP || p + 2 > kMaxQ) invalid("LinearForm: order must be in [1, 16]");
    const int nq = p + 2, nd = p + 1;
    std::vector<double> w;
    const std::vector<double> pts = gauss_points(TFEM_GAUSS_LEGENDRE, nq, &w);
@@ -445,7 +450,7 @@ void linear_form(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *
 void geometry_node_points(tfem_ctx *ctx, const tfem_geometry *g, int p, double *host_xy)
 {
    if (g->dim != 2) invalid("project_coefficient: 2D spaces");
-   if (p < 1 || p > kMaxP) invalid("project_coefficient: order must be in [1, 8]");
+   if (p < 1 || p > kMaxP) invalid("project_coefficient: order must be in [1, 16]");
    std::vector<double> nodes, bary;
    basis_nodes(p, TFEM_NODES_GAUSS_LOBATTO, nodes, bary);
    const GeoTables t = tables_at(g->order, nodes, nullptr);
@@ -474,7 +479,7 @@ double l2_error(tfem_ctx *ctx, const tfem_geometry *g, const tfem_restriction *r
    if (g->dim != 2 || r->dim != 2) invalid("compute_l2_error: 2D spaces");
    if (r->p != p || r->ne != g->ne) invalid("compute_l2_error: geometry / space mismatch");
    const int nq = p + 3, nd = p + 1;
-   if (nq > kMaxQ) invalid("compute_l2_error: order must be <= 7 on the device");
+   if (nq > kMaxQ) invalid("compute_l2_error: order must be <= 16 on the device");
    std::vector<double> w;
    const std::vector<double> pts = gauss_points(TFEM_GAUSS_LEGENDRE, nq, &w);
    const GeoTables t = tables_at(g->order, pts, &w);
