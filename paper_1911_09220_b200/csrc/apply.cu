@@ -311,21 +311,12 @@ void check_pair(const tfem_pa *pa, const tfem_restriction *r)
               "restriction needs a Cartesian geometry and vice versa)");
 }
 
-// FMA numerics on an ordered space with junction tables: patch-side DOFs are
-// summed by the element kernel itself (apply2d_tma.cu junction_finalize).
-bool junction_mode(const tfem_ctx *ctx, const KernelPick &k, const tfem_pa *pa,
-                   const tfem_restriction *r)
-{
-   return tiled(k, r) && r->has_junctions && pa->dim == 2 && pa->p <= 3 &&
-          ctx->numerics == TFEM_NUMERICS_FMA;
-}
-
 void pa_apply_grids(const tfem_pa *pa, const tfem_restriction *r, int64_t *g_elem,
                     int64_t *g_scatter)
 {
    const KernelPick k = pick(pa->ctx, pa);
    *g_elem = elem_blocks(pa->ctx, k, pa->npos);
-   *g_scatter = junction_mode(pa->ctx, k, pa, r) ? 0 : scatter_grid(r, tiled(k, r));
+   *g_scatter = scatter_grid(r, tiled(k, r));
 }
 
 void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const double *x,
@@ -357,13 +348,9 @@ void pa_apply(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, const
    a.energy_dot = edot ? 1 : 0;
    a.dot = f.dot;
    a.done = f.done;
-   const bool junc = junction_mode(ctx, k, pa, r);
-   a.junction = junc ? 1 : 0;
-   a.junc = r->junc;
    k.launch(a, ctx->stream, elem_blocks(ctx, k, pa->npos));
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
-   if (junc) return; // the element kernel summed the patch junctions
    if (r->n_shared > 0)
       scatter_shared(ctx, r, a.evec, x, y, f.overwrite, f.ess_out,
                      f.dot_scatter ? &f.dot_scatter : nullptr, f.done, exact, f.notown, tl, edot);

@@ -218,92 +218,6 @@ __device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const dou
    }
 }
 
-// Patch junctions (FMA numerics, tfem_restriction::Junctions): a warp that
-// has written its side partials arrives at its 4 sides and 4 corners; the
-// last patch to arrive at a junction sums the partials in a fixed order
-// (lower patch / left patch first) and writes y.  Deterministic, no E-vector
-// and no scatter launch; the partials are read from L2 (ld.global.cg).
-template <int P, bool EDOT>
-__device__ __forceinline__ void junction_finalize(const ApplyArgs &a, int64_t t, int lane,
-                                                  double &dot)
-{
-   const tfem_restriction::Junctions &J = a.junc;
-   const int64_t PX = J.px, PY = J.py;
-   constexpr int SX = 8 * P, SY = 4 * P;
-   constexpr int kBot = 0, kTop = SX + 1, kLeft = 2 * (SX + 1), kRight = 2 * (SX + 1) + SY + 1;
-   const int64_t nV = (PX + 1) * PY, nH = PX * (PY + 1);
-   const int64_t px = t % PX, py = t / PX;
-   // side partials of this patch are in memory before the arrivals
-   __threadfence();
-   __syncwarp();
-   int expct = 0;
-   unsigned *cnt = nullptr;
-   if (lane < 2) { // left / right V
-      const int64_t j = py * (PX + 1) + px + lane;
-      expct = J.v_exp[j];
-      cnt = J.cnt + j;
-   } else if (lane < 4) { // bottom / top H
-      const int64_t j = (py + lane - 2) * PX + px;
-      expct = J.h_exp[j];
-      cnt = J.cnt + nV + j;
-   } else if (lane < 8) { // corners (px, py), (px+1, py), (px, py+1), (px+1, py+1)
-      const int k = lane - 4;
-      const int64_t j = (py + k / 2) * (PX + 1) + px + k % 2;
-      expct = J.c_exp[j];
-      cnt = J.cnt + nV + nH + j;
-   }
-   bool last = false;
-   if (expct > 0) {
-      last = atomicAdd(cnt, 1u) == static_cast<unsigned>(expct - 1);
-      if (last) *cnt = 0u; // re-armed for the next launch
-   }
-   const unsigned todo = __ballot_sync(0xffffffffu, last);
-   if (!todo) return;
-   __threadfence();
-   auto side = [&](int64_t qx, int64_t qy, int idx) -> double {
-      return (qx >= 0 && qx < PX && qy >= 0 && qy < PY) ? __ldcg(J.side + (qy * PX + qx) * J.jside + idx)
-                                                          : 0.0;
-   };
-   auto finish = [&](int32_t d, double s) {
-      double v = a.overwrite ? s : a.y[d] + s;
-      const bool es = a.ess_out && bit_set(a.ess_out, static_cast<uint32_t>(d));
-      if (es) v = __ldg(a.x + d);
-      a.y[d] = v;
-      if (EDOT) {
-         if (es) dot = fma(v, v, dot);
-      } else if (a.dot && !(a.notown && bit_set(a.notown, static_cast<uint32_t>(d)))) {
-         dot = fma(__ldg(a.x + d), v, dot);
-      }
-   };
-   for (unsigned m = todo; m; m &= m - 1) {
-      const int k = __ffs(m) - 1; // warp-uniform
-      if (k < 2) {
-         const int64_t cx = px + k, j = py * (PX + 1) + cx;
-         if (lane < SY - 1) {
-            const int32_t d = J.v_dof[j * (SY - 1) + lane];
-            const int Y = lane + 1;
-            if (d >= 0) finish(d, side(cx - 1, py, kRight + Y) + side(cx, py, kLeft + Y));
-         }
-      } else if (k < 4) {
-         const int64_t cy = py + k - 2, j = cy * PX + px;
-         if (lane < SX - 1) {
-            const int32_t d = J.h_dof[j * (SX - 1) + lane];
-            const int X = lane + 1;
-            if (d >= 0) finish(d, side(px, cy - 1, kTop + X) + side(px, cy, kBot + X));
-         }
-      } else {
-         const int c = k - 4;
-         const int64_t cx = px + c % 2, cy = py + c / 2, j = cy * (PX + 1) + cx;
-         if (lane == 0) {
-            const int32_t d = J.c_dof[j];
-            if (d >= 0)
-               finish(d, ((side(cx - 1, cy - 1, kTop + SX) + side(cx, cy - 1, kTop)) +
-                          side(cx - 1, cy, kBot + SX)) + side(cx, cy, kBot));
-         }
-      }
-   }
-}
-
 // EDOT: x . y as the sum of element energies (a.energy_dot; apply.cu).
 template <int P, int Q, int KIND, bool EXACT, bool EDOT>
 __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs a)
@@ -565,39 +479,11 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
                a.y[d] = r;
             } else if (fl == kWarpMember && a.warp_local) {
                // summed by the owner lane
-            } else if (!EXACT && a.junction) {
-               // a patch-side DOF (junction): the slot that no later element
-               // of the patch shares writes the patch's partial -- its lower
-               // in-patch neighbours' slots plus its own, as a warp-local owner
-               constexpr int SX = 8 * P, SY = 4 * P;
-               const int X = pc * p + ia, Y = pr * p + ib;
-               const bool owner = !(ia == p && pc < 7) && !(ib == p && pr < 3);
-               if (owner && (X == 0 || X == SX || Y == 0 || Y == SY)) {
-                  double acc = 0.0;
-                  if (ia == 0 && ib == 0) {
-                     if (pc >= 1 && pr >= 1) acc += u9;
-                     if (pr >= 1) acc += u8a;
-                     if (pc >= 1) acc += u1a;
-                  } else if (ia == 0 && ib == p) {
-                     if (pc >= 1) acc += u1b;
-                  } else if (ia == p && ib == 0) {
-                     if (pr >= 1) acc += u8b;
-                  } else if (ia == 0) {
-                     if (pc >= 1) acc += u1m[ib > 0 ? ib - 1 : 0];
-                  } else if (ib == 0) {
-                     if (pr >= 1) acc += u8m[ia > 0 ? ia - 1 : 0];
-                  }
-                  acc += r;
-                  const int idx = Y == 0 ? X : Y == SY ? SX + 1 + X
-                                : X == 0 ? 2 * (SX + 1) + Y : 2 * (SX + 1) + SY + 1 + Y;
-                  a.junc.side[(e >> 5) * a.junc.jside + idx] = acc;
-               }
             } else {
                a.evec[i * a.ne_pad + e] = r;
             }
          }
       }
-      if (!EXACT && a.junction && live) junction_finalize<P, EDOT>(a, e >> 5, lane, dot);
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.gempty[gb]); // map buffer free again
    }

@@ -233,24 +233,6 @@ struct tfem_restriction {
    int n_gbuckets = 0;
    Bucket gbuckets[kMaxBuckets];
    int64_t n_gshared = 0;
-   // Patch junctions (ordered 2D spaces, FMA numerics): the DOFs on the
-   // sides between warp patches, summed without the E-vector / scatter.
-   // Each warp writes one partial per side DOF (its own slots summed
-   // in-warp) to `side` ([patch][jside] doubles); the last of a junction's
-   // patches to arrive (counter) adds the partials in a fixed order and
-   // writes y.  Junctions: V (vertical side between patch columns cx-1, cx
-   // of patch row py; points Y = 1..4p-1), H (horizontal side between patch
-   // rows cy-1, cy of patch column px; points X = 1..8p-1) and corners
-   // (cx, cy).  Tables hold the DOF of every point (-1: none / not shared
-   // between patches) and the number of patches that arrive (0: inactive).
-   struct Junctions {
-      int px = 0, py = 0, jside = 0;
-      int32_t *v_dof = nullptr, *h_dof = nullptr, *c_dof = nullptr;
-      uint8_t *v_exp = nullptr, *h_exp = nullptr, *c_exp = nullptr;
-      unsigned *cnt = nullptr; // V, then H, then corner counters (zero between launches)
-      double *side = nullptr;
-   } junc;
-   bool has_junctions = false;
    // E-vector scratch (lazy) in the map's layout: slot-major [i][ne_pad],
    // element-major [e][nd] with the element's slots in evperm order (ev_em_p)
    double *evec = nullptr;

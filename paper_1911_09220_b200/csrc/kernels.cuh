@@ -32,8 +32,6 @@ struct ApplyArgs {
                     // scatter then adds only its essential DOFs' x^2)
    DotSink dot;     // fused x . y partials (CG's p . q)
    const int *done; // CG stop flag: skip the work once the solve has ended
-   int junction;    // patch-side DOFs through tfem_restriction::junc (no scatter)
-   tfem_restriction::Junctions junc;
 };
 
 using Launch = void (*)(const ApplyArgs &, cudaStream_t, unsigned);

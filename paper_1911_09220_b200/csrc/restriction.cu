@@ -432,118 +432,6 @@ int warp_partners(int p, int a, int b, int c, int r, Partner *out)
    return n;
 }
 
-// The patch junctions of tfem_restriction::junc from the global buckets
-// (every shared DOF whose slots span several patches).  A DOF's point comes
-// from any of its slots (patch, lane cell, local (a, b)); it lies on a
-// vertical and/or horizontal patch line.  A DOF whose slots do not all lie in
-// the patches its junction expects leaves junctions off (scatter path).
-void build_junctions(tfem_restriction *r, const Layout &L, const std::vector<int32_t> *gd,
-                     const std::vector<uint32_t> *gs)
-{
-   const int p = r->p, D1 = p + 1;
-   const int64_t PX = r->order.px, PY = r->order.py;
-   const int SX = 8 * p, SY = 4 * p; // patch side lengths in lattice intervals
-   tfem_restriction::Junctions &J = r->junc;
-   J.px = static_cast<int>(PX);
-   J.py = static_cast<int>(PY);
-   J.jside = ((2 * (SX + 1) + 2 * (SY + 1)) + 7) / 8 * 8;
-   const int64_t nV = (PX + 1) * PY, nH = PX * (PY + 1), nC = (PX + 1) * (PY + 1);
-   std::vector<int32_t> vd(static_cast<size_t>(nV) * (SY - 1), -1), hd(static_cast<size_t>(nH) * (SX - 1), -1),
-      cd(static_cast<size_t>(nC), -1);
-   auto exists = [&](int64_t px, int64_t py) { return px >= 0 && px < PX && py >= 0 && py < PY; };
-   auto patch_of = [&](uint32_t slot, int64_t &gx, int64_t &gy) {
-      const int64_t pos = L.elem_of(slot);
-      const int i = L.local_of(slot);
-      const int64_t t = pos / 32;
-      const int lane = static_cast<int>(pos % 32);
-      gx = (t % PX) * SX + (lane % 8) * p + i % D1;
-      gy = (t / PX) * SY + (lane / 8) * p + i / D1;
-      return t;
-   };
-   for (int b = 0; b < tfem_restriction::kMaxBuckets; b++) {
-      const int c = r->buckets[b].c;
-      for (size_t k = 0; k < gd[b].size(); k++) {
-         const uint32_t *row = &gs[b][k * c];
-         int64_t gx, gy;
-         patch_of(row[0], gx, gy);
-         const bool onv = gx % SX == 0, onh = gy % SY == 0;
-         // the patches the junction sums (all of the DOF's slots must be there)
-         int64_t want[4];
-         int nw = 0;
-         int32_t *dst = nullptr;
-         if (onv && onh) {
-            const int64_t cx = gx / SX, cy = gy / SY;
-            for (int64_t qy = cy - 1; qy <= cy; qy++)
-               for (int64_t qx = cx - 1; qx <= cx; qx++)
-                  if (exists(qx, qy)) want[nw++] = qy * PX + qx;
-            dst = &cd[cy * (PX + 1) + cx];
-         } else if (onv) {
-            const int64_t cx = gx / SX, py = gy / SY;
-            for (int64_t qx = cx - 1; qx <= cx; qx++)
-               if (exists(qx, py)) want[nw++] = py * PX + qx;
-            dst = &vd[(py * (PX + 1) + cx) * (SY - 1) + gy % SY - 1];
-         } else if (onh) {
-            const int64_t cy = gy / SY, px = gx / SX;
-            for (int64_t qy = cy - 1; qy <= cy; qy++)
-               if (exists(px, qy)) want[nw++] = qy * PX + px;
-            dst = &hd[(cy * PX + px) * (SX - 1) + gx % SX - 1];
-         } else {
-            return; // not on a patch line: keep the scatter
-         }
-         for (int j = 0; j < c; j++) {
-            int64_t x, y;
-            const int64_t t = patch_of(row[j], x, y);
-            bool ok = x == gx && y == gy;
-            bool in = false;
-            for (int w = 0; w < nw; w++) in |= want[w] == t;
-            if (!ok || !in) return;
-         }
-         *dst = gd[b][k];
-      }
-   }
-   std::vector<uint8_t> ve(static_cast<size_t>(nV), 0), he(static_cast<size_t>(nH), 0), ce(static_cast<size_t>(nC), 0);
-   for (int64_t j = 0; j < nV; j++) {
-      bool any = false;
-      for (int k = 0; k < SY - 1; k++) any |= vd[j * (SY - 1) + k] >= 0;
-      const int64_t cx = j % (PX + 1), py = j / (PX + 1);
-      if (any) ve[j] = static_cast<uint8_t>(exists(cx - 1, py) + exists(cx, py));
-   }
-   for (int64_t j = 0; j < nH; j++) {
-      bool any = false;
-      for (int k = 0; k < SX - 1; k++) any |= hd[j * (SX - 1) + k] >= 0;
-      const int64_t px = j % PX, cy = j / PX;
-      if (any) he[j] = static_cast<uint8_t>(exists(px, cy - 1) + exists(px, cy));
-   }
-   for (int64_t j = 0; j < nC; j++) {
-      const int64_t cx = j % (PX + 1), cy = j / (PX + 1);
-      if (cd[j] >= 0)
-         ce[j] = static_cast<uint8_t>(exists(cx - 1, cy - 1) + exists(cx, cy - 1) +
-                                      exists(cx - 1, cy) + exists(cx, cy));
-   }
-   cudaStream_t st = r->ctx->stream;
-   auto up32 = [&](const std::vector<int32_t> &v) {
-      int32_t *d = dalloc<int32_t>(static_cast<int64_t>(v.size()));
-      h2d(st, d, v.data(), sizeof(int32_t) * v.size());
-      return d;
-   };
-   auto up8 = [&](const std::vector<uint8_t> &v) {
-      uint8_t *d = dalloc<uint8_t>(static_cast<int64_t>(v.size()));
-      h2d(st, d, v.data(), v.size());
-      return d;
-   };
-   J.v_dof = up32(vd);
-   J.h_dof = up32(hd);
-   J.c_dof = up32(cd);
-   J.v_exp = up8(ve);
-   J.h_exp = up8(he);
-   J.c_exp = up8(ce);
-   J.cnt = dalloc<unsigned>(nV + nH + nC);
-   TFEM_CUDA(cudaMemsetAsync(J.cnt, 0, sizeof(unsigned) * (nV + nH + nC), st));
-   J.side = dalloc<double>(PX * PY * J.jside);
-   TFEM_CUDA(cudaStreamSynchronize(st));
-   r->has_junctions = true;
-}
-
 void build_warp_local(tfem_restriction *r, const Layout &L)
 {
    cudaStream_t s = r->ctx->stream;
@@ -586,7 +474,6 @@ void build_warp_local(tfem_restriction *r, const Layout &L)
       }
    }
    h2d(s, r->gmap, gmap.data(), sizeof(uint32_t) * gmap.size());
-   build_junctions(r, L, gd, gs);
    for (int b = 0; b < r->n_buckets; b++) {
       if (gd[b].empty()) continue;
       auto &g = r->gbuckets[r->n_gbuckets++];
@@ -807,14 +694,6 @@ tfem_restriction *restriction_create(tfem_ctx *ctx, int dim, int p, int64_t ne, 
 void restriction_destroy(tfem_restriction *r)
 {
    if (!r) return;
-   {
-      auto &J = r->junc;
-      for (void *q : {static_cast<void *>(J.v_dof), static_cast<void *>(J.h_dof),
-                      static_cast<void *>(J.c_dof), static_cast<void *>(J.v_exp),
-                      static_cast<void *>(J.h_exp), static_cast<void *>(J.c_exp),
-                      static_cast<void *>(J.cnt), static_cast<void *>(J.side)})
-         cudaFree(q);
-   }
    cudaFree(r->gmap);
    cudaFree(r->evperm);
    for (int b = 0; b < r->n_buckets; b++) {
