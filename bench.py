@@ -64,6 +64,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-bitexact", action="store_true", help="skip the reference-numerics line")
+    ap.add_argument("--strong", action="store_true",
+                    help="N > 1: partition one n^dim mesh over the ranks (default: weak scaling, "
+                         "~10M DOFs per rank)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the extra configurations (3D BP3 p=3 ~10M, 2D BP3 p=3 ~100M DOFs)")
     return ap.parse_args()
 
 
@@ -270,6 +275,59 @@ def config_of(args, n, p, ndofs, per_step_iters=None, world=1):
 
 
 # ---------------------------------------------------------------- our arm
+def measure_config(tf, dev, dim, p, bp, n, iters, steps, warmup=1):
+    """One more workload on the same device, device-resident, CUDA events:
+    GDOF/s, the CG and the operator roofline fractions (tfem_cg_profile), and
+    the true-residual check.  Used for the extra keys of the bench line."""
+    import torch
+    cells = (n,) * dim
+    sp = tf.FeSpace.cartesian(dev, cells, p)
+    a = tf.BilinearForm(sp)
+    if bp == 1:
+        a.add_mass(1.0)
+    elif bp == 5:
+        a.add_diffusion(1.0, rule="gauss_lobatto", nq=p + 1)
+    else:
+        a.add_diffusion(1.0)
+    a.assemble()
+    ess = sp.essential_true_dofs()
+    op = tf.ConstrainedOperator(a, ess)
+    diag = op.diagonal()
+    pc = None if bp == 1 else diag
+    N, E = sp.n_dofs, sp.n_elements
+    b_host = np.random.default_rng(2020).uniform(-1.0, 1.0, N)
+    b_host[ess] = 0.0
+    b = tf.Vector.from_numpy(dev, b_host)
+    x = tf.Vector(dev, N)
+    for _ in range(warmup):
+        res = tf.cg_solve(op, b, 0.0, iters, pc, x=x)
+    stream = torch.cuda.ExternalStream(dev.stream)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dev.sync()
+    ev0.record(stream)
+    for _ in range(steps):
+        res = tf.cg_solve(op, b, 0.0, iters, pc, x=x)
+    ev1.record(stream)
+    ev1.synchronize()
+    t = ev0.elapsed_time(ev1) / 1e3
+    chk = result_check(tf, dev, op, b_host, res, iters)
+    nc = 1 if bp == 1 else (3 if dim == 2 else 6)
+    nq = p + 1 if bp == 5 else p + 2
+    b_op = E * (nc * nq ** dim * 8 + (p + 1) ** dim * 4) + 16 * N
+    b_it = b_op + (80 if bp == 1 else 96) * N
+    seg = (C.c_double * 3)()
+    xp = tf.Vector(dev, N)
+    tf.abi.check(tf.lib().tfem_cg_profile(dev.h, op.h, b.h, min(iters, 100),
+                                          pc.h if pc is not None else None, xp.h, seg))
+    peak, _ = peaks()
+    value = N * iters * steps / t / 1e9
+    return {"workload": f"BP{bp} {dim}D p={p} n={n}^{dim}", "dofs": N, "value": value,
+            "unit": "GDOF/s", "ms_per_step": 1e3 * t / steps, "iterations_per_step": iters,
+            "steps": steps, "cg_frac": b_it * iters * steps / t / 1e9 / peak,
+            "operator_frac": b_op / (seg[0] * 1e-6) / 1e9 / peak, "operator_us": seg[0],
+            "result_check_drift": chk["drift"]}
+
+
 def result_check(tf, dev, op, b_host, res, iters):
     """After the timed region: the last solve's x against its own claim.
     The true residual ||b - A x|| (one more device operator application,
@@ -466,6 +524,18 @@ def run_tfem(args):
         except Exception:
             dropin = {"error": (out.stdout + out.stderr)[-500:]}
 
+    # ---- extra configurations the north star names (same device, after the
+    # headline legs): 3D BP3 p=3 at ~10M DOFs and 2D BP3 p=3 at ~100M DOFs
+    extra = None
+    if not args.no_extra and args.dim == 2 and args.bp == 3 and args.order == 3 and not args.cells:
+        extra = {}
+        for key, (dim, nn, steps) in {"3d_bp3_p3_10M": (3, 72, 5),
+                                      "2d_bp3_p3_100M": (2, 3334, 3)}.items():
+            try:
+                extra[key] = measure_config(tf, dev, dim, 3, 3, nn, args.iters, steps)
+            except Exception as e:  # reported, never required
+                extra[key] = {"error": str(e)[:300]}
+
     cpu = None
     if not args.no_cpu_baseline and args.dim == 2:
         try:
@@ -493,6 +563,7 @@ def run_tfem(args):
                         "bytes_per_dof_iteration": b_it / N, "kernels": cg_kernels},
         "e2e": e2e, "e2e_dropin": dropin, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
         "bit_exact_numerics": exact, "setup_s": setup_s, "result_check": check,
+        "extra_configs": extra,
     }
     print(json.dumps(line))
 

@@ -6,7 +6,8 @@
 // doctest's semantics, so the suites compile and run unchanged against the
 // TENSORFEM_B200 build:
 //   TEST_CASE, SUBCASE (each run of a test case enters one new leaf
-//   subcase; the case re-runs until every subcase has run), CHECK,
+//   subcase; the case re-runs until every subcase has run, once per leaf as
+//   doctest does), CHECK,
 //   CHECK_FALSE, CHECK_NOTHROW, CHECK_THROWS_AS, REQUIRE, REQUIRE_FALSE,
 //   FAIL, doctest::Approx (epsilon / scale, doctest's comparison rule),
 //   DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN.
@@ -138,9 +139,8 @@ struct State {
    // subcase traversal of the running test case
    std::set<std::vector<std::string>> done;
    std::vector<std::string> stack;
-   std::vector<bool> entered; // a subcase was entered at this depth in this run
-   std::vector<bool> had_child;
-   bool any_entered = false;
+   std::vector<bool> entered;  // a subcase was entered at this depth in this run
+   std::vector<bool> all_done; // per open scope (root first): every child seen is done
    long checks = 0, failed_checks = 0;
    bool case_failed = false;
    const char *current = "";
@@ -179,28 +179,28 @@ public:
    {
       State &s = state();
       const size_t depth = s.stack.size();
-      if (s.entered.size() <= depth) {
-         s.entered.resize(depth + 1, false);
-         s.had_child.resize(depth + 1, false);
-      }
       std::vector<std::string> path = s.stack;
       path.emplace_back(name);
-      if (s.entered[depth] || s.done.count(path)) return;
+      if (s.done.count(path)) return;   // ran completely in an earlier run
+      if (s.entered[depth]) {           // a sibling runs this time: this one later
+         s.all_done[depth] = false;
+         return;
+      }
       s.entered[depth] = true;
-      if (depth > 0) s.had_child[depth - 1] = true;
-      s.had_child[depth] = false;
       s.stack = path;
-      s.any_entered = true;
+      if (s.entered.size() < depth + 2) s.entered.resize(depth + 2, false);
+      s.entered[depth + 1] = false;
+      s.all_done.push_back(true);
       active_ = true;
    }
    ~Subcase()
    {
       if (!active_) return;
       State &s = state();
-      const size_t depth = s.stack.size() - 1;
-      // a subcase with no new child entered in this run has run completely
-      if (depth + 1 >= s.entered.size() || !s.had_child[depth]) s.done.insert(s.stack);
-      if (depth + 1 < s.entered.size()) s.entered[depth + 1] = false;
+      const bool mine = s.all_done.back();
+      s.all_done.pop_back();
+      if (mine) s.done.insert(s.stack); // no child left: this subcase is complete
+      else s.all_done.back() = false;
       s.stack.pop_back();
    }
    explicit operator bool() const { return active_; }
@@ -220,8 +220,7 @@ inline int run_all()
       for (;;) {
          s.stack.clear();
          s.entered.assign(1, false);
-         s.had_child.assign(1, false);
-         s.any_entered = false;
+         s.all_done.assign(1, true);
          try {
             tc.fn();
          } catch (const RequireFailed &) {
@@ -235,7 +234,9 @@ inline int run_all()
                       << "\": unexpected unknown exception\n";
             s.case_failed = true;
          }
-         if (!s.any_entered || s.case_failed) break;
+         // doctest's traversal: re-run while a subcase seen in this run is
+         // still to be entered (one new leaf per run)
+         if (s.all_done[0] || s.case_failed) break;
       }
       if (s.case_failed) failed_cases++;
    }

@@ -146,9 +146,14 @@ __global__ void apply2d_grp_kernel(const ApplyArgs a)
 template <int P, int Q>
 struct Smem3D {
    static constexpr int D1 = P + 1;
-   double V[D1 * D1 * D1];                    // [c][b][a]
    double TB[D1 * D1 * Q], TG[D1 * D1 * Q];   // [c][b][qx]
-   double Px[D1 * Q * Q], Py[D1 * Q * Q], Pz[D1 * Q * Q]; // [c][qy][qx]
+   // V is dead once TB / TG are formed, before the column stage writes the
+   // P planes: they share storage (a smaller per-element footprint fits
+   // more elements per SM at q >= 8)
+   union {
+      double V[D1 * D1 * D1];                                // [c][b][a]
+      struct { double Px[D1 * Q * Q], Py[D1 * Q * Q], Pz[D1 * Q * Q]; }; // [c][qy][qx]
+   };
 };
 
 template <int P, int Q, int KIND>

@@ -294,7 +294,11 @@ def bench_distributed(args, rank: int, world: int, local: int):
     dev = tf.Device(local, numerics=args.numerics)
     n = args.cells or {2: round((10.0e6 ** 0.5 - 1) / args.order),
                    3: round((10.0e6 ** (1 / 3) - 1) / args.order)}[args.dim]
-    n_global = (n,) * (args.dim - 1) + (n * world,)
+    # weak (default): ~10M DOFs per rank, the last axis grows with the ranks;
+    # strong (--strong): one fixed global mesh n^dim cut into `world` slabs
+    # (C2 at 10M, or C5's 333^3 ~ 1B DOFs in 3D)
+    strong = getattr(args, "strong", False)
+    n_global = (n,) * args.dim if strong else (n,) * (args.dim - 1) + (n * world,)
     slab = partition(args.dim, n_global, args.order, rank, world)
     t0 = time.perf_counter()
     d = DistOperator(dev, slab)
@@ -364,7 +368,8 @@ def bench_distributed(args, rank: int, world: int, local: int):
             "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": config_of(args, n, args.order, N_global // world, world=world),
             # the distributed run times the whole CG iteration (no per-kernel
             # split): algorithmic bytes of an iteration per GPU / its time

@@ -53,14 +53,24 @@ METRICS = [
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
     ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
      "long-scoreboard stall/issue"),
+    ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "wait stall/issue"),
+    ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+     "short-scoreboard stall/issue"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("smsp__warps_eligible.avg.per_cycle_active", "eligible warps/scheduler"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
 ]
 
 
 def full(path, tag):
-    raw = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    """path: an .ncu-rep, or the `--page raw --csv` export of one."""
+    if str(path).endswith(".csv"):
+        raw = Path(path).read_text()
+    else:
+        raw = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"],
+                             capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out = [f"# {tag}: ncu --set full summary", "", f"source: `{Path(path).name}`", ""]
