@@ -166,7 +166,7 @@ BucketArgs bucket_args(const tfem_restriction *r, bool global_only)
 // are warp-uniform constant-bank loads.
 template <int DIM>
 __global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne, int64_t ne_pad,
-                            const double *__restrict__ qdata, const uint32_t *gmap,
+                            const double *__restrict__ qdata, int qlayout, const uint32_t *gmap,
                             int elem_major, const uint16_t *evperm, double *evec, double *y)
 {
    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; // position
@@ -179,8 +179,7 @@ __global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne,
    const int ia = i % D1, ib = (i / D1) % D1, ic = i / (D1 * D1);
    // qdata addressing follows the map layout (elem_major_layout)
    auto D = [&](int c, int q) -> double {
-      return elem_major ? __ldg(qdata + (e * ncomp + c) * (int64_t)nqd + q)
-                        : __ldg(qdata + (int64_t)(c * nqd + q) * ne_pad + e);
+      return __ldg(qdata + qdata_index(qlayout, e, c, q, ncomp, nqd, nq, ne_pad));
    };
    double s = 0.0;
    for (int q = 0; q < nqd; q++) {
@@ -366,10 +365,10 @@ void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, do
    const int elem_major = pa->elem_major() ? 1 : 0;
    if (pa->dim == 2)
       diag_kernel<2><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->npos, pa->ne_pad,
-                                                 pa->qdata, r->gmap, elem_major, r->evperm, evec, diag);
+                                                 pa->qdata, pa->qlayout, r->gmap, elem_major, r->evperm, evec, diag);
    else
       diag_kernel<3><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->npos, pa->ne_pad,
-                                                 pa->qdata, r->gmap, elem_major, r->evperm, evec, diag);
+                                                 pa->qdata, pa->qlayout, r->gmap, elem_major, r->evperm, evec, diag);
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
    if (r->n_shared > 0)

@@ -715,9 +715,8 @@ int tfem_pa_qdata(const tfem_pa *pa, double *host)
          const int64_t pos = pa->order.pos_of(e);
          for (int q = 0; q < pa->nqd; q++)
             for (int c = 0; c < pa->ncomp; c++) {
-               const double v = pa->elem_major()
-                                   ? dev[(pos * pa->ncomp + c) * pa->nqd + q]
-                                   : dev[(static_cast<int64_t>(c) * pa->nqd + q) * pa->ne_pad + pos];
+               const double v = dev[qdata_index(pa->qlayout, pos, c, q, pa->ncomp, pa->nqd,
+                                                pa->nq, pa->ne_pad)];
                host[(e * pa->nqd + q) * pa->ncomp + c] = v;
             }
       }

@@ -146,6 +146,25 @@ inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 // element per thread group: element-major map [e][nd] and qdata [e][c][q].
 inline bool elem_major_layout(int dim, int p) { return dim == 3 || p >= 4; }
 
+// qdata layouts: 0 planes [(c*nqd + q)][ne_pad] (element fastest); 1
+// element-major [e][c][q].  (A slab-major [e][qz][c][q2] layout streamed one
+// qz plane at a time was measured for 3D q = 6, 7: slower at BP3 p = 4, 5
+// -- the column stage's second lane pass re-waits on every slab -- and
+// removed.)
+inline int qdata_layout(int dim, int p, int nq, int kind)
+{
+   (void)nq;
+   (void)kind;
+   return elem_major_layout(dim, p) ? 1 : 0;
+}
+__host__ __device__ inline int64_t qdata_index(int layout, int64_t pos, int c, int q, int ncomp,
+                                               int nqd, int nq, int64_t ne_pad)
+{
+   (void)nq;
+   if (layout == 0) return (int64_t)(c * nqd + q) * ne_pad + pos;
+   return (pos * ncomp + c) * (int64_t)nqd + q;
+}
+
 // Scratch for block partials of fused dot products and the last-block
 // ticket.  One per context; every reduction uses a fixed grid so the result
 // is deterministic run to run.
@@ -263,6 +282,7 @@ struct tfem_pa {
    int64_t ne = 0, npos = 0, ne_pad = 0; // npos: element positions (order.n_pos)
    // elem_major_layout(dim, p) ? [e][c][q] : planes [(c * nqd + q)][ne_pad]
    double *qdata = nullptr;
+   int qlayout = 0;       // tfem::qdata_layout(dim, p, nq, kind)
    tfem::ElemOrder order; // element positions of qdata (== the restriction's)
    bool elem_major() const { return tfem::elem_major_layout(dim, p); }
    std::vector<double> B, G; // nq x (p+1)

@@ -115,7 +115,7 @@ __global__ void check_kernel(GeoSource g, GeoTables t, unsigned long long *err)
 
 template <int DIM>
 __global__ void setup_kernel(GeoSource g, GeoTables t, int kind, const double *coeff,
-                             double coeff_const, int64_t ne_pad, int emaj, ElemOrder order,
+                             double coeff_const, int64_t ne_pad, int layout, ElemOrder order,
                              double *qdata, unsigned long long *err)
 {
    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -124,14 +124,14 @@ __global__ void setup_kernel(GeoSource g, GeoTables t, int kind, const double *c
    // Planes [(c*nqd+q)][ne_pad]: element fastest; element-major [e][c][q]:
    // point fastest.  Either way the stores are coalesced.
    // e: reference element number; pos: its position in the device order
+   const bool emaj = layout != 0;
    const int q = static_cast<int>(emaj ? idx % nqd : idx / g.ne);
    const int64_t e = emaj ? idx / nqd : idx % g.ne;
    const int64_t pos = order.pos_of(e);
    const int qx = q % nq, qy = (q / nq) % nq, qz = q / (nq * nq);
    const int ncomp = kind == TFEM_MASS ? 1 : (DIM == 2 ? 3 : 6);
    auto out = [&](int c) -> double & {
-      return emaj ? qdata[(pos * ncomp + c) * (int64_t)nqd + q]
-                  : qdata[(int64_t)(c * nqd + q) * ne_pad + pos];
+      return qdata[qdata_index(layout, pos, c, q, ncomp, nqd, nq, ne_pad)];
    };
    double J[3][3];
    jacobian<DIM>(g, t, e, qx, qy, qz, J);
@@ -329,6 +329,7 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
    pa->B.resize(static_cast<size_t>(nq) * (p + 1));
    pa->G.resize(pa->B.size());
    eval_matrices(p, TFEM_NODES_GAUSS_LOBATTO, nq, rule, pa->B.data(), pa->G.data());
+   pa->qlayout = qdata_layout(dim, p, nq, kind);
    pa->colloc = nq == p + 1;
    for (int q = 0; q < nq && pa->colloc; q++)
       for (int i = 0; i <= p; i++)
@@ -362,12 +363,11 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
    if (dim == 2) {
       check_kernel<2><<<blocks_for(ncd * g->ne, T), T, 0, ctx->stream>>>(src, tc, d_err);
       setup_kernel<2><<<blocks_for(nqd * g->ne, T), T, 0, ctx->stream>>>(
-         src, tq, kind, d_coeff, coeff_const, pa->ne_pad, pa->elem_major() ? 1 : 0, pa->order,
-         pa->qdata, d_err);
+         src, tq, kind, d_coeff, coeff_const, pa->ne_pad, pa->qlayout, pa->order, pa->qdata, d_err);
    } else {
       check_kernel<3><<<blocks_for(ncd * g->ne, T), T, 0, ctx->stream>>>(src, tc, d_err);
       setup_kernel<3><<<blocks_for(nqd * g->ne, T), T, 0, ctx->stream>>>(
-         src, tq, kind, d_coeff, coeff_const, pa->ne_pad, 1, pa->order, pa->qdata, d_err);
+         src, tq, kind, d_coeff, coeff_const, pa->ne_pad, pa->qlayout, pa->order, pa->qdata, d_err);
    }
    ctx->launched(2);
    TFEM_CUDA(cudaGetLastError());
