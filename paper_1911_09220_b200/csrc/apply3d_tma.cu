@@ -63,17 +63,26 @@ struct alignas(16) Warp3 {
 
 template <int P, int Q, int KIND>
 struct Cfg3 {
+   // warps per element: two when neither the (p+1)^2 rows nor the q^2
+   // columns fit one warp (p = 5, q = 6, 7): every stage is then one pass of
+   // 64 threads, and a team's shared memory -- dominated by the element's
+   // double-buffered point factors -- feeds twice the warps.  Measured (10M
+   // DOFs): BP3 p=5 +17 %, BP5 p=5 +64 %; at p = 4, q = 6 (25 rows) one
+   // warp per element stays faster (-7 % with teams: idle threads).
+   static constexpr int WPE = (P + 1) * (P + 1) > 32 && Q * Q > 32 ? 2 : 1;
    static constexpr size_t kWarpBytes = sizeof(Warp3<P, Q, KIND>);
    // computing warps as shared memory allows: 224 KB (vs 200) is +9 % at
    // p = 4 (6 -> 7 warps), neutral where the 11-warp cap or the warp size binds
-   static constexpr int kW0 = static_cast<int>((224 * 1024) / kWarpBytes);
+   static constexpr int kT0 = static_cast<int>((224 * 1024) / kWarpBytes); // teams by smem
    // warp cap from the registers ptxas needs: 11 (170 each) by default, 15
    // (128) at p <= 2 with q <= p + 2 except p = 2, q = 4, 13 (146) at p = 3, q = 5
    static constexpr int kMaxW = KIND != TFEM_DIFFUSION ? 11
                               : (Q <= 3) ? 15 : (P == 3 && Q == 5) ? 13 : 11;
-   static constexpr int kW = kW0 > kMaxW ? kMaxW : (kW0 < 1 ? 1 : kW0); // compute warps
+   static constexpr int kT1 = kT0 * WPE > kMaxW ? kMaxW / WPE : kT0;
+   static constexpr int kT = kT1 < 1 ? 1 : kT1;   // teams (elements in flight)
+   static constexpr int kW = kT * WPE;            // compute warps
    static constexpr int kBlock = 32 * (kW + 1);
-   static constexpr size_t kSmem = kWarpBytes * kW;
+   static constexpr size_t kSmem = kWarpBytes * kT;
 };
 
 // CO (collocated, BP5): q = p + 1 Gauss-Lobatto points on the Gauss-Lobatto
@@ -86,14 +95,15 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    using W = Warp3<P, Q, KIND>;
    constexpr int D1 = W::D1, ND = W::ND, NQD = W::NQD, NC = W::NC, EPW = W::EPW;
    constexpr int kW = Cfg3<P, Q, KIND>::kW, kBlock = Cfg3<P, Q, KIND>::kBlock;
+   constexpr int kT = Cfg3<P, Q, KIND>::kT, WPE = Cfg3<P, Q, KIND>::WPE;
+   constexpr int NTH = 32 * WPE;              // threads per team
    constexpr int kSlots = W::kSlots;
    constexpr int NT = D1 * D1 * Q;         // contraction outputs per element
    constexpr int kSt = W::kSt, kSp = W::kSp, kEt = W::kEt, kEp = W::kEp;
-   constexpr int GPL = (EPW * ND + 31) / 32; // map entries per lane
-   // row-wise contractions (basis operands compile-time) when a warp covers
-   // the rows in one pass, or two at q <= 6 (BP5 p=5 +7 %); measured slower
-   // at q = 7 (two passes, spills)
-   constexpr int kRowMax = Q <= 6 ? 64 : 32;
+   constexpr int GPL = (EPW * ND + NTH - 1) / NTH; // map entries per thread
+   // row-wise contractions (basis operands compile-time) when a team covers
+   // the rows in one pass (or two at q <= 6 with one warp per element)
+   constexpr int kRowMax = WPE > 1 ? NTH : (Q <= 6 ? 64 : 32);
    constexpr bool kRows1 = EPW * D1 * D1 <= kRowMax; // stages a and x
    constexpr bool kRows3 = EPW * Q * D1 <= kRowMax;  // stage y
    constexpr unsigned kQBytes = NC * NQD * 8;
@@ -107,7 +117,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
    auto *ws = reinterpret_cast<W *>(smem_raw);
    if (threadIdx.x == 0) {
-      for (int w = 0; w < kW; w++)
+      for (int w = 0; w < kT; w++)
          for (int s = 0; s < kSlots; s++) {
             mbar_init(&ws[w].full[s], 1);
             mbar_init(&ws[w].empty[s], 1);
@@ -115,10 +125,16 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
    }
    __syncthreads();
-   // warp w of block b takes element groups g = (b kW + w) + k (grid kW);
+   // team w of block b takes element groups g = (b kT + w) + k (grid kT);
    // group g is elements [g EPW, g EPW + EPW)
-   const int64_t stride = (int64_t)gridDim.x * kW;
-   auto group = [&](int w, int64_t k) { return (int64_t)blockIdx.x * kW + w + k * stride; };
+   const int64_t stride = (int64_t)gridDim.x * kT;
+   auto group = [&](int w, int64_t k) { return (int64_t)blockIdx.x * kT + w + k * stride; };
+   // a team: WPE warps on one element group; pt = thread in the team
+   const int team = warp / WPE, pt = lane + 32 * (warp % WPE);
+   auto team_sync = [&]() {
+      if constexpr (WPE == 1) __syncwarp();
+      else asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(NTH) : "memory");
+   };
    auto count = [&](int64_t g) {
       const int64_t left = a.ne - g * EPW;
       return static_cast<int>(left < EPW ? (left > 0 ? left : 0) : EPW);
@@ -129,7 +145,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
       if (lane == 0) {
          for (int64_t k = 0;; k++) {
             bool any = false;
-            for (int w = 0; w < kW; w++) {
+            for (int w = 0; w < kT; w++) {
                const int64_t g = group(w, k);
                const int cnt = count(g);
                if (cnt == 0) continue;
@@ -147,14 +163,14 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
       __syncwarp();
    } else {
       // ---------------------------------------------------------- consumer
-      W &sm = ws[warp];
+      W &sm = ws[team];
       uint32_t gcur[GPL], gnext[GPL], gnn[GPL]; // map entries: this, next, next-but-one group
       uint32_t mcur[GPL], mnext[GPL]; // mask_in words of the map entries
       auto load_map = [&](int64_t g, uint32_t (&m_)[GPL]) {
          const int64_t lim = (int64_t)count(g) * ND;
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
-            const int i = lane + 32 * m;
+            const int i = pt + NTH * m;
             m_[m] = i < lim ? __ldg(a.gmap + g * EPW * ND + i) : 0u;
          }
       };
@@ -163,7 +179,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          if (lim == 0) return;
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
-            const int i = lane + 32 * m;
+            const int i = pt + NTH * m;
             if (i < lim) gather8(&sm.V[buf][i], a.x + (m_[m] & kDofMask));
          }
          cp_async_commit();
@@ -173,16 +189,16 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          const int64_t lim = (int64_t)count(g) * ND;
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
-            const int i = lane + 32 * m;
+            const int i = pt + NTH * m;
             w_[m] = a.mask_in && i < lim ? __ldg(a.mask_in + ((m_[m] & kDofMask) >> 5)) : 0u;
          }
       };
-      load_map(group(warp, 0), gcur);
-      load_map(group(warp, 1), gnext);
-      prefetch_x(group(warp, 0), gcur, 0);
-      load_mask(group(warp, 0), gcur, mcur);
+      load_map(group(team, 0), gcur);
+      load_map(group(team, 1), gnext);
+      prefetch_x(group(team, 0), gcur, 0);
+      load_mask(group(team, 0), gcur, mcur);
       for (int64_t k = 0;; k++) {
-         const int64_t g = group(warp, k);
+         const int64_t g = group(team, k);
          const int cnt = count(g);
          if (cnt == 0) break;
          const int vb = static_cast<int>(k & 1);
@@ -191,7 +207,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          // essential flags to shared memory for the epilogue
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
-            const int i = lane + 32 * m;
+            const int i = pt + NTH * m;
             if (i >= cnt * ND) continue;
             const uint32_t d = gcur[m] & kDofMask;
             const bool mk = (mcur[m] >> (d & 31)) & 1u;
@@ -199,16 +215,16 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             sm.gm[i] = gcur[m];
             sm.es[i] = (a.ess_out == a.mask_in ? mk : (a.ess_out && bit_set(a.ess_out, d))) ? 1 : 0;
          }
-         __syncwarp();
-         const int64_t gn = group(warp, k + 1);
-         load_map(group(warp, k + 2), gnn); // two groups ahead: used a group later
+         team_sync();
+         const int64_t gn = group(team, k + 1);
+         load_map(group(team, k + 2), gnn); // two groups ahead: used a group later
          const double *V = sm.V[vb];
          // contract a -> TB / TG [e][c][b][qx]: a lane per (e, c, b) row, qx
          // unrolled (basis operands from the constant bank) when the rows
          // fit one pass of the warp; else a lane per output.  CO: TB = V,
          // only TG is formed.
          if constexpr (CO) {
-            for (int it = lane; it < EPW * D1 * D1; it += 32) {
+            for (int it = pt; it < EPW * D1 * D1; it += NTH) {
                const int j = it / (D1 * D1), cb = it % (D1 * D1);
                double v[D1];
 #pragma unroll
@@ -223,7 +239,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                }
             }
          } else if constexpr (!kRows1) {
-            for (int jj = lane; jj < EPW * NT; jj += 32) {
+            for (int jj = pt; jj < EPW * NT; jj += NTH) {
                const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q;
                double sb = 0.0, sg = 0.0;
 #pragma unroll
@@ -236,7 +252,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                sm.TG[j * kEt + cb * kSt + jx] = sg;
             }
          } else
-         for (int it = lane; it < EPW * D1 * D1; it += 32) {
+         for (int it = pt; it < EPW * D1 * D1; it += NTH) {
             const int j = it / (D1 * D1), cb = it % (D1 * D1);
             double v[D1];
 #pragma unroll
@@ -256,11 +272,11 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          }
          prefetch_x(gn, gnext, vb ^ 1); // the other buffer is free
          load_mask(gn, gnext, mnext);
-         __syncwarp();
+         team_sync();
          const int s = static_cast<int>(k % kSlots);
          mbar_wait(&sm.full[s], static_cast<unsigned>((k / kSlots) & 1));
          // column stage: (element ej, qx, qy) columns over the lanes
-         for (int cl = lane; cl < EPW * Q * Q; cl += 32) {
+         for (int cl = pt; cl < EPW * Q * Q; cl += NTH) {
             const int ej = cl / (Q * Q), col = cl % (Q * Q);
             const int qx = col % Q, qy = col / Q;
             const bool live = ej < cnt;
@@ -369,13 +385,13 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                }
             }
          }
-         __syncwarp();
-         if (lane == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
+         team_sync();
+         if (pt == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
          // contract qy -> [e][c][b][qx] (x-gradient part in TB, y + z in TG):
          // a lane per (e, c, qx), b unrolled (or a lane per output).  CO: TB
          // is Px itself (read in place below), TG = G_y Py + Pz.
          if constexpr (CO) {
-            for (int it = lane; it < EPW * Q * D1; it += 32) {
+            for (int it = pt; it < EPW * Q * D1; it += NTH) {
                const int j = it / (Q * D1), r = it % (Q * D1), jx = r % Q, c = r / Q;
                const int po = j * kEp + c * kSp + jx;
                if (KIND == TFEM_DIFFUSION) {
@@ -392,7 +408,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                }
             }
          } else if constexpr (!kRows3) {
-            for (int jj = lane; jj < EPW * NT; jj += 32) {
+            for (int jj = pt; jj < EPW * NT; jj += NTH) {
                const int j = jj / NT, r = jj % NT, jx = r % Q, cb = r / Q, b = cb % D1, c = cb / D1;
                const int po = j * kEp;
                double sx = 0.0, syz = 0.0;
@@ -409,7 +425,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                sm.TG[j * kEt + cb * kSt + jx] = syz;
             }
          } else
-         for (int it = lane; it < EPW * Q * D1; it += 32) {
+         for (int it = pt; it < EPW * Q * D1; it += NTH) {
             const int j = it / (Q * D1), r = it % (Q * D1), jx = r % Q, c = r / Q;
             const int po = j * kEp + c * kSp + jx;
             double px[Q], py[Q], pz[Q];
@@ -437,11 +453,11 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                if (KIND == TFEM_DIFFUSION) sm.TG[o] = syz;
             }
          }
-         __syncwarp();
+         team_sync();
          // contract qx -> r(a, b, c) and the epilogue: a lane per (e, c, b),
          // a unrolled (or a lane per output)
          constexpr int kA = kRows1 ? D1 : 1; // outputs per work item
-         for (int it = lane; it < cnt * ND / kA; it += 32) {
+         for (int it = pt; it < cnt * ND / kA; it += NTH) {
             const int j = it / (ND / kA), cb = kRows1 ? it % (D1 * D1) : (it % ND) / D1;
             double tb[Q], tg[Q];
 #pragma unroll
@@ -496,7 +512,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                }
             }
          }
-         __syncwarp(); // TB / TG / P reused by the next group
+         team_sync(); // TB / TG / P reused by the next group
 #pragma unroll
          for (int m = 0; m < GPL; m++) {
             gcur[m] = gnext[m];
@@ -536,7 +552,7 @@ KernelPick make(int sm_count, bool colloc)
          k.launch = colloc ? launch<P, Q, KIND, true> : launch<P, Q, KIND, false>;
       else
          k.launch = launch<P, Q, KIND, false>;
-      k.elems_per_block = Cfg3<P, Q, KIND>::kW * Warp3<P, Q, KIND>::EPW;
+      k.elems_per_block = Cfg3<P, Q, KIND>::kT * Warp3<P, Q, KIND>::EPW;
       k.threads = Cfg3<P, Q, KIND>::kBlock;
       k.persistent_blocks = sm_count;
       k.energy_dot = true;
