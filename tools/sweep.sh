@@ -10,5 +10,5 @@ for p in 1 2 3 4 6 8; do run --dim 2 --order $p; done
 for p in 1 2 3 4 6 8; do run --dim 3 --order $p; done
 run --dim 2 --order 3 --bp 5; run --dim 2 --order 4 --bp 5
 run --dim 3 --order 2 --bp 5; run --dim 3 --order 4 --bp 5
-run --dim 3 --order 2 --bp 1
+run --dim 3 --order 2 --bp 1 --iters 50
 run --dim 2 --order 3 --cells 3334
