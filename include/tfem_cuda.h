@@ -336,6 +336,8 @@ int tfem_operator_set_comm(tfem_operator *op, const tfem_comm *comm, const tfem_
 int tfem_nccl_unique_id(unsigned char id[TFEM_NCCL_ID_BYTES]);
 int tfem_nccl_create(tfem_ctx *ctx, int nranks, int rank,
                      const unsigned char id[TFEM_NCCL_ID_BYTES], tfem_nccl **out);
+/* Operators keep their communicator alive: destroying the handle first is
+ * safe (the last operator using it releases it). */
 int tfem_nccl_destroy(tfem_nccl *comm);
 /* Sum k doubles of device memory over the ranks, in place (synchronous). */
 int tfem_nccl_allreduce(tfem_ctx *ctx, tfem_nccl *comm, double *device_buf, int64_t k);

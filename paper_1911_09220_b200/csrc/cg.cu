@@ -597,6 +597,7 @@ void free_nccl_buffers(tfem_operator *op)
    }
    cudaFree(op->red);
    op->red = nullptr;
+   nccl_destroy(op->nccl); // the operator's reference
    op->nccl = nullptr;
 }
 
@@ -677,6 +678,7 @@ void operator_set_nccl(tfem_ctx *ctx, tfem_operator *op, tfem_nccl *comm, int n_
    op->red = dalloc<double>(4);
    op->comm = tfem_comm{};
    op->nccl = comm;
+   nccl_retain(comm);
 }
 
 // Sum red[0..k) over the ranks, in stream order.

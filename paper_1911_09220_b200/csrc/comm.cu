@@ -101,8 +101,11 @@ tfem_nccl *nccl_create(tfem_ctx *ctx, int nranks, int rank, const unsigned char 
    return c;
 }
 
+void nccl_retain(tfem_nccl *c) { c->refs++; }
+
 void nccl_destroy(tfem_nccl *c)
 {
+   if (--c->refs > 0) return;
    if (c->comm) api().commDestroy(static_cast<ncclComm_t>(c->comm));
    delete c;
 }

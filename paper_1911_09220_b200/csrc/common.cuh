@@ -215,6 +215,9 @@ struct tfem_nccl {
    tfem_ctx *ctx = nullptr;
    void *comm = nullptr; // ncclComm_t
    int rank = 0, nranks = 1;
+   // the handle plus every operator using the communicator: destroying the
+   // handle before its operators leaves the communicator to the last one
+   int refs = 1;
 };
 
 struct tfem_vec {
@@ -339,7 +342,8 @@ void ctx_release(tfem_ctx *ctx);
 // NCCL (comm.cu)
 void nccl_unique_id(unsigned char *id);
 tfem_nccl *nccl_create(tfem_ctx *ctx, int nranks, int rank, const unsigned char *id);
-void nccl_destroy(tfem_nccl *c);
+void nccl_destroy(tfem_nccl *c); // drops one reference (handle or operator)
+void nccl_retain(tfem_nccl *c);
 void nccl_allreduce(tfem_ctx *ctx, const tfem_nccl *c, double *d, int64_t k);
 void nccl_exchange(tfem_ctx *ctx, const tfem_operator *op);
 
