@@ -547,6 +547,66 @@ std::unique_ptr<LinearOperator> constrained_operator(const FormHandle &f,
    return std::make_unique<DeviceOperator>(f.space, f.pa, essential);
 }
 
+// ------------------------------------------------------ RHS / projection
+namespace {
+bool device_h1(const FeSpace &space)
+{
+   return space.collection().family() == FeFamily::H1 &&
+          space.collection().map_type() == MapType::Value && space.collection().order() <= 16;
+}
+
+std::vector<double> eval_at(const std::vector<double> &xy, const std::function<double(Vec2)> &f)
+{
+   std::vector<double> v(xy.size() / 2);
+   for (size_t i = 0; i < v.size(); i++) v[i] = f(Vec2{xy[2 * i], xy[2 * i + 1]});
+   return v;
+}
+} // namespace
+
+bool linear_form(const FeSpace &space, const Coefficient &f, Vector &b)
+{
+   if (!device_h1(space)) return false;
+   tfem_ctx *ctx = context();
+   const auto h = device_space(space);
+   const int p = space.collection().order(), nq = p + 2;
+   std::vector<double> xy(static_cast<size_t>(h->n_elem) * nq * nq * 2);
+   check(tfem_geometry_points(ctx, h->g, nq, TFEM_GAUSS_LEGENDRE, xy.data()));
+   const std::vector<double> fv = eval_at(xy, f);
+   const Wrap wb(b.device_write(), b.size());
+   check(tfem_linear_form(ctx, h->g, h->r, p, fv.data(), wb));
+   return true;
+}
+
+bool project(const FeSpace &space, const std::function<double(Vec2)> &f, Vector &values)
+{
+   if (!device_h1(space)) return false;
+   tfem_ctx *ctx = context();
+   const auto h = device_space(space);
+   const int p = space.collection().order(), nd = p + 1;
+   std::vector<double> xy(static_cast<size_t>(h->n_elem) * nd * nd * 2);
+   check(tfem_geometry_node_points(ctx, h->g, p, xy.data()));
+   const std::vector<double> fv = eval_at(xy, f);
+   // GridFunction(space) starts at zero; DOFs no element touches keep it
+   const Wrap wv(values.device_readwrite(), values.size());
+   check(tfem_project(ctx, h->r, fv.data(), wv));
+   return true;
+}
+
+bool l2_error(const FeSpace &space, const Vector &values, const std::function<double(Vec2)> &u,
+              double &err)
+{
+   if (!device_h1(space)) return false;
+   tfem_ctx *ctx = context();
+   const auto h = device_space(space);
+   const int p = space.collection().order(), nq = p + 3;
+   std::vector<double> xy(static_cast<size_t>(h->n_elem) * nq * nq * 2);
+   check(tfem_geometry_points(ctx, h->g, nq, TFEM_GAUSS_LEGENDRE, xy.data()));
+   const std::vector<double> uv = eval_at(xy, u);
+   const Wrap wx(values.device_read(), values.size());
+   check(tfem_l2_error(ctx, h->g, h->r, p, wx, uv.data(), &err));
+   return true;
+}
+
 // -------------------------------------------------------------------- CG
 const DeviceOperator *device_operator(const LinearOperator &a)
 {

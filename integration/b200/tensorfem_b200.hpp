@@ -113,6 +113,17 @@ Vector form_diagonal(const FormHandle &f);
 std::unique_ptr<LinearOperator> constrained_operator(const FormHandle &f,
                                                      const std::vector<int> &essential);
 
+/// RHS and post-processing on the device for H1 spaces;
+/// each returns false (the reference's host code then runs) for spaces the
+/// device tables do not cover (L2 families, orders > 16).
+///   LinearForm (forms.cpp:400-431): b = G^T B^T (w detJ f)
+///   project_coefficient (fespace.cpp:334-356): nodal values, last element wins
+///   compute_l2_error (fespace.cpp:358-394): q = p+3 Gauss, the host's sequential sum
+bool linear_form(const FeSpace &space, const Coefficient &f, Vector &b);
+bool project(const FeSpace &space, const std::function<double(Vec2)> &f, Vector &values);
+bool l2_error(const FeSpace &space, const Vector &values, const std::function<double(Vec2)> &u,
+              double &err);
+
 /// cg_solve with the whole loop on the device; only a 4-byte state word
 /// crosses per batch of iterations (plus x per iteration when on_iterate is
 /// set, as the callback needs it on the host).

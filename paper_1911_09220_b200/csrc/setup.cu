@@ -303,6 +303,36 @@ inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n +
 
 } // namespace
 
+// Mesh::transformation's audit (mesh.cpp:243-260) ahead of the functions
+// that call it per element in the reference (LinearForm, project_coefficient,
+// compute_l2_error, and the coefficient points of pa_setup): the first
+// inverted element throws the reference's runtime_error.  Cartesian
+// geometries with positive extents cannot invert.
+void audit_geometry(tfem_ctx *ctx, const tfem_geometry *g)
+{
+   if (g->cartesian) return;
+   const GeoTables tc = tables_at(g->order, gauss_points(TFEM_GAUSS_LEGENDRE, g->order + 2, nullptr),
+                                  nullptr);
+   const GeoSource src = source_of(g);
+   unsigned long long *d_err = nullptr;
+   TFEM_CUDA(cudaMalloc(&d_err, sizeof(unsigned long long)));
+   TFEM_CUDA(cudaMemsetAsync(d_err, 0xff, sizeof(unsigned long long), ctx->stream));
+   const int T = 256;
+   const int ncd = g->dim == 2 ? tc.npts * tc.npts : tc.npts * tc.npts * tc.npts;
+   if (g->dim == 2)
+      check_kernel<2><<<blocks_for(ncd * g->ne, T), T, 0, ctx->stream>>>(src, tc, d_err);
+   else
+      check_kernel<3><<<blocks_for(ncd * g->ne, T), T, 0, ctx->stream>>>(src, tc, d_err);
+   ctx->launched();
+   TFEM_CUDA(cudaGetLastError());
+   unsigned long long herr = 0;
+   TFEM_CUDA(cudaMemcpyAsync(&herr, d_err, sizeof(herr), cudaMemcpyDeviceToHost, ctx->stream));
+   TFEM_CUDA(cudaStreamSynchronize(ctx->stream));
+   cudaFree(d_err);
+   if (herr != ~0ull)
+      runtime("Mesh::transformation: inverted element " + std::to_string(herr >> 24));
+}
+
 tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq, int rule,
                   const double *coeff_host, double coeff_const, int64_t *bad_elem)
 {
@@ -392,6 +422,7 @@ tfem_pa *pa_setup(tfem_ctx *ctx, int kind, const tfem_geometry *g, int p, int nq
 void geometry_points(tfem_ctx *ctx, const tfem_geometry *g, int nq, int rule, double *host_xyz)
 {
    if (nq < 1 || nq > kMaxQ) invalid("geometry_points: points per axis must be in [1, 19]");
+   audit_geometry(ctx, g);
    const int dim = g->dim;
    const int nqd = dim == 2 ? nq * nq : nq * nq * nq;
    const GeoTables t = tables_at(g->order, gauss_points(rule, nq, nullptr), nullptr);
@@ -451,6 +482,7 @@ void geometry_node_points(tfem_ctx *ctx, const tfem_geometry *g, int p, double *
 {
    if (g->dim != 2) invalid("project_coefficient: 2D spaces");
    if (p < 1 || p > kMaxP) invalid("project_coefficient: order must be in [1, 16]");
+   audit_geometry(ctx, g);
    std::vector<double> nodes, bary;
    basis_nodes(p, TFEM_NODES_GAUSS_LOBATTO, nodes, bary);
    const GeoTables t = tables_at(g->order, nodes, nullptr);
