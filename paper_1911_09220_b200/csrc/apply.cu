@@ -162,35 +162,22 @@ BucketArgs bucket_args(const tfem_restriction *r, bool global_only)
 // -------------------------------------------------------------- diagonal
 // Exact diagonal with the dense tabulated tables of pa_diagonal
 // (forms.cpp:22-42, 334-347): per (element, local DOF i) sum over the points
-// in order.  i is uniform per block row (blockIdx.y) so the 1D-table reads
-// are warp-uniform constant-bank loads.
-template <int DIM>
-__global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne, int64_t ne_pad,
-                            const double *__restrict__ qdata, int qlayout, const uint32_t *gmap,
-                            int elem_major, const uint16_t *evperm, double *evec, double *y)
+// in order.  Bt(q, i) / Gt(q, i) are the 1D tables, D(c, q) the element's
+// point factors; both kernels below run this one expression.
+template <int DIM, class TB, class TG, class TD>
+__device__ __forceinline__ double diag_sum(int kind, int nq, int nqd, int ia, int ib, int ic,
+                                           TB Bt, TG Gt, TD D)
 {
-   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; // position
-   const int i = blockIdx.y;
-   if (e >= ne) return;
-   const int D1 = p + 1;
-   const int nd = DIM == 2 ? D1 * D1 : D1 * D1 * D1;
-   const int nqd = DIM == 2 ? nq * nq : nq * nq * nq;
-   const int ncomp = kind == TFEM_MASS ? 1 : (DIM == 2 ? 3 : 6);
-   const int ia = i % D1, ib = (i / D1) % D1, ic = i / (D1 * D1);
-   // qdata addressing follows the map layout (elem_major_layout)
-   auto D = [&](int c, int q) -> double {
-      return __ldg(qdata + qdata_index(qlayout, e, c, q, ncomp, nqd, nq, ne_pad));
-   };
    double s = 0.0;
    for (int q = 0; q < nqd; q++) {
       const int qx = q % nq, qy = (q / nq) % nq, qz = q / (nq * nq);
       if (DIM == 2) {
          if (kind == TFEM_MASS) {
-            const double b = __dmul_rn(t.B[qx][ia], t.B[qy][ib]);
+            const double b = __dmul_rn(Bt(qx, ia), Bt(qy, ib));
             s = __dadd_rn(s, __dmul_rn(__dmul_rn(b, b), D(0, q)));
          } else {
-            const double gx = __dmul_rn(t.G[qx][ia], t.B[qy][ib]);
-            const double gy = __dmul_rn(t.B[qx][ia], t.G[qy][ib]);
+            const double gx = __dmul_rn(Gt(qx, ia), Bt(qy, ib));
+            const double gy = __dmul_rn(Bt(qx, ia), Gt(qy, ib));
             const double term =
                __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(gx, gx), D(0, q)),
                                    __dmul_rn(__dmul_rn(__dmul_rn(2.0, gx), gy), D(1, q))),
@@ -198,8 +185,8 @@ __global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne,
             s = __dadd_rn(s, term);
          }
       } else {
-         const double Bx = t.B[qx][ia], By = t.B[qy][ib], Bz = t.B[qz][ic];
-         const double Gx = t.G[qx][ia], Gy = t.G[qy][ib], Gz = t.G[qz][ic];
+         const double Bx = Bt(qx, ia), By = Bt(qy, ib), Bz = Bt(qz, ic);
+         const double Gx = Gt(qx, ia), Gy = Gt(qy, ib), Gz = Gt(qz, ic);
          if (kind == TFEM_MASS) {
             const double b = __dmul_rn(__dmul_rn(Bx, By), Bz);
             s = __dadd_rn(s, __dmul_rn(__dmul_rn(b, b), D(0, q)));
@@ -217,13 +204,82 @@ __global__ void diag_kernel(const Tables t, int p, int nq, int kind, int64_t ne,
          }
       }
    }
-   const int64_t slot = elem_major ? e * nd + i : (int64_t)i * ne_pad + e;
+   return s;
+}
+
+__device__ __forceinline__ void diag_out(double s, int64_t slot, int64_t ev, const uint32_t *gmap,
+                                         double *evec, double *y)
+{
    const uint32_t g = gmap[slot];
    if (is_exclusive(g)) {
       const uint32_t d = g & kDofMask;
       y[d] = __dadd_rn(y[d], s);
    } else {
-      evec[elem_major ? ev_em_p(evperm, nd, e, i) : (int64_t)i * ne_pad + e] = s;
+      evec[ev] = s;
+   }
+}
+
+// Planes layout (2D p <= 3): a thread per element position, i uniform per
+// block row (blockIdx.y) so the 1D-table reads are warp-uniform constant-bank
+// loads and the point-factor reads are coalesced across elements.
+__global__ void diag_planes_kernel(const Tables t, int p, int nq, int kind, int64_t ne,
+                                   int64_t ne_pad, const double *__restrict__ qdata,
+                                   const uint32_t *gmap, double *evec, double *y)
+{
+   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; // position
+   const int i = blockIdx.y;
+   if (e >= ne) return;
+   const int D1 = p + 1, nqd = nq * nq;
+   const int ncomp = kind == TFEM_MASS ? 1 : 3;
+   const double s = diag_sum<2>(
+      kind, nq, nqd, i % D1, i / D1, 0, [&](int q, int k) { return t.B[q][k]; },
+      [&](int q, int k) { return t.G[q][k]; },
+      [&](int c, int q) { return __ldg(qdata + qdata_index(0, e, c, q, ncomp, nqd, nq, ne_pad)); });
+   const int64_t slot = (int64_t)i * ne_pad + e;
+   diag_out(s, slot, slot, gmap, evec, y);
+}
+
+// Element-major layout (3D, 2D p >= 4): a block per epb elements stages
+// their point factors ([e][c][q], contiguous) in shared memory with coalesced
+// loads -- each factor is read from HBM once, not once per local DOF -- and
+// a thread per (element, i) sums over the points from there.  Elements whose
+// factors exceed the budget (3D q >= 13) read them from global memory
+// (staged = 0, one element per block: the block's loads of a factor coincide).
+constexpr int kDiagThreads = 256;
+constexpr size_t kDiagSmemMax = 96 * 1024;
+
+template <int DIM>
+__global__ void __launch_bounds__(kDiagThreads)
+diag_em_kernel(const Tables t, int p, int nq, int kind, int64_t ne, int epb, int staged,
+               const double *__restrict__ qdata, const uint32_t *gmap, const uint16_t *evperm,
+               double *evec, double *y)
+{
+   extern __shared__ double sq[]; // [epb][ncomp][nqd]
+   __shared__ double sB[kMaxQ * (kMaxP + 1)], sG[kMaxQ * (kMaxP + 1)];
+   const int D1 = p + 1;
+   const int nd = DIM == 2 ? D1 * D1 : D1 * D1 * D1;
+   const int nqd = DIM == 2 ? nq * nq : nq * nq * nq;
+   const int ncomp = kind == TFEM_MASS ? 1 : (DIM == 2 ? 3 : 6);
+   const int per = ncomp * nqd;
+   for (int j = threadIdx.x; j < nq * D1; j += blockDim.x) {
+      sB[j] = t.B[j / D1][j % D1];
+      sG[j] = t.G[j / D1][j % D1];
+   }
+   const int64_t e0 = blockIdx.x * (int64_t)epb;
+   const int cnt = static_cast<int>(ne - e0 < epb ? ne - e0 : epb);
+   const double *src = qdata + e0 * per;
+   if (staged)
+      for (int j = threadIdx.x; j < cnt * per; j += blockDim.x) sq[j] = __ldg(src + j);
+   __syncthreads();
+   for (int w = threadIdx.x; w < cnt * nd; w += blockDim.x) {
+      const int el = w / nd, i = w % nd;
+      const double *qd = (staged ? sq : src) + el * per;
+      const double s = diag_sum<DIM>(
+         kind, nq, nqd, i % D1, (i / D1) % D1, i / (D1 * D1),
+         [&](int q, int k) { return sB[q * D1 + k]; }, [&](int q, int k) { return sG[q * D1 + k]; },
+         [&](int c, int q) { return qd[c * nqd + q]; });
+      const int64_t e = e0 + el;
+      diag_out(s, e * nd + i, ev_em_p(evperm, nd, e, i), gmap, evec, y);
    }
 }
 
@@ -360,15 +416,28 @@ void pa_diagonal(tfem_ctx *ctx, const tfem_pa *pa, const tfem_restriction *r, do
    check_pair(pa, r);
    const Tables t = tables_of(pa);
    double *evec = r->needs_evec() ? const_cast<tfem_restriction *>(r)->ensure_evec() : nullptr;
-   const int T = 128;
-   dim3 grid(blocks_for(pa->npos, T), r->nd);
-   const int elem_major = pa->elem_major() ? 1 : 0;
-   if (pa->dim == 2)
-      diag_kernel<2><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->npos, pa->ne_pad,
-                                                 pa->qdata, pa->qlayout, r->gmap, elem_major, r->evperm, evec, diag);
-   else
-      diag_kernel<3><<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->npos, pa->ne_pad,
-                                                 pa->qdata, pa->qlayout, r->gmap, elem_major, r->evperm, evec, diag);
+   if (!pa->elem_major()) {
+      const int T = 128;
+      const dim3 grid(blocks_for(pa->npos, T), r->nd);
+      diag_planes_kernel<<<grid, T, 0, ctx->stream>>>(t, pa->p, pa->nq, pa->kind, pa->npos,
+                                                      pa->ne_pad, pa->qdata, r->gmap, evec, diag);
+   } else {
+      const size_t per = sizeof(double) * pa->ncomp * pa->nqd;
+      const int staged = per <= kDiagSmemMax ? 1 : 0;
+      int epb = std::max(1, kDiagThreads / r->nd);
+      epb = staged ? static_cast<int>(std::min<size_t>(epb, kDiagSmemMax / per)) : 1;
+      const size_t smem = staged ? per * epb : 0;
+      const unsigned grid = blocks_for(pa->npos, epb);
+      if (pa->dim == 2) {
+         max_dynamic_smem((const void *)diag_em_kernel<2>, kDiagSmemMax);
+         diag_em_kernel<2><<<grid, kDiagThreads, smem, ctx->stream>>>(
+            t, pa->p, pa->nq, pa->kind, pa->npos, epb, staged, pa->qdata, r->gmap, r->evperm, evec, diag);
+      } else {
+         max_dynamic_smem((const void *)diag_em_kernel<3>, kDiagSmemMax);
+         diag_em_kernel<3><<<grid, kDiagThreads, smem, ctx->stream>>>(
+            t, pa->p, pa->nq, pa->kind, pa->npos, epb, staged, pa->qdata, r->gmap, r->evperm, evec, diag);
+      }
+   }
    ctx->launched();
    TFEM_CUDA(cudaGetLastError());
    if (r->n_shared > 0)
