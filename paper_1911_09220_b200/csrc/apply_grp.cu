@@ -206,6 +206,20 @@ __global__ void apply3d_kernel(const ApplyArgs a)
    __syncthreads();
    const int qx = t % Q, qy = t / Q;
    if (live && t < Q * Q) {
+      // q >= 10: the column's point factors stream kR planes ahead of the qz
+      // walk (issued before the b contraction), so their latency is not paid
+      // at every qz step (measured p = 8: +8 %; p = 6, 7: neutral to -2 %,
+      // so there each plane is loaded at its own step)
+      constexpr int NCQ = KIND == TFEM_MASS ? 1 : 6;
+      constexpr int kR = Q >= 10 ? 3 : 0;
+      const double *qd = a.qdata + e * (int64_t)NCQ * NQD + qx + Q * qy;
+      double Dq[NCQ][Q];
+      auto load_plane = [&](int qz) {
+#pragma unroll
+         for (int c = 0; c < NCQ; c++) Dq[c][qz] = __ldg(qd + c * NQD + Q * Q * qz);
+      };
+#pragma unroll
+      for (int qz = 0; qz < kR && qz < Q; qz++) load_plane(qz);
       double UBB[D1], UBG[D1], UGB[D1];
 #pragma unroll
       for (int c = 0; c < D1; c++) { // contract b
@@ -227,15 +241,15 @@ __global__ void apply3d_kernel(const ApplyArgs a)
       double Px[D1], Py[D1], Pz[D1];
 #pragma unroll
       for (int c = 0; c < D1; c++) Px[c] = Py[c] = Pz[c] = 0.0;
-      const double *qd = a.qdata + e * (int64_t)(KIND == TFEM_MASS ? 1 : 6) * NQD;
 #pragma unroll
       for (int qz = 0; qz < Q; qz++) { // contract c, point factors, back over qz
-         const int q = qx + Q * (qy + Q * qz);
+         if (kR == 0) load_plane(qz);
+         else if (qz + kR < Q) load_plane(qz + kR);
          if (KIND == TFEM_MASS) {
             double u = 0.0;
 #pragma unroll
             for (int c = 0; c < D1; c++) u = fma(a.t.B[qz][c], UBB[c], u);
-            const double w = u * __ldg(qd + q);
+            const double w = u * Dq[0][qz];
 #pragma unroll
             for (int c = 0; c < D1; c++) Px[c] = fma(a.t.B[qz][c], w, Px[c]);
          } else {
@@ -246,9 +260,8 @@ __global__ void apply3d_kernel(const ApplyArgs a)
                uy = fma(a.t.B[qz][c], UBG[c], uy);
                uz = fma(a.t.G[qz][c], UBB[c], uz);
             }
-            const double D00 = __ldg(qd + q), D01 = __ldg(qd + NQD + q);
-            const double D02 = __ldg(qd + 2 * NQD + q), D11 = __ldg(qd + 3 * NQD + q);
-            const double D12 = __ldg(qd + 4 * NQD + q), D22 = __ldg(qd + 5 * NQD + q);
+            const double D00 = Dq[0][qz], D01 = Dq[1][qz], D02 = Dq[2][qz];
+            const double D11 = Dq[3][qz], D12 = Dq[4][qz], D22 = Dq[5][qz];
             const double wx = fma(D02, uz, fma(D01, uy, D00 * ux));
             const double wy = fma(D12, uz, fma(D11, uy, D01 * ux));
             const double wz = fma(D22, uz, fma(D12, uy, D02 * ux));
