@@ -395,6 +395,12 @@ int tfem_fp64_peak(tfem_ctx *ctx, double *tflops);
  * TFLOP/s -- the ceiling a DMMA contraction would have (north_star: DMMA only
  * where it beats CUDA-core DFMA). */
 int tfem_dmma_peak(tfem_ctx *ctx, double *tflops);
+/* Diagnostics: DFMA vs DMMA A/B of the sum-factorisation contraction stage
+ * (per element X[p+1][(p+1)^2] -> B X, G X with q = p+2 points) on shared-
+ * memory-resident elements, order p in [2, 8]: res[0] DFMA and res[1] DMMA
+ * useful TFLOP/s, res[2] max relative difference of the two results, res[3]
+ * the DMMA tile padding factor (padded / useful multiply-adds). */
+int tfem_contraction_ab(tfem_ctx *ctx, int p, double *res);
 
 #ifdef __cplusplus
 }

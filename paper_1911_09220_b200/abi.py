@@ -164,6 +164,7 @@ _PROTOS = {
     "tfem_cg_profile": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, dp]),
     "tfem_fp64_peak": (C.c_int, [vp, dp]),
     "tfem_dmma_peak": (C.c_int, [vp, dp]),
+    "tfem_contraction_ab": (C.c_int, [vp, C.c_int, dp]),
     "tfem_cg_solve_host": (C.c_int, [vp, vp, dp, C.c_double, C.c_int, dp, dp,
                                      C.POINTER(CgResult)]),
 }

@@ -49,8 +49,12 @@ struct alignas(16) Warp3 {
    static constexpr int D1 = P + 1, ND = D1 * D1 * D1, NQD = Q * Q * Q;
    static constexpr int NC = KIND == TFEM_MASS ? 1 : 6;
    static constexpr int EPW = epw<Q>();
-   static constexpr int kSlots = 2;
-   double q[kSlots][EPW * NC * NQD];                  // the group's point factors
+   // q >= 8 (QG): the point factors are read from global memory in the
+   // column stage (planes prefetched into registers) -- double-buffering
+   // nc q^3 doubles per element in shared memory would leave too few warps
+   static constexpr bool QG = Q >= 8;
+   static constexpr int kSlots = QG ? 1 : 2;
+   double q[kSlots][QG ? 1 : EPW * NC * NQD];         // the group's point factors
    double V[2][EPW * ND];                             // x of the open / next group
    static constexpr int kSt = Q + pad_t3(P, Q), kSp = Q * Q + pad_p3(P, Q); // padded strides
    static constexpr int kEt = D1 * D1 * kSt, kEp = D1 * kSp;                   // per element
@@ -69,19 +73,26 @@ struct Cfg3 {
    // double-buffered point factors -- feeds twice the warps.  Measured (10M
    // DOFs): BP3 p=5 +17 %, BP5 p=5 +64 %; at p = 4, q = 6 (25 rows) one
    // warp per element stays faster (-7 % with teams: idle threads).
-   static constexpr int WPE = (P + 1) * (P + 1) > 32 && Q * Q > 32 ? 2 : 1;
+   // QG: one column per thread, ceil(q^2 / 32) warps per element (<= 4).
+   static constexpr bool QG = Warp3<P, Q, KIND>::QG;
+   static constexpr int WPE = QG ? ((Q * Q + 31) / 32 < 4 ? (Q * Q + 31) / 32 : 4)
+                                 : (P + 1) * (P + 1) > 32 && Q * Q > 32 ? 2 : 1;
    static constexpr size_t kWarpBytes = sizeof(Warp3<P, Q, KIND>);
    // computing warps as shared memory allows: 224 KB (vs 200) is +9 % at
    // p = 4 (6 -> 7 warps), neutral where the 11-warp cap or the warp size binds
    static constexpr int kT0 = static_cast<int>((224 * 1024) / kWarpBytes); // teams by smem
    // warp cap from the registers ptxas needs: 11 (170 each) by default, 15
    // (128) at p <= 2 with q <= p + 2 except p = 2, q = 4, 13 (146) at p = 3, q = 5
-   static constexpr int kMaxW = KIND != TFEM_DIFFUSION ? 11
+   // QG (measured, 10M DOFs): p = 6, q = 8 four two-warp teams (254
+   // registers, +15 % over the group kernel; 12 warps -7 %); p = 7, q = 9
+   // four three-warp teams (168 registers, some spills: +8 %; 6 warps -11 %)
+   static constexpr int kMaxW = QG ? (P == 6 ? 8 : 12)
+                              : KIND != TFEM_DIFFUSION ? 11
                               : (Q <= 3) ? 15 : (P == 3 && Q == 5) ? 13 : 11;
    static constexpr int kT1 = kT0 * WPE > kMaxW ? kMaxW / WPE : kT0;
    static constexpr int kT = kT1 < 1 ? 1 : kT1;   // teams (elements in flight)
    static constexpr int kW = kT * WPE;            // compute warps
-   static constexpr int kBlock = 32 * (kW + 1);
+   static constexpr int kBlock = 32 * (kW + (QG ? 0 : 1)); // + the producer warp
    static constexpr size_t kSmem = kWarpBytes * kT;
 };
 
@@ -140,7 +151,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
       return static_cast<int>(left < EPW ? (left > 0 ? left : 0) : EPW);
    };
    double dot = 0.0;
-   if (warp == kW) {
+   if (!W::QG && warp == kW) {
       // ---------------------------------------------------------- producer
       if (lane == 0) {
          for (int64_t k = 0;; k++) {
@@ -274,13 +285,26 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          load_mask(gn, gnext, mnext);
          team_sync();
          const int s = static_cast<int>(k % kSlots);
-         mbar_wait(&sm.full[s], static_cast<unsigned>((k / kSlots) & 1));
+         if constexpr (!W::QG) mbar_wait(&sm.full[s], static_cast<unsigned>((k / kSlots) & 1));
          // column stage: (element ej, qx, qy) columns over the lanes
          for (int cl = pt; cl < EPW * Q * Q; cl += NTH) {
             const int ej = cl / (Q * Q), col = cl % (Q * Q);
             const int qx = col % Q, qy = col / Q;
             const bool live = ej < cnt;
             const double *TB = sm.TB + ej * kEt, *TG = sm.TG + ej * kEt;
+            // QG: the column's point factors, kR planes ahead of the qz walk
+            // (the first ones issued before the b contraction)
+            constexpr int kR = 3;
+            double Dq[W::QG ? NC : 1][W::QG ? Q : 1];
+            const double *qg = a.qdata + (g * EPW + (live ? ej : 0)) * (int64_t)(NC * NQD) + col;
+            auto load_plane = [&](int qz) {
+               if constexpr (W::QG) {
+#pragma unroll
+                  for (int c = 0; c < NC; c++) Dq[c][qz] = __ldg(qg + c * NQD + Q * Q * qz);
+               }
+            };
+#pragma unroll
+            for (int qz = 0; qz < kR && qz < Q; qz++) load_plane(qz);
             double UBB[D1], UBG[D1], UGB[D1];
             if constexpr (CO) {
                // UBB = V[c][qy][qx], UGB = TG[c][qy][qx], UBG = G_y V
@@ -318,9 +342,15 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
 #pragma unroll
             for (int c = 0; c < D1; c++) Px[c] = Py[c] = Pz[c] = 0.0;
             const double *qd = sm.q[s] + ej * NC * NQD;
+            // point factor c at plane qz of this column
+            auto D = [&](int c, int qz, int q) -> double {
+               if constexpr (W::QG) return Dq[c][qz];
+               else return qd[c * NQD + q];
+            };
 #pragma unroll
             for (int qz = 0; qz < Q; qz++) { // contract c, point factors, back over qz
                const int q = qx + Q * (qy + Q * qz);
+               if (qz + kR < Q) load_plane(qz + kR);
                // (qz, c) are compile-time here: table operands come from the
                // constant bank, not shared memory
                if (KIND == TFEM_MASS) {
@@ -331,7 +361,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
 #pragma unroll
                      for (int c = 0; c < D1; c++) u = fma(a.t.B[qz][c], UBB[c], u);
                   }
-                  const double w = u * qd[q];
+                  const double w = u * D(0, qz, q);
                   if (EDOT && live) dot = fma(u, w, dot);
                   if constexpr (CO) {
                      Px[qz] = w;
@@ -354,8 +384,8 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                         uz = fma(a.t.G[qz][c], UBB[c], uz);
                      }
                   }
-                  const double D00 = qd[q], D01 = qd[NQD + q], D02 = qd[2 * NQD + q];
-                  const double D11 = qd[3 * NQD + q], D12 = qd[4 * NQD + q], D22 = qd[5 * NQD + q];
+                  const double D00 = D(0, qz, q), D01 = D(1, qz, q), D02 = D(2, qz, q);
+                  const double D11 = D(3, qz, q), D12 = D(4, qz, q), D22 = D(5, qz, q);
                   const double wx = fma(D02, uz, fma(D01, uy, D00 * ux));
                   const double wy = fma(D12, uz, fma(D11, uy, D01 * ux));
                   const double wz = fma(D22, uz, fma(D12, uy, D02 * ux));
@@ -386,7 +416,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             }
          }
          team_sync();
-         if (pt == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
+         if (!W::QG && pt == 0) mbar_arrive(&sm.empty[s]); // point factors consumed
          // contract qy -> [e][c][b][qx] (x-gradient part in TB, y + z in TG):
          // a lane per (e, c, qx), b unrolled (or a lane per output).  CO: TB
          // is Px itself (read in place below), TG = G_y Py + Pz.
@@ -546,8 +576,8 @@ template <int P, int Q, int KIND>
 KernelPick make(int sm_count, bool colloc)
 {
    KernelPick k;
-   // bulk copies need 16-byte sizes and element strides
-   if constexpr ((Warp3<P, Q, KIND>::NC * Q * Q * Q) % 2 == 0) {
+   // bulk copies need 16-byte sizes and element strides (QG: none)
+   if constexpr (Warp3<P, Q, KIND>::QG || (Warp3<P, Q, KIND>::NC * Q * Q * Q) % 2 == 0) {
       if constexpr (Q == P + 1)
          k.launch = colloc ? launch<P, Q, KIND, true> : launch<P, Q, KIND, false>;
       else
@@ -563,13 +593,20 @@ KernelPick make(int sm_count, bool colloc)
 template <int KIND>
 KernelPick pick_kind(int p, int nq, int sm, bool co)
 {
-   // up to Q = 7; larger Q leaves too few warps per SM (the group kernel)
+   // q <= 7 bulk-copies the point factors; q >= 8 reads them in the column
+   // stage (QG)
    switch (p) {
    case 1: return nq == 3 ? make<1, 3, KIND>(sm, co) : nq == 2 ? make<1, 2, KIND>(sm, co) : KernelPick{};
    case 2: return nq == 4 ? make<2, 4, KIND>(sm, co) : nq == 3 ? make<2, 3, KIND>(sm, co) : KernelPick{};
    case 3: return nq == 5 ? make<3, 5, KIND>(sm, co) : nq == 4 ? make<3, 4, KIND>(sm, co) : KernelPick{};
    case 4: return nq == 5 ? make<4, 5, KIND>(sm, co) : nq == 6 ? make<4, 6, KIND>(sm, co) : KernelPick{};
    case 5: return nq == 6 ? make<5, 6, KIND>(sm, co) : nq == 7 ? make<5, 7, KIND>(sm, co) : KernelPick{};
+   }
+   // q >= 8, diffusion: QG where it measured faster than the group kernel
+   // (BP3 p = 6, 7; p = 8, BP5 p >= 7 and mass stay on the group kernel)
+   if constexpr (KIND == TFEM_DIFFUSION) {
+      if (p == 6 && nq == 8) return make<6, 8, KIND>(sm, co);
+      if (p == 7 && nq == 9) return make<7, 9, KIND>(sm, co);
    }
    return {};
 }

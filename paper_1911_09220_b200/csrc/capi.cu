@@ -1139,6 +1139,16 @@ int tfem_dmma_peak(tfem_ctx *ctx, double *tflops)
    });
 }
 
+int tfem_contraction_ab(tfem_ctx *ctx, int p, double *res)
+{
+   return guard([&] {
+      need(ctx, "contraction_ab");
+      need(res, "contraction_ab");
+      bind(ctx);
+      contraction_ab(ctx, p, res);
+   });
+}
+
 int tfem_cg_solve_host(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
                        int max_iters, const double *jacobi_diag, double *x, tfem_cg_result *res)
 {

@@ -459,6 +459,9 @@ void operator_mult(tfem_ctx *ctx, const tfem_operator *op, const double *x, doub
 double fp64_peak_tflops(tfem_ctx *ctx);
 // Measured FP64 tensor-core (DMMA m8n8k4) peak in TFLOP/s (probe.cu).
 double dmma_peak_tflops(tfem_ctx *ctx);
+// res[4]: DFMA / DMMA useful TFLOP/s of the x-stage contraction at order p,
+// max relative difference of their results, DMMA padding factor
+void contraction_ab(tfem_ctx *ctx, int p, double *res);
 
 void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double rel_tol,
               int max_iters, const double *diag, double *x, tfem_cg_result *res,

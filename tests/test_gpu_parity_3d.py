@@ -144,3 +144,17 @@ def test_3d_large_properties(dev):
     m.assemble()
     m.mult_true(ones, y)
     assert y.numpy().sum() == pytest.approx(1.0, rel=1e-12)
+
+
+@pytest.mark.parametrize("p", [3, 7])
+def test_contraction_ab_probe(dev, p):
+    """The DFMA vs DMMA contraction A/B (tools/contraction_ab.py): both
+    variants compute the same stage (<= 1e-13 relative) and report rates."""
+    import ctypes as C
+    res = (C.c_double * 4)()
+    tf.abi.check(tf.lib().tfem_contraction_ab(dev.h, p, res))
+    assert res[2] <= 1e-13
+    assert res[0] > 0.5 and res[1] > 0.5
+    assert res[3] >= 1.0
+    with pytest.raises(tf.InvalidArgument):
+        tf.abi.check(tf.lib().tfem_contraction_ab(dev.h, 9, res))
