@@ -86,7 +86,12 @@ struct Cfg3 {
    // QG (measured, 10M DOFs): p = 6, q = 8 four two-warp teams (254
    // registers, +15 % over the group kernel; 12 warps -7 %); p = 7, q = 9
    // four three-warp teams (168 registers, some spills: +8 %; 6 warps -11 %)
+   // (the register file is four 16K banks, one per scheduler: 9-12 warps
+   // per block cap a thread at 168 registers, <= 8 warps at 255.  BP3 p = 5,
+   // q = 7: three teams + producer (7 warps, no spills) +2 % over four teams
+   // at 168 registers with spills.)
    static constexpr int kMaxW = QG ? (P == 6 ? 8 : 12)
+                              : (P == 5 && Q == 7 && KIND == TFEM_DIFFUSION) ? 6
                               : KIND != TFEM_DIFFUSION ? 11
                               : (Q <= 3) ? 15 : (P == 3 && Q == 5) ? 13 : 11;
    static constexpr int kT1 = kT0 * WPE > kMaxW ? kMaxW / WPE : kT0;
