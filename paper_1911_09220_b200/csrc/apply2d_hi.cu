@@ -69,7 +69,7 @@ struct alignas(16) Warp2 {
    uint64_t full[kSlots], empty[kSlots];
 };
 
-template <int P, int Q, int KIND, bool EXACT>
+template <int P, int Q, int KIND, bool EXACT, bool CO = false>
 struct Cfg2 {
    static constexpr size_t kWarpBytes = sizeof(Warp2<P, Q, KIND>);
    // Latency-bound (ncu at p = 6: 2 warps per scheduler, 0.34 eligible):
@@ -81,7 +81,10 @@ struct Cfg2 {
    // needs 168).  12 warps at q = 7, p = 5 measured -2.3 %, at q = 9, p = 8
    // +-1 %: kept at 11 (tools/ab_wide.sh).
    static constexpr bool kDiff = KIND == TFEM_DIFFUSION;
+   // BP5 p = 4 (collocated, 104-112 registers): 13 (+2.6 % at 10M, +1.9 % at
+   // 200M DOFs; 15 -1 %)
    static constexpr int kMaxW = (kDiff && Q == 6 && (P == 4 || P == 5)) ? 15
+                              : (kDiff && CO && P == 4 && Q == 5) ? 13
                               : (kDiff && !EXACT && P == 7 && Q == 9) ? 13
                               : 11;
    static constexpr int kW0 = static_cast<int>((224 * 1024) / kWarpBytes);
@@ -96,12 +99,12 @@ struct Cfg2 {
 // sums add only signed zeros, so results stay bit-identical up to the sign
 // of a zero.
 template <int P, int Q, int KIND, bool EXACT, bool EDOT, bool CO>
-__global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi_kernel(const ApplyArgs a)
+__global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT, CO>::kBlock, 1) apply2d_hi_kernel(const ApplyArgs a)
 {
    static_assert(!CO || Q == P + 1, "collocation needs q = p + 1");
    using W = Warp2<P, Q, KIND>;
    constexpr int D1 = W::D1, ND = W::ND, NQD = W::NQD, NC = W::NC, GRP = W::GRP;
-   constexpr int kW = Cfg2<P, Q, KIND, EXACT>::kW, kBlock = Cfg2<P, Q, KIND, EXACT>::kBlock;
+   constexpr int kW = Cfg2<P, Q, KIND, EXACT, CO>::kW, kBlock = Cfg2<P, Q, KIND, EXACT, CO>::kBlock;
    constexpr int kSlots = W::kSlots;
    constexpr int GPL = (GRP * ND + 31) / 32;
    constexpr unsigned kQBytes = NC * NQD * 8;
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(Cfg2<P, Q, KIND, EXACT>::kBlock, 1) apply2d_hi
 template <int P, int Q, int KIND, bool EXACT, bool CO>
 void launch(const ApplyArgs &a, cudaStream_t s, unsigned grid)
 {
-   using C = Cfg2<P, Q, KIND, EXACT>;
+   using C = Cfg2<P, Q, KIND, EXACT, CO>;
    static_assert(C::kSmem <= 227 * 1024, "shared memory budget");
    if (a.energy_dot) {
       max_dynamic_smem((const void *)apply2d_hi_kernel<P, Q, KIND, EXACT, true, CO>, C::kSmem);
@@ -408,8 +411,16 @@ KernelPick make(bool exact, int sm_count, bool colloc)
 {
    KernelPick k;
    k.launch = exact ? launcher<P, Q, KIND, true>(colloc) : launcher<P, Q, KIND, false>(colloc);
-   k.elems_per_block = (exact ? Cfg2<P, Q, KIND, true>::kW : Cfg2<P, Q, KIND, false>::kW) * Warp2<P, Q, KIND>::GRP;
-   k.threads = exact ? Cfg2<P, Q, KIND, true>::kBlock : Cfg2<P, Q, KIND, false>::kBlock;
+   int kw = exact ? Cfg2<P, Q, KIND, true>::kW : Cfg2<P, Q, KIND, false>::kW;
+   int kb = exact ? Cfg2<P, Q, KIND, true>::kBlock : Cfg2<P, Q, KIND, false>::kBlock;
+   if constexpr (Q == P + 1) {
+      if (colloc) {
+         kw = exact ? Cfg2<P, Q, KIND, true, true>::kW : Cfg2<P, Q, KIND, false, true>::kW;
+         kb = exact ? Cfg2<P, Q, KIND, true, true>::kBlock : Cfg2<P, Q, KIND, false, true>::kBlock;
+      }
+   }
+   k.elems_per_block = kw * Warp2<P, Q, KIND>::GRP;
+   k.threads = kb;
    k.persistent_blocks = sm_count;
    k.energy_dot = true;
    return k;
