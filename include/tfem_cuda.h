@@ -331,7 +331,10 @@ int tfem_operator_set_comm(tfem_operator *op, const tfem_comm *comm, const tfem_
  * per rank (one process -- or one context -- per GPU): rank 0 makes the id,
  * the caller ships it to the other ranks (any channel), every rank creates
  * its communicator.  peer[k] is the rank the k-th send / receive list pairs
- * with; send / receive buffers are allocated by the library. */
+ * with (a rank may list itself); send / receive buffers are allocated by the
+ * library.  In CG the send planes of the new direction are packed first and
+ * exchanged on a side stream while the direction update of the whole vector
+ * runs (halo / compute overlap, graph-captured). */
 #define TFEM_NCCL_ID_BYTES 128
 int tfem_nccl_unique_id(unsigned char id[TFEM_NCCL_ID_BYTES]);
 int tfem_nccl_create(tfem_ctx *ctx, int nranks, int rank,

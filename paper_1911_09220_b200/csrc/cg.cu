@@ -489,6 +489,22 @@ void enqueue_iteration(tfem_ctx *ctx, const tfem_operator *op, Workspace &w, XBu
    TFEM_CUDA(cudaGetLastError());
 }
 
+// The halo part of the direction update, packed for the send: out[i] = the
+// new p at DOF idx[i], with cg_direction_kernel's arithmetic (same bits), so
+// the exchange can run while that kernel updates all of p.
+__global__ void pack_direction_kernel(const CgState *st, const double *__restrict__ r,
+                                      const double *__restrict__ diag,
+                                      const double *__restrict__ p, const int32_t *idx, int64_t n,
+                                      double *out)
+{
+   if (st->done) return;
+   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (i >= n) return;
+   const int32_t j = idx[i];
+   const double zi = diag ? __ddiv_rn(r[j], diag[j]) : r[j];
+   out[i] = __dadd_rn(zi, __dmul_rn(st->beta, p[j]));
+}
+
 __global__ void gather_idx_kernel(const double *v, const int32_t *idx, int64_t n, double *out)
 {
    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -597,6 +613,11 @@ void free_nccl_buffers(tfem_operator *op)
    }
    cudaFree(op->red);
    op->red = nullptr;
+   if (op->side) cudaStreamDestroy(op->side);
+   if (op->ev_fork) cudaEventDestroy(op->ev_fork);
+   if (op->ev_join) cudaEventDestroy(op->ev_join);
+   op->side = nullptr;
+   op->ev_fork = op->ev_join = nullptr;
    nccl_destroy(op->nccl); // the operator's reference
    op->nccl = nullptr;
 }
@@ -666,8 +687,10 @@ void operator_set_nccl(tfem_ctx *ctx, tfem_operator *op, tfem_nccl *comm, int n_
                        const int64_t *n_recv, const int32_t *const *recv_idx,
                        int64_t n_not_owned, const int32_t *not_owned)
 {
+   // a rank may list itself (a self send / receive pair: NCCL supports it;
+   // periodic plans and the overlap test use it)
    for (int k = 0; k < n_peers; k++)
-      if (peer[k] < 0 || peer[k] >= comm->nranks || peer[k] == comm->rank)
+      if (peer[k] < 0 || peer[k] >= comm->nranks)
          invalid("tfem_operator_set_nccl: bad peer rank");
    set_plan(ctx, op, n_peers, n_send, send_idx, n_recv, recv_idx, n_not_owned, not_owned);
    for (int k = 0; k < n_peers; k++) {
@@ -679,6 +702,11 @@ void operator_set_nccl(tfem_ctx *ctx, tfem_operator *op, tfem_nccl *comm, int n_
    op->comm = tfem_comm{};
    op->nccl = comm;
    nccl_retain(comm);
+   if (n_peers > 0) {
+      TFEM_CUDA(cudaStreamCreateWithFlags(&op->side, cudaStreamNonBlocking));
+      TFEM_CUDA(cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming));
+      TFEM_CUDA(cudaEventCreateWithFlags(&op->ev_join, cudaEventDisableTiming));
+   }
 }
 
 // Sum red[0..k) over the ranks, in stream order.
@@ -697,12 +725,53 @@ void halo_exchange(tfem_ctx *ctx, const tfem_operator *op, double *v)
             v, op->send_idx[k], op->n_send[k], op->send_buf[k]);
          ctx->launched();
       }
-   if (op->nccl) nccl_exchange(ctx, op);
+   if (op->nccl) nccl_exchange(ctx, op, ctx->stream);
    else op->comm.exchange(op->comm.user);
    for (int k = 0; k < op->n_peers; k++)
       if (op->n_recv[k] > 0) {
          scatter_idx_kernel<<<blocks_for(op->n_recv[k], 256), 256, 0, ctx->stream>>>(
             op->recv_buf[k], op->recv_idx[k], op->n_recv[k], v);
+         ctx->launched();
+      }
+   TFEM_CUDA(cudaGetLastError());
+}
+
+// The direction step of a distributed iteration with the next operator's
+// halo update folded in: the send planes of the new p are packed straight
+// from r, diag and the old p; with NCCL the exchange then runs on the side
+// stream while cg_direction_kernel updates p and x on the context stream,
+// and the received planes land after both (the direction kernel's values
+// there -- not-owned DOFs -- are overwritten, as the halo update at the
+// start of the iteration used to do).  The host-hook path runs the same
+// data flow synchronously.
+void halo_direction(tfem_ctx *ctx, const tfem_operator *op, CgState *st, const XBufs &xb,
+                    const double *r, const double *diag, double *p, int64_t n, unsigned *ticket)
+{
+   for (int k = 0; k < op->n_peers; k++)
+      if (op->n_send[k] > 0) {
+         pack_direction_kernel<<<blocks_for(op->n_send[k], 256), 256, 0, ctx->stream>>>(
+            st, r, diag, p, op->send_idx[k], op->n_send[k], op->send_buf[k]);
+         ctx->launched();
+      }
+   const bool overlap = op->nccl && op->side;
+   if (overlap) {
+      TFEM_CUDA(cudaEventRecord(op->ev_fork, ctx->stream));
+      TFEM_CUDA(cudaStreamWaitEvent(op->side, op->ev_fork, 0));
+      nccl_exchange(ctx, op, op->side);
+      TFEM_CUDA(cudaEventRecord(op->ev_join, op->side));
+   } else if (op->nccl) {
+      nccl_exchange(ctx, op, ctx->stream);
+   } else {
+      op->comm.exchange(op->comm.user);
+   }
+   cg_direction_kernel<<<vec_blocks(ctx, n), kVecThreads, 0, ctx->stream>>>(st, xb, r, diag, p, n,
+                                                                           ticket);
+   ctx->launched();
+   if (overlap) TFEM_CUDA(cudaStreamWaitEvent(ctx->stream, op->ev_join, 0));
+   for (int k = 0; k < op->n_peers; k++)
+      if (op->n_recv[k] > 0) {
+         scatter_idx_kernel<<<blocks_for(op->n_recv[k], 256), 256, 0, ctx->stream>>>(
+            op->recv_buf[k], op->recv_idx[k], op->n_recv[k], p);
          ctx->launched();
       }
    TFEM_CUDA(cudaGetLastError());
@@ -876,10 +945,12 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
    TFEM_CUDA(cudaGetLastError());
    const XBufs xb{{x, w.xa, w.xb}};
 
-   // Distributed iteration: halo update of p, then the same kernels with the
-   // rank-local folds summed over ranks by the allreduce hook.
+   // Distributed iteration: the same kernels with the rank-local folds
+   // summed over ranks (NCCL allreduce or the hook); p's halo is valid on
+   // entry (the initial update below, then halo_direction at the end of
+   // every iteration).
+   if (comm) halo_exchange(ctx, op, w.p);
    auto dist_iteration = [&]() {
-      halo_exchange(ctx, op, w.p);
       operator_mult(ctx, op, w.p, w.q, &w.s_elem.s, w.s_scatter.grid ? &w.s_scatter.s : nullptr,
                     &w.st->done);
       fold_to_kernel<<<1, kVecThreads, 0, ctx->stream>>>(w.s_elem.s.chunks, w.s_elem.nch,
@@ -893,10 +964,8 @@ void cg_solve(tfem_ctx *ctx, const tfem_operator *op, const double *b, double re
                                                          0, 2, op->red);
       comm_allreduce(ctx, op, 2);
       red_beta_kernel<<<1, 1, 0, ctx->stream>>>(op->red, w.st);
-      cg_direction_kernel<<<vb, kVecThreads, 0, ctx->stream>>>(w.st, xb, w.r, diag, w.p, n,
-                                                            w.dir_ticket);
-      ctx->launched(6);
-      TFEM_CUDA(cudaGetLastError());
+      ctx->launched(5);
+      halo_direction(ctx, op, w.st, xb, w.r, diag, w.p, n, w.dir_ticket);
    };
 
    auto read_state = [&]() {

@@ -121,18 +121,19 @@ void nccl_allreduce(tfem_ctx *ctx, const tfem_nccl *c, double *d, int64_t k)
 
 // The halo update's transfers: every peer's send buffer out, its receive
 // buffer in, one NCCL group (deadlock-free in any peer order).
-void nccl_exchange(tfem_ctx *ctx, const tfem_operator *op)
+void nccl_exchange(tfem_ctx *ctx, const tfem_operator *op, cudaStream_t s)
 {
+   (void)ctx;
    const NcclApi &a = api();
    nccl_check(a.groupStart(), "ncclGroupStart");
    for (int k = 0; k < op->n_peers; k++) {
       if (op->n_send[k] > 0)
          nccl_check(a.send(op->send_buf[k], static_cast<size_t>(op->n_send[k]), ncclFloat64,
-                           op->peer_rank[k], static_cast<ncclComm_t>(op->nccl->comm), ctx->stream),
+                           op->peer_rank[k], static_cast<ncclComm_t>(op->nccl->comm), s),
                     "ncclSend");
       if (op->n_recv[k] > 0)
          nccl_check(a.recv(op->recv_buf[k], static_cast<size_t>(op->n_recv[k]), ncclFloat64,
-                           op->peer_rank[k], static_cast<ncclComm_t>(op->nccl->comm), ctx->stream),
+                           op->peer_rank[k], static_cast<ncclComm_t>(op->nccl->comm), s),
                     "ncclRecv");
    }
    nccl_check(a.groupEnd(), "ncclGroupEnd");

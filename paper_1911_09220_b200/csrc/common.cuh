@@ -330,6 +330,10 @@ struct tfem_operator {
    int32_t *send_idx[TFEM_MAX_PEERS] = {}, *recv_idx[TFEM_MAX_PEERS] = {}; // device
    double *send_buf[TFEM_MAX_PEERS] = {}, *recv_buf[TFEM_MAX_PEERS] = {}; // caller's
    double *red = nullptr;                                                // caller's
+   // NCCL halo overlap: the exchange runs on `side` while the direction
+   // kernel runs on the context stream (fork / join events; graph-capturable)
+   cudaStream_t side = nullptr;
+   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
    int32_t *rowptr = nullptr, *cols = nullptr;
    double *vals = nullptr;
 };
@@ -345,7 +349,7 @@ tfem_nccl *nccl_create(tfem_ctx *ctx, int nranks, int rank, const unsigned char 
 void nccl_destroy(tfem_nccl *c); // drops one reference (handle or operator)
 void nccl_retain(tfem_nccl *c);
 void nccl_allreduce(tfem_ctx *ctx, const tfem_nccl *c, double *d, int64_t k);
-void nccl_exchange(tfem_ctx *ctx, const tfem_operator *op);
+void nccl_exchange(tfem_ctx *ctx, const tfem_operator *op, cudaStream_t s);
 
 constexpr int kChunk = 32;
 
