@@ -7,6 +7,9 @@ rank-local folds + allreduce).
 * 2 ranks sharing the one GPU over gloo (host-staged hooks; no kernel waits
   on another process): same iteration count as the single-device solve of
   the global problem, same solution on owned DOFs.
+* the halo / direction overlap of the NCCL path (side stream, fork / join,
+  graph-captured) against the synchronous hook path on a self-exchange plan:
+  bit-identical iterates.
 """
 import socket
 import sys
