@@ -55,6 +55,15 @@ struct alignas(16) Warp3 {
    static constexpr bool QG = Q >= 8;
    static constexpr int kSlots = QG ? 1 : 2;
    double q[kSlots][QG ? 1 : EPW * NC * NQD];         // the group's point factors
+   // QG slab ring: each column thread's point factors of kSlab qz planes in
+   // flight (cp.async, completion on sfull[slot]); thread-private entries
+   // (q >= 9: +23 % at BP3 p = 7 over the register prefetch; at q = 8 the
+   // register prefetch is 5 % faster)
+   static constexpr bool SLAB = QG && Q >= 9;
+   static constexpr int kSlab = SLAB ? 4 : 1;
+   static constexpr int NTHq = 32 * ((Q * Q + 31) / 32 < 4 ? (Q * Q + 31) / 32 : 4);
+   double slab[SLAB ? kSlab * NC * NTHq : 1]; // [slot][c][thread]
+   uint64_t sfull[kSlab];
    double V[2][EPW * ND];                             // x of the open / next group
    static constexpr int kSt = Q + pad_t3(P, Q), kSp = Q * Q + pad_p3(P, Q); // padded strides
    static constexpr int kEt = D1 * D1 * kSt, kEp = D1 * kSp;                   // per element
@@ -81,17 +90,21 @@ struct Cfg3 {
    // computing warps as shared memory allows: 224 KB (vs 200) is +9 % at
    // p = 4 (6 -> 7 warps), neutral where the 11-warp cap or the warp size binds
    static constexpr int kT0 = static_cast<int>((224 * 1024) / kWarpBytes); // teams by smem
-   // warp cap from the registers ptxas needs: 11 (170 each) by default, 15
-   // (128) at p <= 2 with q <= p + 2 except p = 2, q = 4, 13 (146) at p = 3, q = 5
-   // QG (measured, 10M DOFs): p = 6, q = 8 four two-warp teams (254
-   // registers, +15 % over the group kernel; 12 warps -7 %); p = 7, q = 9
-   // four three-warp teams (168 registers, some spills: +8 %; 6 warps -11 %)
-   // (the register file is four 16K banks, one per scheduler: 9-12 warps
-   // per block cap a thread at 168 registers, <= 8 warps at 255.  BP3 p = 5,
-   // q = 7: three teams + producer (7 warps, no spills) +2 % over four teams
-   // at 168 registers with spills.)
-   static constexpr int kMaxW = QG ? (P == 6 ? 8 : 12)
-                              : (P == 5 && Q == 7 && KIND == TFEM_DIFFUSION) ? 6
+   // Warps per block: 11 by default, 15 at p <= 2 with q <= p + 2 except
+   // p = 2, q = 4, 13 at p = 3, q = 5 (what ptxas needs fits there).
+   // Measured, ~10M DOFs (the register file is four 16K
+   // banks, one per scheduler: 9-12 warps per block cap a thread at 168
+   // registers, <= 8 warps at 255):
+   //   QG q = 8 (BP3 p = 6, BP5 p = 7): four two-warp teams, 254 registers
+   //     (p = 6: +14 % over the group kernel; 12 warps -7 %);
+   //   QG BP3 p = 7: four three-warp teams (168 registers; two teams -12 %);
+   //   QG BP3 p = 8: two four-warp teams (+2 % over three);
+   //   QG BP5 p = 8: two three-warp teams (no spills, +29 % over three);
+   //   BP3 p = 5, q = 7 and BP5 p = 6, q = 7: three teams + producer (7
+   //     warps, no spills; +2 % and +17 % over four teams with spills);
+   //   BP5 p = 5: five teams (three: -16 %).
+   static constexpr int kMaxW = QG ? (P == 8 && Q == 10 ? 8 : P == 8 && Q == 9 ? 6 : Q == 8 ? 8 : 12)
+                              : ((P == 5 || P == 6) && Q == 7 && KIND == TFEM_DIFFUSION) ? 6
                               : KIND != TFEM_DIFFUSION ? 11
                               : (Q <= 3) ? 15 : (P == 3 && Q == 5) ? 13 : 11;
    static constexpr int kT1 = kT0 * WPE > kMaxW ? kMaxW / WPE : kT0;
@@ -133,11 +146,14 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
    auto *ws = reinterpret_cast<W *>(smem_raw);
    if (threadIdx.x == 0) {
-      for (int w = 0; w < kT; w++)
+      for (int w = 0; w < kT; w++) {
          for (int s = 0; s < kSlots; s++) {
             mbar_init(&ws[w].full[s], 1);
             mbar_init(&ws[w].empty[s], 1);
          }
+         if constexpr (W::SLAB)
+            for (int s = 0; s < W::kSlab; s++) mbar_init(&ws[w].sfull[s], Q * Q);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
    }
    __syncthreads();
@@ -232,6 +248,25 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             sm.es[i] = (a.ess_out == a.mask_in ? mk : (a.ess_out && bit_set(a.ess_out, d))) ? 1 : 0;
          }
          team_sync();
+         // SLAB: column thread pt's point factors of plane qz of this group go
+         // to slot (k q + qz) % kSlab; the first kSlab - 1 planes now, so the
+         // x stage below covers their latency
+         auto slab_issue = [&](int qz) {
+            if constexpr (W::SLAB) {
+               const int64_t t = k * Q + qz;
+               const int s = static_cast<int>(t % W::kSlab);
+               double *dst = sm.slab + s * NC * W::NTHq + pt;
+               const double *src = a.qdata + g * (int64_t)(NC * NQD) + pt + Q * Q * qz;
+#pragma unroll
+               for (int c = 0; c < NC; c++) gather8(dst + c * W::NTHq, src + c * NQD);
+               gather_arrive(&sm.sfull[s]);
+            }
+         };
+         if constexpr (W::SLAB) {
+            if (pt < Q * Q)
+#pragma unroll
+               for (int qz = 0; qz < W::kSlab - 1; qz++) slab_issue(qz);
+         }
          const int64_t gn = group(team, k + 1);
          load_map(group(team, k + 2), gnn); // two groups ahead: used a group later
          const double *V = sm.V[vb];
@@ -303,7 +338,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             double Dq[W::QG ? NC : 1][W::QG ? Q : 1];
             const double *qg = a.qdata + (g * EPW + (live ? ej : 0)) * (int64_t)(NC * NQD) + col;
             auto load_plane = [&](int qz) {
-               if constexpr (W::QG) {
+               if constexpr (W::QG && !W::SLAB) {
 #pragma unroll
                   for (int c = 0; c < NC; c++) Dq[c][qz] = __ldg(qg + c * NQD + Q * Q * qz);
                }
@@ -349,13 +384,21 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
             const double *qd = sm.q[s] + ej * NC * NQD;
             // point factor c at plane qz of this column
             auto D = [&](int c, int qz, int q) -> double {
-               if constexpr (W::QG) return Dq[c][qz];
+               if constexpr (W::SLAB)
+                  return sm.slab[((k * Q + qz) % W::kSlab) * NC * W::NTHq + c * W::NTHq + pt];
+               else if constexpr (W::QG) return Dq[c][qz];
                else return qd[c * NQD + q];
             };
 #pragma unroll
             for (int qz = 0; qz < Q; qz++) { // contract c, point factors, back over qz
                const int q = qx + Q * (qy + Q * qz);
-               if (qz + kR < Q) load_plane(qz + kR);
+               if constexpr (W::SLAB) {
+                  if (qz + W::kSlab - 1 < Q) slab_issue(qz + W::kSlab - 1);
+                  const int64_t t = k * Q + qz;
+                  mbar_wait(&sm.sfull[t % W::kSlab], static_cast<unsigned>((t / W::kSlab) & 1));
+               } else if (qz + kR < Q) {
+                  load_plane(qz + kR);
+               }
                // (qz, c) are compile-time here: table operands come from the
                // constant bank, not shared memory
                if (KIND == TFEM_MASS) {
@@ -606,12 +649,17 @@ KernelPick pick_kind(int p, int nq, int sm, bool co)
    case 3: return nq == 5 ? make<3, 5, KIND>(sm, co) : nq == 4 ? make<3, 4, KIND>(sm, co) : KernelPick{};
    case 4: return nq == 5 ? make<4, 5, KIND>(sm, co) : nq == 6 ? make<4, 6, KIND>(sm, co) : KernelPick{};
    case 5: return nq == 6 ? make<5, 6, KIND>(sm, co) : nq == 7 ? make<5, 7, KIND>(sm, co) : KernelPick{};
+   case 6: if (nq == 7) return make<6, 7, KIND>(sm, co); break; // BP5 p = 6
    }
-   // q >= 8, diffusion: QG where it measured faster than the group kernel
-   // (BP3 p = 6, 7; p = 8, BP5 p >= 7 and mass stay on the group kernel)
+   // q >= 8, diffusion (QG; measured against the group kernel at ~10M
+   // DOFs: BP3 p = 6 +14 %, p = 7 +33 %, p = 8 +32 %, BP5 p = 7 +70 %,
+   // p = 8 +38 %); mass stays on the group kernel
    if constexpr (KIND == TFEM_DIFFUSION) {
       if (p == 6 && nq == 8) return make<6, 8, KIND>(sm, co);
       if (p == 7 && nq == 9) return make<7, 9, KIND>(sm, co);
+      if (p == 7 && nq == 8) return make<7, 8, KIND>(sm, co);   // BP5 p = 7
+      if (p == 8 && nq == 9) return make<8, 9, KIND>(sm, co);   // BP5 p = 8
+      if (p == 8 && nq == 10) return make<8, 10, KIND>(sm, co);
    }
    return {};
 }

@@ -12,4 +12,4 @@ if [ $# -gt 0 ]; then
   exit 0
 fi
 for p in 2 3 4 5 6 7 8; do run --dim 3 --order $p; done
-for p in 2 4 5; do run --dim 3 --order $p --bp 5; done
+for p in 2 4 5 6 7 8; do run --dim 3 --order $p --bp 5; done
