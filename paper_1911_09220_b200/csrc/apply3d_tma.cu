@@ -52,14 +52,15 @@ struct alignas(16) Warp3 {
    // q >= 8 (QG): the point factors are read from global memory in the
    // column stage (planes prefetched into registers) -- double-buffering
    // nc q^3 doubles per element in shared memory would leave too few warps
-   static constexpr bool QG = Q >= 8;
+   // (and BP3 p = 5, q = 7: +15 % over the point-factor ring with three teams)
+   static constexpr bool QG = Q >= 8 || (P == 5 && Q == 7 && KIND == TFEM_DIFFUSION);
    static constexpr int kSlots = QG ? 1 : 2;
    double q[kSlots][QG ? 1 : EPW * NC * NQD];         // the group's point factors
    // QG slab ring: each column thread's point factors of kSlab qz planes in
    // flight (cp.async, completion on sfull[slot]); thread-private entries
    // (q >= 9: +23 % at BP3 p = 7 over the register prefetch; at q = 8 the
-   // register prefetch is 5 % faster)
-   static constexpr bool SLAB = QG && Q >= 9;
+   // register prefetch is 5 % faster with four teams, 8 % with six)
+   static constexpr bool SLAB = QG && Q != 8;
    static constexpr int kSlab = SLAB ? 4 : 1;
    static constexpr int NTHq = 32 * ((Q * Q + 31) / 32 < 4 ? (Q * Q + 31) / 32 : 4);
    double slab[SLAB ? kSlab * NC * NTHq : 1]; // [slot][c][thread]
@@ -100,11 +101,12 @@ struct Cfg3 {
    //   QG BP3 p = 7: four three-warp teams (168 registers; two teams -12 %);
    //   QG BP3 p = 8: two four-warp teams (+2 % over three);
    //   QG BP5 p = 8: two three-warp teams (no spills, +29 % over three);
-   //   BP3 p = 5, q = 7 and BP5 p = 6, q = 7: three teams + producer (7
-   //     warps, no spills; +2 % and +17 % over four teams with spills);
+   //   QG BP3 p = 5 (q = 7): six two-warp teams, slab ring;
+   //   BP5 p = 6, q = 7: three teams + producer (7 warps, no spills; +17 %
+   //     over four teams with spills);
    //   BP5 p = 5: five teams (three: -16 %).
    static constexpr int kMaxW = QG ? (P == 8 && Q == 10 ? 8 : P == 8 && Q == 9 ? 6 : Q == 8 ? 8 : 12)
-                              : ((P == 5 || P == 6) && Q == 7 && KIND == TFEM_DIFFUSION) ? 6
+                              : (P == 6 && Q == 7 && KIND == TFEM_DIFFUSION) ? 6
                               : KIND != TFEM_DIFFUSION ? 11
                               : (Q <= 3) ? 15 : (P == 3 && Q == 5) ? 13 : 11;
    static constexpr int kT1 = kT0 * WPE > kMaxW ? kMaxW / WPE : kT0;
