@@ -23,7 +23,7 @@ full elem3d_p3 apply3d_tma --dim 3 --order 3
 full elem3d_p5 apply3d_tma --dim 3 --order 5
 full elem3d_p6_qg apply3d_tma --dim 3 --order 6
 full elem3d_p7_qg apply3d_tma --dim 3 --order 7
-full elem3d_p8 apply3d_kernel --dim 3 --order 8
+full elem3d_p8_qg apply3d_tma --dim 3 --order 8
 full elem2d_bp5_p4 apply2d_hi --dim 2 --order 4 --bp 5
 full elem3d_bp5_p4 apply3d_tma --dim 3 --order 4 --bp 5
 du -sh $O; ls -la $O/${T}_*
