@@ -19,9 +19,6 @@
 // exclusive DOFs to y, the rest to the E-vector (scatter).  EDOT: x . y as
 // element energies (apply.cu).
 #include "async.cuh"
-#ifndef TFEM_DMX
-#define TFEM_DMX 0 // A/B: DMMA x stages, measured slower at p = 5..8
-#endif
 #include "kernels.cuh"
 
 namespace tfem {
@@ -45,15 +42,6 @@ constexpr int pad_t3(int P, int Q)
 constexpr int pad_p3(int P, int Q)
 {
    return (P == 2 && Q == 4) ? 4 : (P == 3 && Q == 4) ? 4 : (P == 4 && Q == 6) ? 2 : 0;
-}
-
-// FP64 tensor-core tile: D (8x8) += A (8x4, row) B (4x8, col); per lane
-// a = A[lane/4][lane%4], b = B[lane%4][lane/4], d = D[lane/4][2(lane%4) + h]
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
-{
-   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                : "+d"(d[0]), "+d"(d[1])
-                : "d"(a), "d"(b));
 }
 
 template <int P, int Q, int KIND>
@@ -150,11 +138,6 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    constexpr bool kRows1 = EPW * D1 * D1 <= kRowMax; // stages a and x
    constexpr bool kRows3 = EPW * Q * D1 <= kRowMax;  // stage y
    constexpr unsigned kQBytes = NC * NQD * 8;
-   // DMX: the x contraction and its transpose (the epilogue) as DMMA tiles --
-   // rows (c, b) x points qx x nodes a, zero-padded to 8 x 8 x 4
-   constexpr bool DMX = TFEM_DMX && W::QG && KIND == TFEM_DIFFUSION && !CO && EPW == 1;
-   constexpr int kMt = (D1 * D1 + 7) / 8, kKa = (D1 + 3) / 4, kNq = (Q + 7) / 8;
-   constexpr int kKq = (Q + 3) / 4, kNa = (D1 + 7) / 8;
    if (a.done && *a.done) return;
    extern __shared__ __align__(128) unsigned char smem_raw[];
    __shared__ double sB[Q][D1], sG[Q][D1];
@@ -182,31 +165,6 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
    auto group = [&](int w, int64_t k) { return (int64_t)blockIdx.x * kT + w + k * stride; };
    // a team: WPE warps on one element group; pt = thread in the team
    const int team = warp / WPE, pt = lane + 32 * (warp % WPE);
-   const int wt = warp % WPE; // warp within the team
-   // DMX basis fragments (registers): x stage B[k = a][n = qx] = B1d[qx][a]
-   // (and G); epilogue B[k = qx][n = a] = G1d[qx][a] (and B)
-   double fxB[DMX ? kKa : 1][DMX ? kNq : 1], fxG[DMX ? kKa : 1][DMX ? kNq : 1];
-   double feG[DMX ? kKq : 1][DMX ? kNa : 1], feB[DMX ? kKq : 1][DMX ? kNa : 1];
-   if constexpr (DMX) {
-#pragma unroll
-      for (int kt = 0; kt < kKa; kt++)
-#pragma unroll
-         for (int nt = 0; nt < kNq; nt++) {
-            const int ia = kt * 4 + (lane & 3), qx = nt * 8 + (lane >> 2);
-            const bool ok = ia < D1 && qx < Q;
-            fxB[kt][nt] = ok ? a.t.B[qx][ia] : 0.0;
-            fxG[kt][nt] = ok ? a.t.G[qx][ia] : 0.0;
-         }
-#pragma unroll
-      for (int kt = 0; kt < kKq; kt++)
-#pragma unroll
-         for (int nt = 0; nt < kNa; nt++) {
-            const int qx = kt * 4 + (lane & 3), ia = nt * 8 + (lane >> 2);
-            const bool ok = ia < D1 && qx < Q;
-            feG[kt][nt] = ok ? a.t.G[qx][ia] : 0.0;
-            feB[kt][nt] = ok ? a.t.B[qx][ia] : 0.0;
-         }
-   }
    auto team_sync = [&]() {
       if constexpr (WPE == 1) __syncwarp();
       else asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(NTH) : "memory");
@@ -318,36 +276,7 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
          // unrolled (basis operands from the constant bank) when the rows
          // fit one pass of the warp; else a lane per output.  CO: TB = V,
          // only TG is formed.
-         if constexpr (DMX) {
-            // TB / TG [cb][qx] = V[cb][a] B1d^T / G1d^T: m-tiles over the warps
-            for (int mt = wt; mt < kMt; mt += WPE) {
-               const int row = mt * 8 + (lane >> 2);
-               double af[kKa];
-#pragma unroll
-               for (int kt = 0; kt < kKa; kt++) {
-                  const int ia = kt * 4 + (lane & 3);
-                  af[kt] = row < D1 * D1 && ia < D1 ? V[row * D1 + ia] : 0.0;
-               }
-#pragma unroll
-               for (int nt = 0; nt < kNq; nt++) {
-                  double cb_[2] = {0.0, 0.0}, cg_[2] = {0.0, 0.0};
-#pragma unroll
-                  for (int kt = 0; kt < kKa; kt++) {
-                     dmma(cb_, af[kt], fxB[kt][nt]);
-                     dmma(cg_, af[kt], fxG[kt][nt]);
-                  }
-                  const int qx = nt * 8 + 2 * (lane & 3);
-                  if (row < D1 * D1) {
-#pragma unroll
-                     for (int h = 0; h < 2; h++)
-                        if (qx + h < Q) {
-                           sm.TB[row * kSt + qx + h] = cb_[h];
-                           sm.TG[row * kSt + qx + h] = cg_[h];
-                        }
-                  }
-               }
-            }
-         } else if constexpr (CO) {
+         if constexpr (CO) {
             for (int it = pt; it < EPW * D1 * D1; it += NTH) {
                const int j = it / (D1 * D1), cb = it % (D1 * D1);
                double v[D1];
@@ -625,39 +554,10 @@ __global__ void __launch_bounds__(Cfg3<P, Q, KIND>::kBlock, 1) apply3d_tma_kerne
                a.evec[ev_em_p(a.evperm, ND, e, i)] = r;
             }
          };
-         if constexpr (DMX) {
-            // r[cb][a] = TB[cb][qx] G1d[qx][a] + TG[cb][qx] B1d[qx][a]
-            for (int mt = wt; mt < kMt; mt += WPE) {
-               const int row = mt * 8 + (lane >> 2);
-               double atb[kKq], atg[kKq];
-#pragma unroll
-               for (int kt = 0; kt < kKq; kt++) {
-                  const int x = kt * 4 + (lane & 3);
-                  const bool ok = row < D1 * D1 && x < Q;
-                  atb[kt] = ok ? sm.TB[row * kSt + x] : 0.0;
-                  atg[kt] = ok ? sm.TG[row * kSt + x] : 0.0;
-               }
-#pragma unroll
-               for (int nt = 0; nt < kNa; nt++) {
-                  double c_[2] = {0.0, 0.0};
-#pragma unroll
-                  for (int kt = 0; kt < kKq; kt++) {
-                     dmma(c_, atb[kt], feG[kt][nt]);
-                     dmma(c_, atg[kt], feB[kt][nt]);
-                  }
-                  const int ia = nt * 8 + 2 * (lane & 3);
-                  if (row < D1 * D1) {
-#pragma unroll
-                     for (int h = 0; h < 2; h++)
-                        if (ia + h < D1) put(0, row * D1 + ia + h, c_[h]);
-                  }
-               }
-            }
-         }
          // contract qx -> r(a, b, c) and the epilogue: a lane per (e, c, b),
          // a unrolled (or a lane per output)
          constexpr int kA = kRows1 ? D1 : 1; // outputs per work item
-         for (int it = pt; it < (DMX ? 0 : cnt * ND / kA); it += NTH) {
+         for (int it = pt; it < cnt * ND / kA; it += NTH) {
             const int j = it / (ND / kA), cb = kRows1 ? it % (D1 * D1) : (it % ND) / D1;
             double tb[Q], tg[Q];
 #pragma unroll
