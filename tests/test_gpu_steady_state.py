@@ -231,9 +231,13 @@ def test_cg_iterations_3d_wrapped(capped, p):
 
 
 @pytest.mark.parametrize("capped", [("fma", 2)], indirect=True)
-@pytest.mark.parametrize("p", [2, 4, 6])
+@pytest.mark.parametrize("p", [2, 4, 6, 7, 8])
 def test_cg_iterations_3d_bp5_wrapped(capped, p):
-    n = {2: 10, 4: 7, 6: 6}[p]
+    # p = 8 at n = 5 stops one iteration before the restatement (263 vs 264:
+    # the device's relative residual 9.83e-11 crosses the 1e-10 threshold
+    # within FMA-vs-reference rounding); n = 4 stays clear of the threshold.
+    # The p = 8 operator itself is checked at 1e-12 in test_3d_bp5_n24.
+    n = {2: 10, 4: 7, 6: 6, 7: 5, 8: 4}[p]
     _cg_3d(capped, (n, n, n), p, "diffusion", "gll", True, seed=30 + p)
 
 
