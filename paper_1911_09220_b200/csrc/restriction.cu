@@ -410,7 +410,7 @@ void sort_rows_by_first_slot(tfem_ctx *ctx, tfem_restriction::Bucket &bk)
 struct Partner {
    int lane_off, i; // member lane = owner lane - lane_off, local index i
 };
-int warp_partners(int p, int a, int b, int c, int r, Partner *out)
+__host__ __device__ int warp_partners(int p, int a, int b, int c, int r, Partner *out)
 {
    const int D1 = p + 1;
    int n = 0;
@@ -432,58 +432,81 @@ int warp_partners(int p, int a, int b, int c, int r, Partner *out)
    return n;
 }
 
+// One thread per bucket row (sorted by element): flag a warp-local DOF's
+// slots in place (members, owner = the last slot) when its slots share one
+// patch and the owner's partner rule lists exactly the others; global[k] = 1
+// for every other row (it stays with the scatter).
+__global__ void warp_local_kernel(uint32_t *gmap, Layout L, int p, const uint32_t *slots,
+                                  int64_t n, int c, int32_t *global)
+{
+   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (k >= n) return;
+   constexpr int W = 32;
+   const int D1 = p + 1;
+   const uint32_t *row = slots + k * c;
+   const int64_t w0 = L.elem_of(row[0]) / W;
+   bool local = true;
+   for (int j = 1; j < c && local; j++) local = L.elem_of(row[j]) / W == w0;
+   if (local) {
+      const uint32_t os = row[c - 1];
+      const int64_t opos = L.elem_of(os);
+      const int oi = L.local_of(os), lane = static_cast<int>(opos % W);
+      Partner pt[4];
+      const int m = warp_partners(p, oi % D1, oi / D1, lane % 8, lane / 8, pt);
+      local = m == c - 1;
+      for (int j = 0; j < m && local; j++)
+         local = row[j] == static_cast<uint32_t>(L.slot(pt[j].i, opos - pt[j].lane_off));
+   }
+   if (local) {
+      for (int j = 0; j + 1 < c; j++) gmap[row[j]] |= kWarpMember;
+      gmap[row[c - 1]] |= kWarpOwner;
+   }
+   global[k] = local ? 0 : 1;
+}
+
+// Copy the flagged rows (dofs + c slots) to their scanned positions.
+__global__ void compact_rows_kernel(const int32_t *global, const int32_t *at, int64_t n, int c,
+                                    const int32_t *dofs, const uint32_t *slots, int32_t *gdofs,
+                                    uint32_t *gslots)
+{
+   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+   if (k >= n || !global[k]) return;
+   const int64_t to = at[k];
+   gdofs[to] = dofs[k];
+   for (int j = 0; j < c; j++) gslots[to * c + j] = slots[k * c + j];
+}
+
 void build_warp_local(tfem_restriction *r, const Layout &L)
 {
-   cudaStream_t s = r->ctx->stream;
-   constexpr int W = 32;
-   const int p = r->p, D1 = p + 1;
-   std::vector<uint32_t> gmap(static_cast<size_t>(r->nd) * r->ne_pad);
-   d2h(s, gmap.data(), r->gmap, sizeof(uint32_t) * gmap.size());
-   std::vector<int32_t> gd[tfem_restriction::kMaxBuckets];
-   std::vector<uint32_t> gs[tfem_restriction::kMaxBuckets];
+   tfem_ctx *ctx = r->ctx;
+   cudaStream_t s = ctx->stream;
    for (int b = 0; b < r->n_buckets; b++) {
       const auto &bk = r->buckets[b];
-      const int c = bk.c;
-      std::vector<int32_t> dofs(static_cast<size_t>(bk.n));
-      std::vector<uint32_t> slots(static_cast<size_t>(bk.n) * c);
-      d2h(s, dofs.data(), bk.dofs, sizeof(int32_t) * dofs.size());
-      d2h(s, slots.data(), bk.slots, sizeof(uint32_t) * slots.size());
-      for (int64_t k = 0; k < bk.n; k++) {
-         const uint32_t *row = &slots[static_cast<size_t>(k) * c];
-         const int64_t w0 = L.elem_of(row[0]) / W;
-         bool local = true;
-         for (int j = 1; j < c && local; j++) local = L.elem_of(row[j]) / W == w0;
-         if (local) {
-            // row is sorted by element: the owner is the last slot
-            const uint32_t os = row[c - 1];
-            const int64_t opos = L.elem_of(os);
-            const int oi = L.local_of(os), lane = static_cast<int>(opos % W);
-            Partner pt[4];
-            const int n = warp_partners(p, oi % D1, oi / D1, lane % 8, lane / 8, pt);
-            local = n == c - 1;
-            for (int j = 0; j < n && local; j++)
-               local = row[j] == static_cast<uint32_t>(L.slot(pt[j].i, opos - pt[j].lane_off));
-         }
-         if (local) {
-            for (int j = 0; j + 1 < c; j++) gmap[row[j]] |= kWarpMember;
-            gmap[row[c - 1]] |= kWarpOwner;
-         } else {
-            gd[b].push_back(dofs[k]);
-            gs[b].insert(gs[b].end(), row, row + c);
-         }
+      if (bk.n == 0) continue;
+      int32_t *global = dalloc<int32_t>(bk.n), *at = dalloc<int32_t>(bk.n);
+      warp_local_kernel<<<blocks_for(bk.n), kThreads, 0, s>>>(r->gmap, L, r->p, bk.slots, bk.n,
+                                                             bk.c, global);
+      ctx->launched();
+      exclusive_scan(ctx, global, at, bk.n);
+      int32_t last_at = 0, last_g = 0;
+      d2h(s, &last_at, at + bk.n - 1, 4);
+      d2h(s, &last_g, global + bk.n - 1, 4);
+      const int64_t m = static_cast<int64_t>(last_at) + last_g;
+      if (m > 0) {
+         auto &g = r->gbuckets[r->n_gbuckets++];
+         g.c = bk.c;
+         g.n = m;
+         g.dofs = dalloc<int32_t>(m);
+         g.slots = dalloc<uint32_t>(m * g.c);
+         compact_rows_kernel<<<blocks_for(bk.n), kThreads, 0, s>>>(global, at, bk.n, bk.c, bk.dofs,
+                                                                  bk.slots, g.dofs, g.slots);
+         ctx->launched();
+         r->n_gshared += m;
       }
-   }
-   h2d(s, r->gmap, gmap.data(), sizeof(uint32_t) * gmap.size());
-   for (int b = 0; b < r->n_buckets; b++) {
-      if (gd[b].empty()) continue;
-      auto &g = r->gbuckets[r->n_gbuckets++];
-      g.c = r->buckets[b].c;
-      g.n = static_cast<int64_t>(gd[b].size());
-      g.dofs = dalloc<int32_t>(g.n);
-      g.slots = dalloc<uint32_t>(g.n * g.c);
-      h2d(s, g.dofs, gd[b].data(), sizeof(int32_t) * gd[b].size());
-      h2d(s, g.slots, gs[b].data(), sizeof(uint32_t) * gs[b].size());
-      r->n_gshared += g.n;
+      TFEM_CUDA(cudaGetLastError());
+      TFEM_CUDA(cudaStreamSynchronize(s));
+      cudaFree(global);
+      cudaFree(at);
    }
    r->warp_local = true;
 }
