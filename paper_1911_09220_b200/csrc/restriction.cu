@@ -399,7 +399,7 @@ void sort_rows_by_first_slot(tfem_ctx *ctx, tfem_restriction::Bucket &bk)
       cudaFree(p);
 }
 
-// Warp-local DOFs of an ordered space (host side, once per space).  A
+// Warp-local DOFs of an ordered space (on the device, once per space).  A
 // shared DOF is warp-local when all its slots lie in one warp patch (32
 // positions, lane = 8 r + c); its slot of the highest element is the owner
 // (kWarpOwner), the others members.  The kernel finds an owner's members by
