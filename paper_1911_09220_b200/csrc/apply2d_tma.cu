@@ -31,10 +31,16 @@ namespace tfem {
 namespace {
 
 
-constexpr int kCompute = 7;                 // compute warps per block (8 warps of 255
-                                            // registers fill the register file)
-constexpr int kTile = 32 * kCompute;        // elements per tile
-constexpr int kBlock = 32 * (kCompute + 1); // + the producer warp
+// Compute warps per block: 7 at p = 3 (8 warps of 254 registers fill the
+// register file); where ptxas needs fewer, more warps per SM (the register
+// file is four 16K banks, one per scheduler): p = 2 eleven (168 registers,
+// +5 % over 7), p = 1 fifteen (~120 registers, +12 %).
+template <int P>
+struct TileCfg {
+   static constexpr int kCompute = P == 1 ? 15 : P == 2 ? 11 : 7;
+   static constexpr int kTile = 32 * kCompute;        // elements per tile
+   static constexpr int kBlock = 32 * (kCompute + 1); // + the producer warp
+};
 
 template <int P, int Q, int KIND, bool EXACT>
 struct TileSmem {
@@ -50,15 +56,15 @@ struct TileSmem {
    static constexpr int kStages = kDeep ? 5 : 4; // qdata slice ring
    static constexpr int kXb = kDeep ? 1 : 2;     // x buffers
    static constexpr int kMaps = 3; // the open tile's map stays until its epilogue
-   double q[kStages][SLICE][kTile];
-   uint32_t gmap[kMaps][ND][kTile];
-   uint32_t gess[kMaps][kTile];  // a.elem_ess words of the tile (when given)
-   double xs[kXb][ND][kTile];    // x of the open / next tile [i][lane]
-   uint32_t essm[kTile];         // per lane: slots whose DOF is essential (ess_out)
+   double q[kStages][SLICE][TileCfg<P>::kTile];
+   uint32_t gmap[kMaps][ND][TileCfg<P>::kTile];
+   uint32_t gess[kMaps][TileCfg<P>::kTile];  // a.elem_ess words of the tile (when given)
+   double xs[kXb][ND][TileCfg<P>::kTile];    // x of the open / next tile [i][lane]
+   uint32_t essm[TileCfg<P>::kTile];         // per lane: slots whose DOF is essential (ess_out)
    uint64_t full[kStages];  // slice landed (tx count)
-   uint64_t empty[kStages]; // slice consumed (kCompute arrivals)
+   uint64_t empty[kStages]; // slice consumed (TileCfg<P>::kCompute arrivals)
    uint64_t gfull[kMaps], gempty[kMaps];
-   uint64_t xfull[kXb];     // a tile's gathers landed (kTile lane arrivals)
+   uint64_t xfull[kXb];     // a tile's gathers landed (TileCfg<P>::kTile lane arrivals)
 };
 
 // Issue qdata slice `k` of this block (tile lt = k / Q, qy = k % Q).
@@ -71,10 +77,10 @@ __device__ __forceinline__ void issue_slice(TileSmem<P, Q, KIND, EXACT> &sm, con
    const int qy = static_cast<int>(k % Q);
    const int64_t t = blockIdx.x + lt * gridDim.x;
    if (t >= ntiles) return;
-   const int64_t e0 = t * kTile;
+   const int64_t e0 = t * TileCfg<P>::kTile;
    // whole 224-element runs except the last tile (ne_pad: multiple of 64)
    const int64_t avail = a.ne_pad - e0;
-   const unsigned bytes = static_cast<unsigned>(avail < kTile ? avail : kTile) * 8u;
+   const unsigned bytes = static_cast<unsigned>(avail < TileCfg<P>::kTile ? avail : TileCfg<P>::kTile) * 8u;
    constexpr int kStages = TileSmem<P, Q, KIND, EXACT>::kStages;
    const int s = static_cast<int>(k % kStages);
    mbar_expect_tx(&sm.full[s], bytes * SLICE);
@@ -93,9 +99,9 @@ __device__ __forceinline__ void issue_gmap(TileSmem<P, Q, KIND, EXACT> &sm, cons
    constexpr int ND = (P + 1) * (P + 1);
    const int64_t t = blockIdx.x + lt * gridDim.x;
    if (t >= ntiles) return;
-   const int64_t e0 = t * kTile;
+   const int64_t e0 = t * TileCfg<P>::kTile;
    const int64_t avail = a.ne_pad - e0;
-   const unsigned bytes = static_cast<unsigned>(avail < kTile ? avail : kTile) * 4u;
+   const unsigned bytes = static_cast<unsigned>(avail < TileCfg<P>::kTile ? avail : TileCfg<P>::kTile) * 4u;
    const int b = static_cast<int>(lt % TileSmem<P, Q, KIND, EXACT>::kMaps);
    const unsigned ebytes = a.elem_ess ? bytes : 0u; // elem_ess: ne_pad words
    mbar_expect_tx(&sm.gfull[b], bytes * ND + ebytes);
@@ -110,7 +116,7 @@ __device__ __forceinline__ void issue_gmap(TileSmem<P, Q, KIND, EXACT> &sm, cons
 template <int P, int Q, bool EXACT, bool FIRST, bool EN>
 __device__ __forceinline__ void diffusion_slice(const ApplyArgs &a, int qy, const double (&T1)[Q][P + 1],
                                                 const double (&T2)[Q][P + 1],
-                                                const double (*qs)[kTile], int tid,
+                                                const double (*qs)[TileCfg<P>::kTile], int tid,
                                                 double (&vx)[P + 1][P + 1],
                                                 double (&vy)[P + 1][P + 1], double &en, bool live)
 {
@@ -157,7 +163,7 @@ template <int P, int Q, bool FIRST, bool EN>
 __device__ __forceinline__ void diffusion_slice_fused(const ApplyArgs &a, int qy,
                                                       const double (&T1)[Q][P + 1],
                                                       const double (&T2)[Q][P + 1],
-                                                      const double (*qs)[kTile], int tid,
+                                                      const double (*qs)[TileCfg<P>::kTile], int tid,
                                                       double (&R)[P + 1][P + 1], double &en, bool live)
 {
    constexpr int D1 = P + 1;
@@ -194,7 +200,7 @@ __device__ __forceinline__ void diffusion_slice_fused(const ApplyArgs &a, int qy
 
 template <int P, int Q, bool EXACT, bool FIRST, bool EN>
 __device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const double (&T)[Q][P + 1],
-                                           const double (*qs)[kTile], int tid,
+                                           const double (*qs)[TileCfg<P>::kTile], int tid,
                                            double (&R)[P + 1][P + 1], double &en, bool live)
 {
    constexpr int D1 = P + 1;
@@ -220,7 +226,7 @@ __device__ __forceinline__ void mass_slice(const ApplyArgs &a, int qy, const dou
 
 // EDOT: x . y as the sum of element energies (a.energy_dot; apply.cu).
 template <int P, int Q, int KIND, bool EXACT, bool EDOT>
-__global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs a)
+__global__ void __launch_bounds__(TileCfg<P>::kBlock, 1) apply2d_tma_kernel(const ApplyArgs a)
 {
    using Smem = TileSmem<P, Q, KIND, EXACT>;
    constexpr int D1 = P + 1, ND = D1 * D1;
@@ -230,25 +236,25 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
    auto &sm = *reinterpret_cast<Smem *>(smem_raw);
    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
    const int tid = threadIdx.x; // element slot inside the tile (compute warps)
-   const int64_t ntiles = (a.ne + kTile - 1) / kTile;
+   const int64_t ntiles = (a.ne + TileCfg<P>::kTile - 1) / TileCfg<P>::kTile;
    const int64_t my_tiles =
       blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
    if (threadIdx.x == 0) {
       for (int s = 0; s < kStages; s++) {
          mbar_init(&sm.full[s], 1);
-         mbar_init(&sm.empty[s], kCompute);
+         mbar_init(&sm.empty[s], TileCfg<P>::kCompute);
       }
       for (int b = 0; b < Smem::kMaps; b++) {
          mbar_init(&sm.gfull[b], 1);
-         mbar_init(&sm.gempty[b], kCompute);
+         mbar_init(&sm.gempty[b], TileCfg<P>::kCompute);
       }
-      for (int b = 0; b < Smem::kXb; b++) mbar_init(&sm.xfull[b], kTile);
+      for (int b = 0; b < Smem::kXb; b++) mbar_init(&sm.xfull[b], TileCfg<P>::kTile);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
    }
    __syncthreads();
-   auto tile_elem = [&](int64_t lt) { return (blockIdx.x + lt * gridDim.x) * kTile + tid; };
+   auto tile_elem = [&](int64_t lt) { return (blockIdx.x + lt * gridDim.x) * TileCfg<P>::kTile + tid; };
    double dot = 0.0;
-   if (warp == kCompute) {
+   if (warp == TileCfg<P>::kCompute) {
       // ---------------------------------------------------------- producer
       // map(lt + 1) goes out before tile lt's slices (exact numerics gather
       // the next tile's x during tile lt).
@@ -274,7 +280,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
    } else {
    // ---------------------------------------------------------- consumers
    int64_t k = 0; // slice counter
-   auto acquire = [&]() -> const double(*)[kTile] {
+   auto acquire = [&]() -> const double(*)[TileCfg<P>::kTile] {
       const int s = static_cast<int>(k % kStages);
       mbar_wait(&sm.full[s], static_cast<unsigned>((k / kStages) & 1));
       return sm.q[s];
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
          const uint32_t mw = live ? sm.gess[gb][tid] : 0u;
 #pragma unroll
          for (int i = 0; i < ND; i++) {
-            const double v = live ? xs[i * kTile + tid] : 0.0;
+            const double v = live ? xs[i * TileCfg<P>::kTile + tid] : 0.0;
             V[i % D1][i / D1] = (mw >> i) & 1u ? 0.0 : v;
          }
          if (ess_is_mask) {
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
 #pragma unroll
          for (int i = 0; i < ND; i++) {
             const uint32_t d = sm.gmap[gb][i][tid] & kDofMask;
-            double v = live ? xs[i * kTile + tid] : 0.0;
+            double v = live ? xs[i * TileCfg<P>::kTile + tid] : 0.0;
             const bool m = a.mask_in && live && bit_set(a.mask_in, d);
             const bool es = ess_is_mask ? m : live && a.ess_out && bit_set(a.ess_out, d);
             essm |= static_cast<uint32_t>(es) << i;
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(kBlock, 1) apply2d_tma_kernel(const ApplyArgs 
    } // consumers
    if (a.dot) {
       const double v[1] = {dot};
-      emit<kBlock, 1>(a.dot, v);
+      emit<TileCfg<P>::kBlock, 1>(a.dot, v);
    }
 }
 
@@ -502,10 +508,10 @@ void launch(const ApplyArgs &a, cudaStream_t s, unsigned grid)
    static_assert(sizeof(TileSmem<P, Q, KIND, EXACT>) <= 227 * 1024, "shared memory budget");
    if (a.energy_dot) {
       max_dynamic_smem((const void *)apply2d_tma_kernel<P, Q, KIND, EXACT, true>, smem);
-      apply2d_tma_kernel<P, Q, KIND, EXACT, true><<<grid, kBlock, smem, s>>>(a);
+      apply2d_tma_kernel<P, Q, KIND, EXACT, true><<<grid, TileCfg<P>::kBlock, smem, s>>>(a);
    } else {
       max_dynamic_smem((const void *)apply2d_tma_kernel<P, Q, KIND, EXACT, false>, smem);
-      apply2d_tma_kernel<P, Q, KIND, EXACT, false><<<grid, kBlock, smem, s>>>(a);
+      apply2d_tma_kernel<P, Q, KIND, EXACT, false><<<grid, TileCfg<P>::kBlock, smem, s>>>(a);
    }
 }
 
@@ -536,8 +542,8 @@ KernelPick pick_apply2d_tma(int p, int nq, int kind, bool exact, int sm_count)
    KernelPick k;
    k.launch = kind == TFEM_MASS ? pick_p<TFEM_MASS>(p, nq, exact)
                                 : pick_p<TFEM_DIFFUSION>(p, nq, exact);
-   k.elems_per_block = kTile;
-   k.threads = kBlock;
+   k.elems_per_block = p == 1 ? TileCfg<1>::kTile : p == 2 ? TileCfg<2>::kTile : TileCfg<3>::kTile;
+   k.threads = p == 1 ? TileCfg<1>::kBlock : p == 2 ? TileCfg<2>::kBlock : TileCfg<3>::kBlock;
    k.persistent_blocks = sm_count;
    k.warp_reduce = true;
    k.energy_dot = true;
