@@ -1,10 +1,11 @@
-// K2, 2D p <= 3: the thread-per-element sum factorisation of apply2d_reg.cu
-// fed by an asynchronous bulk-copy pipeline (sm_90+ cp.async.bulk + mbarrier;
-// SASS UBLKCP, LDGSTS).
+// K2, 2D p <= 3: a thread-per-element sum factorisation (every stage in
+// registers) fed by an asynchronous bulk-copy pipeline (sm_90+
+// cp.async.bulk + mbarrier; SASS UBLKCP, LDGSTS).
 //
-// Warp-specialised persistent kernel, one block of 8 warps per SM: warps 0-6
-// compute (one element per lane; a tile is 224 consecutive element positions,
-// seven 8 x 4 warp patches in ElemOrder), warp 7 is the producer.  A tile's
+// Warp-specialised persistent kernel, one block per SM: kCompute computing
+// warps (7 at p = 3, 11 at p = 2, 15 at p = 1: TileCfg) with one element per
+// lane -- a tile is 32 kCompute consecutive element positions, that many
+// 8 x 4 warp patches in ElemOrder -- and one producer warp.  A tile's
 // qdata is streamed as Q "slices" (one per qy: the nc*Q planes (c, qy, qx),
 // each a contiguous 1792 B run of the [(c*nqd+q)][ne_pad] layout) through a
 // 4- or 5-deep ring of shared-memory stages, and the element map (D1^2 planes)
