@@ -79,7 +79,7 @@ __device__ __forceinline__ void issue_slice(TileSmem<P, Q, KIND, EXACT> &sm, con
    const int64_t t = blockIdx.x + lt * gridDim.x;
    if (t >= ntiles) return;
    const int64_t e0 = t * TileCfg<P>::kTile;
-   // whole 224-element runs except the last tile (ne_pad: multiple of 64)
+   // whole tile runs except the last tile (ne_pad: multiple of 64)
    const int64_t avail = a.ne_pad - e0;
    const unsigned bytes = static_cast<unsigned>(avail < TileCfg<P>::kTile ? avail : TileCfg<P>::kTile) * 8u;
    constexpr int kStages = TileSmem<P, Q, KIND, EXACT>::kStages;
