@@ -85,6 +85,7 @@ struct Cfg2 {
    // 200M DOFs; 15 -1 %)
    static constexpr int kMaxW = (kDiff && Q == 6 && (P == 4 || P == 5)) ? 15
                               : (kDiff && CO && P == 4 && Q == 5) ? 13
+                              : (kDiff && CO && P == 7) ? 7 // BP5 p = 7: 255 registers, no spills: +2.5 %
                               : (kDiff && !EXACT && P == 7 && Q == 9) ? 13
                               : 11;
    static constexpr int kW0 = static_cast<int>((224 * 1024) / kWarpBytes);

@@ -114,7 +114,7 @@ def test_2d_high_order_n300(p, numerics):
         dev.close()
 
 
-@pytest.mark.parametrize("p", [4, 8])
+@pytest.mark.parametrize("p", [4, 7, 8])
 def test_2d_high_order_mass_and_bp5(dev_fma, p):
     _check_operator(dev_fma, (300, 300), p, "mass", False, seed=3)
     _check_operator(dev_fma, (300, 300), p, "diffusion", False, rule="gll", seed=4)
